@@ -1,0 +1,152 @@
+"""Oracle pins for the fused greedy decisions (§2.3), CPU only.
+
+Special cases that reduce to library routines (lambda = 0 -> numpy argmax /
+plain greedy CTC collapse), invariants (blank retention, repeat rule) and
+hand-computed constructed cases on the Fig. 1 LM whose LM values are exact
+fractions (tests/golden/fig1_rows.txt).
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import AED, CTC, RNNT, Oracle
+
+
+@pytest.fixture(scope="module")
+def tri(small_lms):
+    f = small_lms["tri64"]
+    return Oracle(f.arpa, vocab_size=f.vocab_size), f
+
+
+@pytest.fixture(scope="module")
+def fig1(fig1_paths):
+    return Oracle(*fig1_paths)
+
+
+def test_lambda0_is_plain_argmax(tri):
+    o, f = tri
+    sents = synth.read_sentences(f.heldout)
+    x = synth.rnnt_logits(B=64, steps=4, V=o.V, seed=4).reshape(-1, o.V + 1)
+    # force several exact ties at the max
+    x[::7, 3] = x[::7].max(axis=1)
+    states = synth.uniform_states(o.num_states, x.shape[0], seed=3)
+    for mode in (RNNT, AED):
+        tok, st, _ = o.fused_step(mode, x, states, lam=0.0)
+        assert (tok == np.argmax(x, axis=1)).all()          # numpy: first max wins
+    tok, st, pv = o.fused_step(CTC, x, states, prev=np.full(x.shape[0], -1), lam=0.0)
+    assert (tok == np.argmax(x, axis=1)).all()
+
+
+def ctc_decode(o, logits, lam, start):
+    """Frame loop over the oracle's fused step; returns emitted tokens per row."""
+    B, T, _ = logits.shape
+    st = np.full(B, start, dtype=np.int32)
+    pv = np.full(B, -1, dtype=np.int32)
+    out = [[] for _ in range(B)]
+    adv = np.zeros(B, dtype=np.int64)
+    frames = []
+    for t in range(T):
+        old_pv, old_st = pv.copy(), st.copy()
+        tok, st, pv = o.fused_step(CTC, logits[:, t], st, prev=pv, lam=lam)
+        frames.append(tok)
+        for b in range(B):
+            if tok[b] != o.V and tok[b] != old_pv[b]:
+                out[b].append(int(tok[b]))
+            adv[b] += int(st[b] != old_st[b] or (tok[b] != o.V and tok[b] != old_pv[b]))
+    return out, np.stack(frames, 1), adv
+
+
+def test_ctc_lambda0_is_greedy_collapse(tri):
+    o, f = tri
+    sents = synth.read_sentences(f.heldout)
+    x = synth.ctc_logits(sents, B=6, T=40, V=o.V, seed=4)
+    out, frames, adv = ctc_decode(o, x, 0.0, 0)
+    for b in range(6):
+        path = np.argmax(x[b], axis=1)
+        collapsed = [int(k) for k, _ in itertools.groupby(path) if k != o.V]
+        assert out[b] == collapsed
+        assert adv[b] == len(collapsed)       # one LM advance per emission
+
+
+def test_ctc_fused_changes_decisions_and_counts_advances(tri):
+    o, f = tri
+    sents = synth.read_sentences(f.heldout)
+    x = synth.ctc_logits(sents, B=6, T=40, V=o.V, seed=5)
+    out0, fr0, _ = ctc_decode(o, x, 0.0, 0)
+    out1, fr1, adv = ctc_decode(o, x, 3.0, 0)
+    assert (fr0 != fr1).any()                 # the LM matters at this weight
+    for b in range(6):
+        assert adv[b] == len(out1[b])
+
+
+def test_rnnt_blank_retention(tri):
+    o, f = tri
+    x = synth.rnnt_logits(B=128, steps=2, V=o.V, seed=7).reshape(-1, o.V + 1)
+    states = synth.uniform_states(o.num_states, x.shape[0], seed=3)
+    raw = np.argmax(x, axis=1)
+    for lam in (0.0, 1.0, 10.0):
+        tok, st, _ = o.fused_step(RNNT, x, states, lam=lam)
+        blank = raw == o.V
+        assert (tok[blank] == o.V).all() and (st[blank] == states[blank]).all()
+        assert (tok[~blank] != o.V).all()
+
+
+def test_constructed_fig1_cases(fig1):
+    """State 11 ("on the"): lm(sat) = ln 1/32, lm(mat) = ln 21/32, final = ln 1/32.
+    asr: sat = -1.0, mat = -1.5, eos/blank column 6 = -1.2, others -10.
+    lambda = 1: sat -> -1 + ln(1/32) = -4.466, mat -> -1.5 + ln(21/32) = -1.921."""
+    o = fig1
+    row = np.full((1, 7), -10.0, dtype=np.float32)
+    row[0, 2], row[0, 4], row[0, 6] = -1.0, -1.5, -1.2
+    s = np.array([11], dtype=np.int32)
+    # RNN-T: stage 1 raw argmax = sat (non-blank) -> stage 2 picks mat -> "the mat" = 8
+    tok, st, _ = o.fused_step(RNNT, row, s, lam=1.0)
+    assert tok[0] == 4 and st[0] == 8
+    # lambda = 0: stays with the raw argmax
+    tok, st, _ = o.fused_step(RNNT, row, s, lam=0.0)
+    assert tok[0] == 2 and st[0] == 3            # "on the" + sat -> "sat" (3)
+    # CTC: the blank column is never rescored: raw -1.2 beats fused mat (-1.921)
+    tok, st, pv = o.fused_step(CTC, row, s, prev=np.array([-1]), lam=1.0)
+    assert tok[0] == 6 and st[0] == 11 and pv[0] == -1
+    # CTC with blank at -3.0, prev = none: mat wins as for the transducer
+    rowc = row.copy(); rowc[0, 6] = -3.0
+    tok, st, pv = o.fused_step(CTC, rowc, s, prev=np.array([-1]), lam=1.0)
+    assert tok[0] == 4 and st[0] == 8 and pv[0] == 4
+    # CTC, prev = sat: the repeated token keeps its raw -1.0 and beats mat's -1.921:
+    # selected but collapsed -> no LM advance, prev stays sat
+    tok, st, pv = o.fused_step(CTC, rowc, s, prev=np.array([2]), lam=1.0)
+    assert tok[0] == 2 and st[0] == 11 and pv[0] == 2
+    # CTC: blank column raw -1.2 vs fused mat -1.921 -> blank when it is the best raw
+    row2 = row.copy(); row2[0, 6] = -0.5
+    tok, st, pv = o.fused_step(CTC, row2, s, prev=np.array([4]), lam=1.0)
+    assert tok[0] == 6 and st[0] == 11 and pv[0] == -1
+    # AED: eos column = -1.2 + ln(1/32) = -4.666 loses to mat; with asr[eos] = 2.0
+    # eos = 2 - 3.466 = -1.466 beats mat (-1.921): stop, state unchanged
+    tok, st, _ = o.fused_step(AED, row, s, lam=1.0)
+    assert tok[0] == 4 and st[0] == 8
+    row3 = row.copy(); row3[0, 6] = 2.0
+    tok, st, _ = o.fused_step(AED, row3, s, lam=1.0)
+    assert tok[0] == 6 and st[0] == 11
+    assert math.isclose(2.0 + math.log(1 / 32), -1.4657359, abs_tol=1e-6)
+
+
+def test_inactive_rows_untouched(fig1):
+    row = np.zeros((2, 7), dtype=np.float32)
+    row[:, 1] = 1.0
+    tok, st, pv = fig1.fused_step(CTC, row, np.array([11, 11]), prev=np.array([-1, -1]),
+                                  active=np.array([0, 1]), lam=0.0)
+    assert tok[0] == -1 and st[0] == 11 and pv[0] == -1
+    assert tok[1] == 1 and st[1] == 7
+
+
+def test_fusion_weight_tie_break_lowest_column(fig1):
+    # two columns with identical fused values: lowest column wins (torch.argmax rule)
+    row = np.full((1, 7), -10.0, dtype=np.float32)
+    # state 0: lm(cat) = lm(sat) = ln 1/8; equal asr -> equal fused values
+    row[0, 1] = row[0, 2] = -0.25
+    for mode in (RNNT, AED, CTC):
+        tok, st, _ = fig1.fused_step(mode, row, np.array([0]), prev=np.array([-1]), lam=0.7)
+        assert tok[0] == 1 and st[0] == 2
