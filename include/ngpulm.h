@@ -1,0 +1,168 @@
+/* ngpulm.h — C ABI of the B200-native NGPU-LM hot path (libngpulm.so).
+ *
+ * NGPU-LM (arXiv 2505.22857) stores a back-off n-gram LM as flat tensors and
+ * answers batched full-vocabulary queries  state[B] -> (token_weights[B,V],
+ * next_states[B,V])  (§2.2) with Algorithm 1
+ * (PAPER.md:54-89), and fuses that query into greedy shallow-fusion decoding
+ * for CTC, transducer and AED models (§2.3).
+ *
+ * Conventions for every call below:
+ *  - All log-probabilities are natural-log float32 (ARPA log10 values are
+ *    converted at load, R1). ARPA's -99 dummy becomes -1e30 (R3).
+ *  - Token ids are 0..V-1 (vocabulary line index, or the decimal token itself
+ *    when no vocabulary file is given). State ids are 0..S-1, root = 0, ids
+ *    ordered by (context length, context token ids) with <s> = V (R6).
+ *  - "dev" pointers are CUDA device memory on the model's device; that device
+ *    must be the caller's current device. Hot-path calls (advance, final,
+ *    fused_greedy_step) are asynchronous on `stream` (NULL = legacy default
+ *    stream), never synchronize, never allocate and are CUDA-graph capturable.
+ *  - Return codes: NGPULM_OK, or
+ *      NGPULM_EDOMAIN  invalid ARPA / vocabulary content (message names the line),
+ *      NGPULM_EUSAGE   bad arguments (NULL, negative sizes, bad mode/blank id,
+ *                      wrong current device, V beyond the kernels' limit),
+ *      NGPULM_ECUDA    a CUDA runtime error (message carries cudaGetErrorString),
+ *      NGPULM_EIO      a file could not be read.
+ *    ngpulm_last_error() returns a thread-local message for the last non-OK return.
+ *  - Out-of-range state ids are reported asynchronously: the affected row gets
+ *    NaN scores / -1 next states (advance), NaN (final) or token -1 and an
+ *    unchanged state (fused step), and the first offending row index is kept
+ *    in a sticky per-model device word read by ngpulm_check().
+ *  - B = 0 is a no-op returning NGPULM_OK.
+ *  - A model is immutable after load: concurrent calls on distinct streams are
+ *    safe; outputs depend only on inputs.
+ */
+#ifndef NGPULM_H
+#define NGPULM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ngpulm_model ngpulm_model;
+typedef struct CUstream_st* ngpulm_stream; /* == cudaStream_t */
+
+enum { NGPULM_OK = 0, NGPULM_EDOMAIN = 1, NGPULM_EUSAGE = 2, NGPULM_ECUDA = 3, NGPULM_EIO = 4 };
+enum { NGPULM_CTC = 0, NGPULM_RNNT = 1, NGPULM_AED = 2 };
+enum { NGPULM_MAX_ORDER = 32 };
+
+typedef struct {
+  int32_t order;          /* N, highest n-gram order in the ARPA */
+  int32_t vocab_size;     /* V */
+  int32_t num_states;     /* S */
+  int32_t root_state;     /* always 0: the empty context (unigram state) */
+  int32_t bos_state;      /* state of "<s>", or root when absent (R4) */
+  int32_t device;         /* CUDA device, or -1 for a host-only model */
+  int64_t num_arcs;       /* incl. the V root arcs */
+  int64_t num_unk_filled; /* M: vocabulary tokens without a unigram (R2) */
+  int64_t num_dropped;    /* n-grams with <unk> beyond the unigram, dropped (R5) */
+  int64_t device_bytes;   /* bytes of the resident model on the device */
+  int32_t max_vocab;      /* largest V the kernels accept */
+  int32_t reserved;
+} ngpulm_info;
+
+/* Read-only view of the model's host copy of the flat arrays.
+ * Valid until ngpulm_free. Arcs are sorted by (from_state, token); state s owns
+ * arcs [arc_offsets[s], arc_offsets[s+1]) (PAPER.md:122 start_arcs/end_arcs);
+ * the root owns exactly arcs [0, V) with arc_tokens[v] = v. */
+typedef struct {
+  const int32_t* arc_tokens;     /* [num_arcs] */
+  const float* arc_weights;      /* [num_arcs] */
+  const int32_t* arc_to_states;  /* [num_arcs] */
+  const int32_t* arc_offsets;    /* [num_states + 1] */
+  const int32_t* boff_to_states; /* [num_states]; root -> root */
+  const float* boff_weights;     /* [num_states]; root -> 0 */
+  const float* final_weights;    /* [num_states] */
+} ngpulm_host_view;
+
+/* Parse an ARPA file (PAPER.md:94-96 line format), validate it, build the flat
+ * trie on the host (sorted arcs, arc ranges, back-off targets and weights,
+ * root filled to V arcs with the normalized <unk> weight, precomputed finals)
+ * and upload it to `cuda_device` (-1: host only; hot-path calls then return
+ * EUSAGE). `vocab_path`: one token per line, id = line index;
+ * NULL: tokens are canonical decimal ids in [0, vocab_size). `vocab_size` may
+ * be 0 with a vocabulary file. Synchronous. On success *out owns everything. */
+int ngpulm_load_arpa(const char* arpa_path, const char* vocab_path, int32_t vocab_size,
+                     int32_t cuda_device, ngpulm_model** out);
+
+/* Copy an existing model's arrays to another device without re-parsing
+ * (one replica per GPU for multi-GPU sharding). */
+int ngpulm_replicate(const ngpulm_model* src, int32_t cuda_device, ngpulm_model** out);
+
+void ngpulm_free(ngpulm_model* model);
+int ngpulm_get_info(const ngpulm_model* model, ngpulm_info* out);
+int ngpulm_host_view_get(const ngpulm_model* model, ngpulm_host_view* out);
+const char* ngpulm_last_error(void);
+
+/* Host helper: the state of the longest suffix of ("<s>" if with_bos) + tokens[0..n)
+ * that is a state — the LM context a decoder holds after those tokens. */
+int ngpulm_state_of(const ngpulm_model* model, int32_t with_bos, const int32_t* tokens,
+                    int32_t n, int32_t* out_state);
+
+/* Batched full-vocabulary query, Algorithm 1 for each row:
+ *   scores[b*V + v] = log P(v | context(states[b]))  (float32; back-off
+ *                     weights accumulated left to right, R10)
+ *   next[b*V + v]   = state after emitting v (longest suffix of context+v that
+ *                     is a state, R7)
+ *   final_out[b]    = final weight of states[b], when non-NULL.
+ * states: dev [B] int32. scores: dev [B,V] float32, next: dev [B,V] int32,
+ * both row-major and caller-owned; final_out: dev [B] float32 or NULL. */
+int ngpulm_advance(const ngpulm_model* model, const int32_t* states, int32_t B, float* scores,
+                   int32_t* next, float* final_out, ngpulm_stream stream);
+
+/* final_out[b] = final weight of states[b] (the AED <eos> score).
+ * states: dev [B] int32; final_out: dev [B] float32. */
+int ngpulm_final(const ngpulm_model* model, const int32_t* states, int32_t B, float* final_out,
+                 ngpulm_stream stream);
+
+/* One greedy shallow-fusion step for B rows, with the LM
+ * row of each state computed on chip and never written to memory.
+ *   logits:  dev float32; row b is logits + b*row_stride, V+1 columns: the V
+ *            tokens and the special column `blank_id` (blank for CTC/RNN-T,
+ *            <eos> for AED); token v sits in column v (v < blank_id) or v+1 (R19).
+ *   states:  dev [B] int32, in/out LM states.
+ *   prev:    dev [B] int32, in/out, CTC only (else ignored, may be NULL): column
+ *            selected at the previous frame, -1 = none/blank (R17).
+ *   active:  dev [B] uint8 or NULL (= all rows); inactive rows are untouched
+ *            and get tokens_out = -1.
+ *   tokens_out: dev [B] int32: the selected column.
+ * Decision rules (fused value = fmaf(lambda, lm, asr), single rounding, R13;
+ * argmax ties -> lowest column, R14):
+ *   NGPULM_RNNT two-stage: raw argmax over all columns; blank -> keep it (state
+ *               unchanged); else argmax of fused values over non-blank columns,
+ *               state <- next.
+ *   NGPULM_CTC  blank and prev columns raw, all others fused; argmax; blank ->
+ *               prev = -1; == prev -> no LM advance; else state <- next,
+ *               prev <- column.
+ *   NGPULM_AED  token columns fused, the <eos> column fmaf(lambda, final(state),
+ *               asr[eos]); eos -> state unchanged; else state <- next.
+ */
+int ngpulm_fused_greedy_step(const ngpulm_model* model, int32_t mode, const float* logits,
+                             int64_t row_stride, int32_t B, int32_t* states, int32_t* prev,
+                             const uint8_t* active, float lambda, int32_t blank_id,
+                             int32_t* tokens_out, ngpulm_stream stream);
+
+/* Synchronizes `stream`, reads and clears the sticky bad-row word:
+ * *first_bad_row = smallest row index that carried an invalid state since the
+ * last check, or -1. */
+int ngpulm_check(const ngpulm_model* model, ngpulm_stream stream, int64_t* first_bad_row);
+
+/* End-to-end convenience for callers holding HOST buffers (ideally pinned):
+ * copies states_host [B] in, runs ngpulm_advance on model-owned device
+ * scratch, copies scores_host [B,V], next_host [B,V] and final_host [B] (may
+ * be NULL) back, and synchronizes `stream`. Allocates scratch on first use. */
+int ngpulm_advance_host(ngpulm_model* model, const int32_t* states_host, int32_t B,
+                        float* scores_host, int32_t* next_host, float* final_host,
+                        ngpulm_stream stream);
+
+/* Measurement support (host only): unique model bytes a call on this batch
+ * must read — state records and arc ranges of every distinct state on the
+ * rows' back-off chains, the V root arcs once, and the finals. */
+int ngpulm_touched_bytes(const ngpulm_model* model, const int32_t* states_host, int32_t B,
+                         int64_t* out_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NGPULM_H */

@@ -280,11 +280,12 @@ bool load(Oracle& o, const char* arpa, const char* vocab_path, int32_t V) {
     // [R5] n-grams containing <unk> beyond the unigram are unreachable: dropped
     if (std::find(g.begin(), g.end(), o.UNK) != g.end()) continue;
     if (!o.ngram.emplace(g, e).second) return fail("duplicate n-gram line " + std::to_string(lineno));
-    o.N = std::max(o.N, k);
   }
   if (!ended) return fail("missing \\end\\");
-  for (auto& d : declared)
+  for (auto& d : declared) {
     if (seen[d.first] != d.second) return fail("count mismatch for order " + std::to_string(d.first));
+    if (d.second > 0) o.N = std::max(o.N, d.first);  // order N = highest declared non-empty order
+  }
   if (!o.find({o.EOS})) return fail("missing </s> unigram");
   // [R4] the <s> unigram's probability is never used: "<s>" is a state, not a token
 

@@ -1,0 +1,258 @@
+"""paper_2505_22857_b200 — B200-native NGPU-LM hot path (arXiv 2505.22857).
+
+Thin ctypes binding over lib/libngpulm.so (C ABI: include/ngpulm.h). Every step
+of the hot path runs in the library's CUDA kernels; this module only marshals
+arguments (torch tensors -> device pointers, the current CUDA stream). There
+is no CPU or PyTorch fallback: if the library is missing or a call fails, it
+raises.
+
+    lm = load_arpa("lm.arpa", vocab_size=1024, device=0)
+    scores, nxt, fin = lm.advance(states)             # [B,V] f32, [B,V] i32, [B] f32
+    tokens = lm.fused_greedy_step(CTC, logits_t, states, prev=prev, lam=0.3)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libngpulm.so")
+
+NGPULM_OK, NGPULM_EDOMAIN, NGPULM_EUSAGE, NGPULM_ECUDA, NGPULM_EIO = 0, 1, 2, 3, 4
+CTC, RNNT, AED = 0, 1, 2
+MAX_ORDER = 32
+
+
+class NgpulmError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"ngpulm error {code}: {msg}")
+        self.code = code
+
+
+class Info(C.Structure):
+    _fields_ = [("order", C.c_int32), ("vocab_size", C.c_int32), ("num_states", C.c_int32),
+                ("root_state", C.c_int32), ("bos_state", C.c_int32), ("device", C.c_int32),
+                ("num_arcs", C.c_int64), ("num_unk_filled", C.c_int64), ("num_dropped", C.c_int64),
+                ("device_bytes", C.c_int64), ("max_vocab", C.c_int32), ("reserved", C.c_int32)]
+
+
+class HostView(C.Structure):
+    _fields_ = [("arc_tokens", C.c_void_p), ("arc_weights", C.c_void_p),
+                ("arc_to_states", C.c_void_p), ("arc_offsets", C.c_void_p),
+                ("boff_to_states", C.c_void_p), ("boff_weights", C.c_void_p),
+                ("final_weights", C.c_void_p)]
+
+
+# (name, restype, argtypes) — every symbol of include/ngpulm.h
+_P, _I32, _I64, _F = C.c_void_p, C.c_int32, C.c_int64, C.c_float
+SIGNATURES = {
+    "ngpulm_load_arpa": (C.c_int, [C.c_char_p, C.c_char_p, _I32, _I32, C.POINTER(_P)]),
+    "ngpulm_replicate": (C.c_int, [_P, _I32, C.POINTER(_P)]),
+    "ngpulm_free": (None, [_P]),
+    "ngpulm_get_info": (C.c_int, [_P, C.POINTER(Info)]),
+    "ngpulm_host_view_get": (C.c_int, [_P, C.POINTER(HostView)]),
+    "ngpulm_last_error": (C.c_char_p, []),
+    "ngpulm_state_of": (C.c_int, [_P, _I32, _P, _I32, C.POINTER(_I32)]),
+    "ngpulm_advance": (C.c_int, [_P, _P, _I32, _P, _P, _P, _P]),
+    "ngpulm_final": (C.c_int, [_P, _P, _I32, _P, _P]),
+    "ngpulm_fused_greedy_step": (C.c_int, [_P, _I32, _P, _I64, _I32, _P, _P, _P, _F, _I32, _P, _P]),
+    "ngpulm_check": (C.c_int, [_P, _P, C.POINTER(_I64)]),
+    "ngpulm_advance_host": (C.c_int, [_P, _P, _I32, _P, _P, _P, _P]),
+    "ngpulm_touched_bytes": (C.c_int, [_P, _P, _I32, C.POINTER(_I64)]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libngpulm.so (in-tree). Raises if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype, fn.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def _check(code: int):
+    if code != NGPULM_OK:
+        raise NgpulmError(code, lib().ngpulm_last_error().decode(errors="replace"))
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream  # torch.cuda.Stream
+
+
+def _dev_ptr(t, dtype, name, numel=None):
+    import torch
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name}: expected a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    if numel is not None and t.numel() < numel:
+        raise ValueError(f"{name}: needs {numel} elements, has {t.numel()}")
+    return t.data_ptr()
+
+
+class NgpuLM:
+    """A resident NGPU-LM model (one replica per device)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        self.info = Info()
+        _check(lib().ngpulm_get_info(self._h, C.byref(self.info)))
+        self.V = self.info.vocab_size
+        self.order = self.info.order
+        self.num_states = self.info.num_states
+        self.bos_state = self.info.bos_state
+        self.device = self.info.device
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.ngpulm_free(h)
+            self._h = None
+
+    # ---------------------------------------------------------------- host helpers
+    def replicate(self, device: int) -> "NgpuLM":
+        out = C.c_void_p()
+        _check(lib().ngpulm_replicate(self._h, device, C.byref(out)))
+        return NgpuLM(out.value)
+
+    def state_of(self, with_bos: bool, tokens) -> int:
+        arr = (C.c_int32 * max(1, len(tokens)))(*tokens)
+        out = C.c_int32()
+        _check(lib().ngpulm_state_of(self._h, int(with_bos), C.cast(arr, C.c_void_p), len(tokens),
+                                     C.byref(out)))
+        return out.value
+
+    def host_arrays(self):
+        """numpy views of the host copy of the flat trie (see ngpulm_host_view)."""
+        import numpy as np
+        hv = HostView()
+        _check(lib().ngpulm_host_view_get(self._h, C.byref(hv)))
+        A, S = self.info.num_arcs, self.num_states
+
+        def arr(p, n, ct, dt):
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(ct)), shape=(n,)).view(dt).copy()
+        return {
+            "arc_tokens": arr(hv.arc_tokens, A, C.c_int32, np.int32),
+            "arc_weights": arr(hv.arc_weights, A, C.c_float, np.float32),
+            "arc_to_states": arr(hv.arc_to_states, A, C.c_int32, np.int32),
+            "arc_offsets": arr(hv.arc_offsets, S + 1, C.c_int32, np.int32),
+            "boff_to_states": arr(hv.boff_to_states, S, C.c_int32, np.int32),
+            "boff_weights": arr(hv.boff_weights, S, C.c_float, np.float32),
+            "final_weights": arr(hv.final_weights, S, C.c_float, np.float32),
+        }
+
+    def touched_bytes(self, states_np) -> int:
+        import numpy as np
+        st = np.ascontiguousarray(states_np, dtype=np.int32)
+        out = C.c_int64()
+        _check(lib().ngpulm_touched_bytes(self._h, st.ctypes.data, st.size, C.byref(out)))
+        return out.value
+
+    # ---------------------------------------------------------------- hot path
+    def advance(self, states, scores=None, next=None, final_out=None, want_final=True, stream=None):
+        """ngpulm_advance: states [B] int32 (CUDA) -> scores [B,V] f32, next [B,V] i32, final [B]."""
+        import torch
+        B = states.numel()
+        if scores is None:
+            scores = torch.empty((B, self.V), dtype=torch.float32, device=states.device)
+        if next is None:
+            next = torch.empty((B, self.V), dtype=torch.int32, device=states.device)
+        if final_out is None and want_final:
+            final_out = torch.empty(B, dtype=torch.float32, device=states.device)
+        _check(lib().ngpulm_advance(
+            self._h, _dev_ptr(states, torch.int32, "states", B), B,
+            _dev_ptr(scores, torch.float32, "scores", B * self.V),
+            _dev_ptr(next, torch.int32, "next", B * self.V),
+            _dev_ptr(final_out, torch.float32, "final_out", B), _stream(stream)))
+        return scores, next, final_out
+
+    def final(self, states, out=None, stream=None):
+        import torch
+        B = states.numel()
+        if out is None:
+            out = torch.empty(B, dtype=torch.float32, device=states.device)
+        _check(lib().ngpulm_final(self._h, _dev_ptr(states, torch.int32, "states", B), B,
+                                  _dev_ptr(out, torch.float32, "out", B), _stream(stream)))
+        return out
+
+    def fused_greedy_step(self, mode: int, logits, states, prev=None, active=None, lam: float = 0.3,
+                          blank_id: int | None = None, tokens_out=None, row_stride: int | None = None,
+                          B: int | None = None, stream=None):
+        """ngpulm_fused_greedy_step. logits: CUDA f32 tensor whose row b starts at
+        b*row_stride (default: a [B, V+1] contiguous tensor, or a strided 2-D view
+        such as logits3d[:, t] of a [B, T, V+1] tensor). states/prev updated in place."""
+        import torch
+        if B is None:
+            B = states.numel()
+        if logits.dtype != torch.float32 or not logits.is_cuda:
+            raise TypeError("logits: expected a CUDA float32 tensor")
+        if row_stride is None:
+            row_stride = logits.stride(0) if logits.dim() >= 2 else self.V + 1
+            if logits.dim() == 2 and logits.stride(1) != 1:
+                raise ValueError("logits rows must be contiguous")
+        if tokens_out is None:
+            tokens_out = torch.empty(B, dtype=torch.int32, device=states.device)
+        blank = self.V if blank_id is None else blank_id
+        _check(lib().ngpulm_fused_greedy_step(
+            self._h, mode, logits.data_ptr(), row_stride, B,
+            _dev_ptr(states, torch.int32, "states", B),
+            _dev_ptr(prev, torch.int32, "prev", B) if prev is not None else None,
+            _dev_ptr(active, torch.uint8, "active", B) if active is not None else None,
+            float(lam), blank, _dev_ptr(tokens_out, torch.int32, "tokens_out", B), _stream(stream)))
+        return tokens_out
+
+    def check(self, stream=None) -> int:
+        out = C.c_int64()
+        _check(lib().ngpulm_check(self._h, _stream(stream), C.byref(out)))
+        return out.value
+
+    def advance_host(self, states_h, scores_h, next_h, final_h=None, stream=None):
+        """ngpulm_advance_host over host (ideally pinned) CPU tensors."""
+        import torch
+        B = states_h.numel()
+        for t, dt in ((states_h, torch.int32), (scores_h, torch.float32), (next_h, torch.int32)):
+            assert not t.is_cuda and t.dtype == dt and t.is_contiguous()
+        _check(lib().ngpulm_advance_host(
+            self._h, states_h.data_ptr(), B, scores_h.data_ptr(), next_h.data_ptr(),
+            final_h.data_ptr() if final_h is not None else None, _stream(stream)))
+
+
+def load_arpa(arpa_path: str, vocab_path: str | None = None, vocab_size: int = 0,
+              device: int | None = None) -> NgpuLM:
+    """ngpulm_load_arpa. device=None -> torch's current device; -1 -> host-only model."""
+    if device is None:
+        import torch
+        device = torch.cuda.current_device()
+    out = C.c_void_p()
+    _check(lib().ngpulm_load_arpa(arpa_path.encode(), vocab_path.encode() if vocab_path else None,
+                                  vocab_size, device, C.byref(out)))
+    return NgpuLM(out.value)
+
+
+# C-ABI names, for callers that mirror include/ngpulm.h
+ngpulm_load_arpa = load_arpa
+ngpulm_advance = NgpuLM.advance
+ngpulm_final = NgpuLM.final
+ngpulm_fused_greedy_step = NgpuLM.fused_greedy_step
+ngpulm_check = NgpuLM.check
+ngpulm_replicate = NgpuLM.replicate
+ngpulm_state_of = NgpuLM.state_of
+ngpulm_advance_host = NgpuLM.advance_host
+ngpulm_touched_bytes = NgpuLM.touched_bytes

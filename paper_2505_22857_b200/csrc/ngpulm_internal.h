@@ -1,0 +1,61 @@
+// Internal types of libngpulm (product code; never seen by the oracle).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/ngpulm.h"
+
+namespace ngpulm {
+
+// One 16-byte record per state: the chain walk (Algorithm 1 lines 72, 81, 82)
+// reads exactly one aligned sector per back-off level.
+struct alignas(16) StateRec {
+  int32_t arc_begin;  // start_arcs[state]
+  int32_t arc_end;    // end_arcs[state]
+  int32_t boff_to;    // boff_to_states[state]
+  float boff_w;       // boff_weights[state]
+};
+
+// The flat trie on the host (SPEC.md:95-111 FlatLM).
+struct HostModel {
+  int32_t V = 0, order = 0, num_states = 0, bos_state = 0;
+  int64_t num_unk_filled = 0, num_dropped = 0;
+  std::vector<int32_t> arc_tok, arc_to;  // [A]
+  std::vector<float> arc_w;              // [A]
+  std::vector<int32_t> arc_off;          // [S+1]
+  std::vector<int32_t> boff_to;          // [S]
+  std::vector<float> boff_w, final_w;    // [S]
+  // (parent state, token) -> child state: the prefix edges of the context trie
+  std::vector<uint64_t> child_keys;
+  std::vector<int32_t> child_vals;
+  uint64_t child_mask = 0;
+
+  int32_t child(int32_t parent, int32_t tok) const;
+};
+
+// Parse + validate + build. Returns NGPULM_OK or an error code with `err` set.
+int build_from_arpa(const char* arpa_path, const char* vocab_path, int32_t vocab_size,
+                    HostModel& out, std::string& err);
+
+// Device-side view passed to kernels by value.
+struct DevModel {
+  const StateRec* srec;
+  const float* final_w;
+  const int32_t* arc_tok;
+  const float* arc_w;
+  const int32_t* arc_to;
+  int32_t S, V, order;
+  unsigned long long* bad_row;  // sticky min bad row (ULLONG_MAX = none)
+};
+
+// Kernel launchers (kernels.cu). Return cudaError_t as int.
+int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* scores,
+                   int32_t* next, float* final_out, void* stream);
+int launch_final(const DevModel& m, const int32_t* states, int32_t B, float* out, void* stream);
+int launch_fused(const DevModel& m, int32_t mode, const float* logits, int64_t row_stride,
+                 int32_t B, int32_t* states, int32_t* prev, const uint8_t* active, float lambda,
+                 int32_t blank, int32_t* tokens_out, void* stream);
+int max_vocab_supported();
+
+}  // namespace ngpulm

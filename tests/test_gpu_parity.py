@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Bar (BASELINE.json north_star): next-state ids and argmax tokens bit-exact;
+scores within 1e-5 (f32). Against the oracle's Algorithm-1-order float32 value
+(score32) the kernels are required to be BIT-EXACT, and
+within 1e-5 of the f64 definition where the f32 bound allows it.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import AED, CTC, RNNT, Oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2505_22857_b200 as ng  # noqa: E402
+
+SMALL = ["uni16", "bi16", "tiny3", "tri64", "five48", "ten24"]
+
+
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch.device("cuda:0")
+
+
+def same_bits(a, b):
+    return np.array_equal(np.asarray(a, np.float32).view(np.int32), np.asarray(b, np.float32).view(np.int32))
+
+
+@pytest.fixture(scope="module")
+def pairs(small_lms, fig1_paths):
+    out = {}
+    for n in SMALL:
+        f = small_lms[n]
+        out[n] = (ng.load_arpa(f.arpa, vocab_size=f.vocab_size, device=0), Oracle(f.arpa, vocab_size=f.vocab_size), f)
+    arpa, vocab = fig1_paths
+    out["fig1"] = (ng.load_arpa(arpa, vocab, device=0), Oracle(arpa, vocab), None)
+    return out
+
+
+def gpu_advance(m, states_np):
+    st = torch.from_numpy(np.ascontiguousarray(states_np, np.int32)).to(dev())
+    s, n, f = m.advance(st)
+    torch.cuda.synchronize()
+    return s.cpu().numpy(), n.cpu().numpy(), f.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", SMALL + ["fig1"])
+def test_advance_exhaustive_small(pairs, name):
+    """All states x all tokens of every small LM (config 0 = tiny3)."""
+    m, o, _ = pairs[name]
+    states = np.arange(o.num_states, dtype=np.int32)
+    s, n, f = gpu_advance(m, states)
+    s32, s64, n_o, _ = o.rows(states)
+    f32, f64 = o.finals(states)
+    assert np.array_equal(n, n_o)
+    assert same_bits(s, s32)
+    assert same_bits(f, f32)
+    assert np.max(np.abs(s - s64)) < 1e-5
+    assert m.check() == -1
+
+
+def test_config0_batches_of_4(pairs):
+    """BASELINE configs[0]: tiny 3-gram V=32, batch 4 states."""
+    m, o, _ = pairs["tiny3"]
+    rng = np.random.default_rng(11)
+    for _ in range(10):
+        states = rng.integers(0, o.num_states, size=4).astype(np.int32)
+        s, n, f = gpu_advance(m, states)
+        s32, _, n_o, _ = o.rows(states, want64=False)
+        assert np.array_equal(n, n_o) and same_bits(s, s32)
+
+
+def test_unaligned_outputs_scalar_path(pairs):
+    m, o, _ = pairs["tri64"]
+    B, V = 37, m.V
+    states = torch.arange(B, dtype=torch.int32, device=dev()) * 3 % o.num_states
+    sc = torch.empty(B * V + 1, dtype=torch.float32, device=dev())[1:]
+    nx = torch.empty(B * V + 1, dtype=torch.int32, device=dev())[1:]
+    m.advance(states, scores=sc, next=nx, want_final=False)
+    torch.cuda.synchronize()
+    s32, _, n_o, _ = o.rows(states.cpu().numpy(), want64=False)
+    assert same_bits(sc.cpu().numpy().reshape(B, V), s32)
+    assert np.array_equal(nx.cpu().numpy().reshape(B, V), n_o)
+
+
+def test_invalid_state_and_empty_batch(pairs):
+    m, o, _ = pairs["tri64"]
+    states = np.array([0, 5, o.num_states + 3, 2, -1], dtype=np.int32)
+    s, n, f = gpu_advance(m, states)
+    assert np.isnan(s[2]).all() and (n[2] == -1).all() and np.isnan(f[2])
+    assert m.check() == 2
+    assert m.check() == -1                     # sticky word cleared by the read
+    s32, _, n_o, _ = o.rows(states[[0, 1, 3]], want64=False)
+    assert same_bits(s[[0, 1, 3]], s32) and np.array_equal(n[[0, 1, 3]], n_o)
+    e = torch.empty(0, dtype=torch.int32, device=dev())
+    m.advance(e)                                # B = 0: no-op
+    fin = m.final(torch.tensor([1, -7], dtype=torch.int32, device=dev()))
+    torch.cuda.synchronize()
+    assert np.isnan(fin[1].item()) and m.check() == 1
+
+
+@pytest.fixture(scope="module")
+def lm6(lm_dir):
+    """BASELINE configs[1]: token 6-gram, V=1024 BPE-like, ~1M n-grams."""
+    f = synth.make_lm(lm_dir, 1024, 6, tokens=430000, seed=1, heldout=2000, tag="cfg1_6gram")
+    return ng.load_arpa(f.arpa, vocab_size=1024, device=0), Oracle(f.arpa, vocab_size=1024), f
+
+
+def trajectory_states(m, f, n, seed):
+    ctx = synth.sample_contexts(synth.read_sentences(f.heldout), f.order, n, seed)
+    return np.array([m.state_of(b, t) for b, t in ctx], dtype=np.int32), ctx
+
+
+def test_config1_b128_full_rows(lm6):
+    m, o, f = lm6
+    assert m.info.num_arcs > 500_000 and 800_000 < sum(1 for _ in open(f.arpa)) < 1_300_000
+    st_traj, ctx = trajectory_states(m, f, 96, seed=2)
+    # the library's and the oracle's context -> state maps agree (R6, R7)
+    assert [o.state_of(b, t) for b, t in ctx] == st_traj.tolist()
+    states = np.concatenate([st_traj, synth.uniform_states(m.num_states, 32, seed=3)])
+    s, n, fin = gpu_advance(m, states)
+    s32, s64, n_o, lv = o.rows(states)
+    f32, _ = o.finals(states)
+    assert np.array_equal(n, n_o) and same_bits(s, s32) and same_bits(fin, f32)
+    assert np.max(np.abs(s - s64)) < 1e-5
+    assert lv.max() <= 6
+
+
+def test_headline_b1024_sampled_rows(lm6):
+    """The bench launch (B=1024 trajectory rows) checked on sampled rows."""
+    m, o, f = lm6
+    states, _ = trajectory_states(m, f, 1024, seed=2)
+    s, n, fin = gpu_advance(m, states)
+    rows = np.random.default_rng(5).choice(1024, 48, replace=False)
+    s32, s64, n_o, _ = o.rows(states[rows])
+    assert np.array_equal(n[rows], n_o) and same_bits(s[rows], s32)
+    assert np.max(np.abs(s[rows] - s64)) < 1e-5
+    # properties that hold for every row: normalization against the final weight
+    tot = np.exp(s.astype(np.float64)).sum(1) + np.exp(fin.astype(np.float64))
+    assert np.max(np.abs(tot - 1)) < 1e-4
+    # sharded == unsharded, bit for bit (rows are independent)
+    parts = [gpu_advance(m, states[i:i + 256]) for i in range(0, 1024, 256)]
+    assert same_bits(np.concatenate([p[0] for p in parts]), s)
+    assert np.array_equal(np.concatenate([p[1] for p in parts]), n)
+
+
+def test_advance_host_and_replica_and_streams(lm6):
+    m, o, f = lm6
+    states, _ = trajectory_states(m, f, 200, seed=7)
+    s, n, fin = gpu_advance(m, states)
+    sh = torch.empty((200, m.V), dtype=torch.float32).pin_memory()
+    nh = torch.empty((200, m.V), dtype=torch.int32).pin_memory()
+    fh = torch.empty(200, dtype=torch.float32).pin_memory()
+    m.advance_host(torch.from_numpy(states).pin_memory(), sh, nh, fh)
+    assert same_bits(sh.numpy(), s) and np.array_equal(nh.numpy(), n) and same_bits(fh.numpy(), fin)
+    r = m.replicate(0)
+    s2, n2, _ = gpu_advance(r, states)
+    assert same_bits(s2, s) and np.array_equal(n2, n)
+    st = torch.from_numpy(states).to(dev())
+    outs = []
+    for _ in range(2):
+        with torch.cuda.stream(torch.cuda.Stream()):
+            outs.append(m.advance(st))
+    torch.cuda.synchronize()
+    for a, b, _ in outs:
+        assert same_bits(a.cpu().numpy(), s) and np.array_equal(b.cpu().numpy(), n)
+
+
+# ---------------------------------------------------------------- fused greedy step
+def gpu_step(m, mode, logits_np, states, prev=None, active=None, lam=0.3, blank=None):
+    x = torch.from_numpy(np.ascontiguousarray(logits_np, np.float32)).to(dev())
+    st = torch.from_numpy(np.array(states, np.int32)).to(dev())
+    pv = torch.from_numpy(np.array(prev, np.int32)).to(dev()) if prev is not None else None
+    ac = torch.from_numpy(np.array(active, np.uint8)).to(dev()) if active is not None else None
+    tok = m.fused_greedy_step(mode, x, st, prev=pv, active=ac, lam=lam, blank_id=blank)
+    torch.cuda.synchronize()
+    return tok.cpu().numpy(), st.cpu().numpy(), (pv.cpu().numpy() if pv is not None else None)
+
+
+@pytest.mark.parametrize("mode", [CTC, RNNT, AED])
+@pytest.mark.parametrize("lam", [0.0, 0.3, 3.0])
+@pytest.mark.parametrize("name", ["tiny3", "five48", "ten24"])
+def test_fused_step_matches_oracle(pairs, mode, lam, name):
+    m, o, _ = pairs[name]
+    rng = np.random.default_rng(17)
+    B = 300
+    x = synth.rnnt_logits(B, 1, o.V, seed=9)[0]
+    x[::11, 2] = x[::11].max(axis=1)              # exact ties at the top
+    states = rng.integers(0, o.num_states, size=B).astype(np.int32)
+    prev = rng.integers(-1, o.V + 1, size=B).astype(np.int32)
+    prev[prev == o.V] = -1
+    active = (rng.random(B) > 0.1).astype(np.uint8)
+    tg, sg, pg = gpu_step(m, mode, x, states, prev if mode == CTC else None, active, lam)
+    to, so, po = o.fused_step(mode, x, states, prev=prev if mode == CTC else None, active=active, lam=lam)
+    assert np.array_equal(tg, to) and np.array_equal(sg, so)
+    if mode == CTC:
+        assert np.array_equal(pg, po)
+
+
+@pytest.mark.parametrize("mode", [CTC, RNNT, AED])
+def test_fused_step_blank_first_column(pairs, mode):
+    """blank_id = 0 (special column first): tokens v sit in column v+1 (R19)."""
+    m, o, _ = pairs["tri64"]
+    B = 200
+    x = synth.rnnt_logits(B, 1, o.V, seed=3, blank=0)[0]
+    states = synth.uniform_states(o.num_states, B, seed=4)
+    prev = np.full(B, -1, np.int32)
+    tg, sg, pg = gpu_step(m, mode, x, states, prev if mode == CTC else None, None, 1.0, blank=0)
+    to, so, po = o.fused_step(mode, x, states, prev=prev if mode == CTC else None, lam=1.0, blank_id=0)
+    assert np.array_equal(tg, to) and np.array_equal(sg, so)
+
+
+def test_ctc_decode_loop_config2_shape(lm6):
+    """BASELINE configs[2] layout: logits [B, T, V+1] (row stride T*(V+1)), lambda=0.3,
+    frame loop on the GPU vs the oracle on sampled utterances."""
+    m, o, f = lm6
+    B, T = 256, 64
+    sents = synth.read_sentences(f.heldout)
+    x = synth.ctc_logits(sents, B, T, m.V, seed=4)
+    xd = torch.from_numpy(x).to(dev())
+    st = torch.zeros(B, dtype=torch.int32, device=dev())
+    pv = torch.full((B,), -1, dtype=torch.int32, device=dev())
+    frames = torch.empty((T, B), dtype=torch.int32, device=dev())
+    for t in range(T):
+        m.fused_greedy_step(CTC, xd[:, t], st, prev=pv, lam=0.3, tokens_out=frames[t])
+    torch.cuda.synchronize()
+    rows = np.arange(0, B, 16)
+    so, po = np.zeros(rows.size, np.int32), np.full(rows.size, -1, np.int32)
+    fo = []
+    for t in range(T):
+        tok, so, po = o.fused_step(CTC, x[rows, t], so, prev=po, lam=0.3)
+        fo.append(tok)
+    assert np.array_equal(frames.cpu().numpy()[:, rows], np.stack(fo))
+    assert np.array_equal(st.cpu().numpy()[rows], so) and np.array_equal(pv.cpu().numpy()[rows], po)
+    # the LM changed some decisions relative to plain greedy (the test means something)
+    assert (np.stack(fo) != np.argmax(x[rows], axis=2).T).any()
+
+
+def test_fused_invalid_state(pairs):
+    m, o, _ = pairs["tri64"]
+    x = synth.rnnt_logits(3, 1, o.V, seed=1)[0]
+    tg, sg, pg = gpu_step(m, CTC, x, [1, o.num_states, 2], [-1, -1, -1], None, 0.5)
+    assert tg[1] == -1 and sg[1] == o.num_states and m.check() == 1
