@@ -46,6 +46,7 @@ typedef struct CUstream_st* ngpulm_stream; /* == cudaStream_t */
 enum { NGPULM_OK = 0, NGPULM_EDOMAIN = 1, NGPULM_EUSAGE = 2, NGPULM_ECUDA = 3, NGPULM_EIO = 4 };
 enum { NGPULM_CTC = 0, NGPULM_RNNT = 1, NGPULM_AED = 2 };
 enum { NGPULM_MAX_ORDER = 32 };
+enum { NGPULM_CHAIN_TABLE = 0, NGPULM_CHAIN_WALK = 1 };
 
 typedef struct {
   int32_t order;          /* N, highest n-gram order in the ARPA */
@@ -59,7 +60,7 @@ typedef struct {
   int64_t num_dropped;    /* n-grams with <unk> beyond the unigram, dropped (R5) */
   int64_t device_bytes;   /* bytes of the resident model on the device */
   int32_t max_vocab;      /* largest V the kernels accept */
-  int32_t reserved;
+  int32_t chain_mode;     /* NGPULM_CHAIN_TABLE or NGPULM_CHAIN_WALK */
 } ngpulm_info;
 
 /* Read-only view of the model's host copy of the flat arrays.
@@ -91,6 +92,17 @@ int ngpulm_load_arpa(const char* arpa_path, const char* vocab_path, int32_t voca
 int ngpulm_replicate(const ngpulm_model* src, int32_t cuda_device, ngpulm_model** out);
 
 void ngpulm_free(ngpulm_model* model);
+
+/* How the kernels obtain a row's back-off levels (Algorithm 1 lines 72, 81-82):
+ *   NGPULM_CHAIN_TABLE (default): from a per-state record built at load time
+ *     (arc range and acc_boff of every level of the back-off chain, accumulated
+ *     in Algorithm 1's order) — one dependent memory access instead of one per
+ *     level; costs 16 * max(1, order) bytes per state of HBM.
+ *   NGPULM_CHAIN_WALK: walk boff_to_states / boff_weights at query time, level
+ *     by level, exactly as Algorithm 1 is written.
+ * Both give bit-identical results. Not to be called concurrently with hot-path
+ * calls on the same model (it changes what later launches read). */
+int ngpulm_set_chain_mode(ngpulm_model* model, int32_t mode);
 int ngpulm_get_info(const ngpulm_model* model, ngpulm_info* out);
 int ngpulm_host_view_get(const ngpulm_model* model, ngpulm_host_view* out);
 const char* ngpulm_last_error(void);

@@ -16,10 +16,11 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libngpulm.so")
+LIB_PATH = os.environ.get("NGPULM_LIB") or os.path.join(HERE, "lib", "libngpulm.so")
 
 NGPULM_OK, NGPULM_EDOMAIN, NGPULM_EUSAGE, NGPULM_ECUDA, NGPULM_EIO = 0, 1, 2, 3, 4
 CTC, RNNT, AED = 0, 1, 2
+CHAIN_TABLE, CHAIN_WALK = 0, 1
 MAX_ORDER = 32
 
 
@@ -33,7 +34,7 @@ class Info(C.Structure):
     _fields_ = [("order", C.c_int32), ("vocab_size", C.c_int32), ("num_states", C.c_int32),
                 ("root_state", C.c_int32), ("bos_state", C.c_int32), ("device", C.c_int32),
                 ("num_arcs", C.c_int64), ("num_unk_filled", C.c_int64), ("num_dropped", C.c_int64),
-                ("device_bytes", C.c_int64), ("max_vocab", C.c_int32), ("reserved", C.c_int32)]
+                ("device_bytes", C.c_int64), ("max_vocab", C.c_int32), ("chain_mode", C.c_int32)]
 
 
 class HostView(C.Structure):
@@ -49,6 +50,7 @@ SIGNATURES = {
     "ngpulm_load_arpa": (C.c_int, [C.c_char_p, C.c_char_p, _I32, _I32, C.POINTER(_P)]),
     "ngpulm_replicate": (C.c_int, [_P, _I32, C.POINTER(_P)]),
     "ngpulm_free": (None, [_P]),
+    "ngpulm_set_chain_mode": (C.c_int, [_P, _I32]),
     "ngpulm_get_info": (C.c_int, [_P, C.POINTER(Info)]),
     "ngpulm_host_view_get": (C.c_int, [_P, C.POINTER(HostView)]),
     "ngpulm_last_error": (C.c_char_p, []),
@@ -127,6 +129,11 @@ class NgpuLM:
             self._h = None
 
     # ---------------------------------------------------------------- host helpers
+    def set_chain_mode(self, mode: int) -> None:
+        """CHAIN_TABLE (load-time chain records, default) or CHAIN_WALK (Algorithm 1 walk)."""
+        _check(lib().ngpulm_set_chain_mode(self._h, mode))
+        self.info.chain_mode = mode
+
     def replicate(self, device: int) -> "NgpuLM":
         out = C.c_void_p()
         _check(lib().ngpulm_replicate(self._h, device, C.byref(out)))
@@ -253,6 +260,7 @@ ngpulm_final = NgpuLM.final
 ngpulm_fused_greedy_step = NgpuLM.fused_greedy_step
 ngpulm_check = NgpuLM.check
 ngpulm_replicate = NgpuLM.replicate
+ngpulm_set_chain_mode = NgpuLM.set_chain_mode
 ngpulm_state_of = NgpuLM.state_of
 ngpulm_advance_host = NgpuLM.advance_host
 ngpulm_touched_bytes = NgpuLM.touched_bytes

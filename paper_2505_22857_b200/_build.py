@@ -24,6 +24,14 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def build_phase_timing() -> str:
+    """Debug variant with per-CTA phase stamps (tools/phase_timing.py); not the product."""
+    out = os.path.join(LIBDIR, "libngpulm_timing.so")
+    cmd = [NVCC, *ARCH, *FLAGS, "-DNGPULM_PHASE_TIMING", "-o", out, *[os.path.join(CSRC, s) for s in SOURCES]]
+    subprocess.run(cmd, check=True)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB

@@ -413,4 +413,33 @@ int build_from_arpa(const char* arpa_path, const char* vocab_path, int32_t V, Ho
   return NGPULM_OK;
 }
 
+void build_chain_table(const HostModel& m, std::vector<int32_t>& out, int32_t& slots) {
+  slots = std::max(1, m.order);
+  const int32_t S = m.num_states;
+  out.assign((size_t)S * slots * 4, 0);
+  for (int32_t s = 0; s < S; ++s) {
+    int32_t* rec = out.data() + (size_t)s * slots * 4;
+    float acc = 0.0f;
+    int32_t n = 0, pre = 0, x = s;
+    for (int it = 0; it < slots && x != 0; ++it) {  // Algorithm 1 lines 72-82, at load time
+      const int32_t b = m.arc_off[x], e = m.arc_off[x + 1];
+      if (e > b && n + 1 < slots) {
+        int32_t* lv = rec + (size_t)(n + 1) * 4;
+        lv[0] = b;
+        lv[1] = pre;
+        std::memcpy(&lv[2], &acc, 4);
+        pre += e - b;
+        ++n;
+      }
+      acc = acc + m.boff_w[x];
+      x = m.boff_to[x];
+    }
+    rec[0] = n;
+    std::memcpy(&rec[1], &acc, 4);
+    std::memcpy(&rec[2], &m.final_w[s], 4);
+    rec[3] = pre;
+    for (int32_t i = n + 1; i < slots; ++i) rec[(size_t)i * 4 + 1] = pre;
+  }
+}
+
 }  // namespace ngpulm

@@ -19,6 +19,8 @@ struct ngpulm_model {
   void* blob = nullptr;
   size_t blob_bytes = 0;
   ngpulm::DevModel dm{};
+  const void* chain_dev = nullptr;  // chain table inside blob
+  int32_t chain_mode = NGPULM_CHAIN_TABLE;
   void* scratch = nullptr;  // ngpulm_advance_host only
   size_t scratch_bytes = 0;
   std::mutex mu;
@@ -58,7 +60,12 @@ int upload(ngpulm_model* m, int device) {
   const size_t o_tok = align256(o_fin + S * 4);
   const size_t o_w = align256(o_tok + A * 4);
   const size_t o_to = align256(o_w + A * 4);
-  const size_t o_bad = align256(o_to + A * 4);
+  std::vector<int32_t> chain;
+  int32_t slots = 1;
+  ngpulm::build_chain_table(h, chain, slots);
+  const size_t o_tag = align256(o_to + A * 4);
+  const size_t o_chain = align256(o_tag + (size_t)h.V * 4);
+  const size_t o_bad = align256(o_chain + chain.size() * 4);
   const size_t total = align256(o_bad + 8);
   std::vector<unsigned char> stage(total, 0);
   auto* rec = reinterpret_cast<ngpulm::StateRec*>(stage.data() + o_srec);
@@ -68,6 +75,9 @@ int upload(ngpulm_model* m, int device) {
   std::memcpy(stage.data() + o_tok, h.arc_tok.data(), A * 4);
   std::memcpy(stage.data() + o_w, h.arc_w.data(), A * 4);
   std::memcpy(stage.data() + o_to, h.arc_to.data(), A * 4);
+  std::memcpy(stage.data() + o_chain, chain.data(), chain.size() * 4);
+  auto* tag = reinterpret_cast<int32_t*>(stage.data() + o_tag);
+  for (int32_t v = 0; v < h.V; ++v) tag[v] = (int32_t)((uint32_t)h.arc_to[v] | 0x80000000u);
   std::memset(stage.data() + o_bad, 0xff, 8);
 
   DeviceGuard g(device);
@@ -86,6 +96,10 @@ int upload(ngpulm_model* m, int device) {
   m->dm.arc_w = reinterpret_cast<const float*>(base + o_w);
   m->dm.arc_to = reinterpret_cast<const int32_t*>(base + o_to);
   m->dm.bad_row = reinterpret_cast<unsigned long long*>(base + o_bad);
+  m->dm.root_tag = reinterpret_cast<const int32_t*>(base + o_tag);
+  m->chain_dev = base + o_chain;
+  m->dm.chain = m->chain_mode == NGPULM_CHAIN_TABLE ? m->chain_dev : nullptr;
+  m->dm.chain_slots = slots;
   m->dm.S = h.num_states;
   m->dm.V = h.V;
   m->dm.order = h.order;
@@ -152,6 +166,14 @@ void ngpulm_free(ngpulm_model* m) {
   delete m;
 }
 
+int ngpulm_set_chain_mode(ngpulm_model* m, int32_t mode) {
+  if (!m) return err(NGPULM_EUSAGE, "model is NULL");
+  if (mode != NGPULM_CHAIN_TABLE && mode != NGPULM_CHAIN_WALK) return err(NGPULM_EUSAGE, "bad chain mode");
+  m->chain_mode = mode;
+  m->dm.chain = mode == NGPULM_CHAIN_TABLE ? m->chain_dev : nullptr;
+  return NGPULM_OK;
+}
+
 int ngpulm_get_info(const ngpulm_model* m, ngpulm_info* out) {
   if (!m || !out) return err(NGPULM_EUSAGE, "NULL argument");
   std::memset(out, 0, sizeof *out);
@@ -166,6 +188,7 @@ int ngpulm_get_info(const ngpulm_model* m, ngpulm_info* out) {
   out->num_dropped = m->h.num_dropped;
   out->device_bytes = (int64_t)m->blob_bytes;
   out->max_vocab = ngpulm::max_vocab_supported();
+  out->chain_mode = m->chain_mode;
   return NGPULM_OK;
 }
 

@@ -1,161 +1,362 @@
 // NGPU-LM hot path for sm_100a: batched full-vocabulary query (Algorithm 1,
 // PAPER.md:54-89) and the fused greedy shallow-fusion step.
 //
-// Design: one CTA per batch row, 256 threads.
-//  1. one thread walks the row's back-off chain (Algorithm 1 lines 72, 81-82):
-//     one 16-byte StateRec per level, acc_boff accumulated left to right in
-//     float (R10); the root is never loaded (its arcs are [0, V)).
-//  2. all threads scatter the non-root levels' arcs into shared memory: pass 1
-//     takes, per token, the lowest level index with an arc (= the first level
-//     Algorithm 1 would fill, lines 77-79) with a shared-memory atomicMin; pass
-//     2 writes that level's acc + weight and target.
-//  3. the root level is dense: every remaining token takes
-//     acc_root + root_w[v] and root_to[v]; the row leaves in 16-byte streaming
-//     stores (advance) or feeds a warp-shuffle argmax (fused step), so the LM
-//     row of the fused step never touches HBM.
-// No tensor cores: this is gather/scatter + store bandwidth.
+// Design: one CTA of 256 threads per batch row; the row
+// lives in shared memory as (score, next state) per token, 8 KB at V = 1024,
+// so 8 CTAs fit per SM and B = 1024 rows run as one wave. Bulk data moves by
+// TMA (cp.async.bulk), so the SM's load/store queue only carries the
+// latency-critical gathers (state, chain record, arcs), which complete in
+// issue order behind whatever else that queue holds.
+//  0. prologue, independent of earlier kernels (model data is immutable): one
+//     thread bulk-copies the root level (an arc for every token,
+//     [0, V)) into the row: weights into the score slots, targets into the
+//     next-state slots. Then griddepcontrol.wait (programmatic dependent
+//     launch), so launch and prologue overlap the previous kernel.
+//  1. warp 0 reads the row's state and its back-off levels (Algorithm 1 lines
+//     72, 81-82) — from the load-time chain table (one 16-byte record slot per
+//     level and lane, acc_boff pre-accumulated left to right in float, R10)
+//     or, in walk mode, lane 0 walks boff_to_states level by level exactly as
+//     Algorithm 1 does. One barrier publishes them.
+//  2. every thread gathers up to 4 arcs of the row into registers, all loads
+//     in flight together (a level's arcs are contiguous: arcs are sorted by
+//     (from_state, token)), while the root slots get acc_root
+//     added (root score = acc_root + root weight).
+//  3. the gathered arcs are written into the row level by level from the
+//     lowest order up, one barrier per level, so a higher-order arc
+//     overwrites a lower-order one — Algorithm 1's "first level found wins"
+//     (lines 77-79) with plain shared-memory stores, no atomics.
+//  4. advance: the finished row leaves by two TMA bulk stores (scores, next);
+//     fused step: the columns' fused values feed a shuffle argmax, so the LM
+//     row never touches HBM.
+// Rows with more than 1024 non-root arcs repeat steps 2-3 per 1024-arc chunk.
+// No tensor cores: gather/scatter + store bandwidth only.
 #include <cuda_runtime.h>
 
 #include <climits>
-#include <cstdint>
 #include <cmath>
+#include <cstdint>
 
 #include "ngpulm_internal.h"
 
 namespace ngpulm {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;   // threads per row (CTA)
+constexpr int kMinBlocks = 8;   // CTAs per SM (32 registers per thread)
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxL = NGPULM_MAX_ORDER;
+constexpr int kUnroll = 4;      // arcs gathered per thread per chunk
+constexpr int kChunk = kThreads * kUnroll;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kFull = 0xffffffffu;
 
-struct RowCtl {
-  int32_t beg[kMaxL];      // first arc of level i
-  int32_t pre[kMaxL + 1];  // prefix count of arcs over levels
-  float acc[kMaxL];        // acc_boff when level i is visited
-  float acc_root;          // acc_boff at the root level
-  float fin;               // final weight of the row's state (AED)
-  int32_t nlev;            // non-root levels
-  int32_t bad;             // invalid state id / corrupted chain
-  int32_t state;
-  int32_t prevc;           // CTC: previous frame's column
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) / 16 * 16; }
+__host__ __device__ constexpr int32_t level_cap(int32_t order) { return order > 1 ? order : 1; }
+__host__ __device__ constexpr size_t levels_bytes(int32_t order) {  // beg[Lc] pre[Lc+1] acc[Lc]
+  return align16(((size_t)3 * level_cap(order) + 1) * 4);
+}
+// row_s[V] | row_n[V] | scratch, barrier, row scalars | levels
+__host__ __device__ constexpr size_t row_smem(int32_t V, int32_t order) {
+  return 2 * align16((size_t)V * 4) + 128 + levels_bytes(order);
+}
+
+struct Row {  // per-row scalars
+  int32_t state, nlev, total, bad;
+  float acc_root, fin;
 };
 
-// Algorithm 1 lines 67-82 for one row, serial by nature (pointer chase).
-__device__ __forceinline__ void walk_chain(const DevModel& m, int32_t s, RowCtl& c) {
-  c.state = s;
-  c.acc_root = 0.f;
-  c.nlev = 0;
-  c.pre[0] = 0;
-  if (s < 0 || s >= m.S) { c.bad = 1; return; }
-  float acc = 0.f;
-  int32_t n = 0, pre = 0;
-  const int4* rec = reinterpret_cast<const int4*>(m.srec);
-  for (; n < kMaxL && s != 0; ++n) {
-    const int4 r = __ldg(rec + s);  // {arc_begin, arc_end, boff_to, boff_w}
-    c.beg[n] = r.x;
-    c.pre[n] = pre;
-    c.acc[n] = acc;
-    pre += r.y - r.x;
-    acc = __fadd_rn(acc, __int_as_float(r.w));  // acc_boff += boff_weights[state]
-    s = r.z;                                     // state = boff_to_states[state]
-  }
-  c.pre[n] = pre;
-  c.nlev = n;
-  c.acc_root = acc;
-  c.bad = (s != 0) ? 2 : 0;
+struct Slice {     // the row in shared memory
+  float* row_s;    // [V] score per token (root weight until step 2)
+  int32_t* row_n;  // [V] next state per token
+  float* red_v;    // argmax scratch [kWarps]
+  int32_t* red_c;
+  uint64_t* bar;   // mbarrier of the root bulk copy
+  Row* row;        // row scalars (written by warp 0)
+  int32_t* beg;    // levels: [Lc] first arc of level i
+  int32_t* pre;    // [Lc+1] prefix count of arcs (pre[nlev] = total)
+  float* acc;      // [Lc] acc_boff when level i is visited
+};
+
+__device__ __forceinline__ Slice carve(unsigned char* p, int32_t V, int32_t order) {
+  const int32_t Lc = level_cap(order);
+  Slice s;
+  s.row_s = reinterpret_cast<float*>(p);
+  p += align16((size_t)V * 4);
+  s.row_n = reinterpret_cast<int32_t*>(p);
+  p += align16((size_t)V * 4);
+  s.red_v = reinterpret_cast<float*>(p);
+  s.red_c = reinterpret_cast<int32_t*>(p + 32);
+  s.bar = reinterpret_cast<uint64_t*>(p + 64);
+  s.row = reinterpret_cast<Row*>(p + 72);
+  p += 128;
+  int32_t* l = reinterpret_cast<int32_t*>(p);
+  s.beg = l;
+  s.pre = l + Lc;
+  s.acc = reinterpret_cast<float*>(l + 2 * Lc + 1);
+  return s;
 }
 
-// Non-root levels -> shared-memory overrides; first (highest-order) level wins.
-__device__ __forceinline__ void scatter_levels(const DevModel& m, const RowCtl& c, uint32_t* lvl,
-                                               float* ovr_s, int32_t* ovr_n) {
-  const int32_t T = c.pre[c.nlev];
-  for (int32_t j = threadIdx.x; j < T; j += kThreads) {
-    int L = 0;
-    while (j >= c.pre[L + 1]) ++L;
-    const int32_t a = c.beg[L] + (j - c.pre[L]);
-    atomicMin(&lvl[__ldg(&m.arc_tok[a])], (uint32_t)L);
+#ifdef NGPULM_PHASE_TIMING
+// Debug build only (tools/phase_timing.py): per-row phase stamps (thread 0).
+__device__ unsigned long long g_phase[16384 * 8];
+__device__ __forceinline__ unsigned sm_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+#define PHASE(row, i)                                                                 \
+  do {                                                                                \
+    if (threadIdx.x == 0 && (row) < 16384) {                                          \
+      unsigned long long t;                                                           \
+      if ((i) == 0 || (i) == 7) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); \
+      else if ((i) == 3) t = sm_id();                                                 \
+      else t = clock64();                                                             \
+      g_phase[(row) * 8 + (i)] = t;                                                   \
+    }                                                                                 \
+  } while (0)
+#else
+#define PHASE(row, i) \
+  do {                \
+  } while (0)
+#endif
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t b = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(b), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
+// Step 0 (one thread of warp 1, so warp 0's state load is not queued behind
+// it): root level -> row slots by TMA bulk copy (SASS: UBLKCP). The barrier
+// init is made visible to the async proxy with a CTA-scope proxy fence.
+constexpr int kTmaThread = 32;
+__device__ __forceinline__ void prologue(const DevModel& m, const Slice& s, bool tma) {
+  if (threadIdx.x != kTmaThread) return;
+  const uint32_t b = smem_u32(s.bar), bytes = (uint32_t)m.V * 4u;
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (!tma) return;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(2u * bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(s.row_s)),
+               "l"(m.arc_w), "r"(bytes), "r"(b)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(s.row_n)),
+               "l"(m.arc_to), "r"(bytes), "r"(b)
+               : "memory");
+}
+
+// Step 1, warp 0: the row's levels into shared memory + the Row scalars.
+template <bool kTable>
+__device__ __forceinline__ Row load_levels(const DevModel& m, int32_t st, const Slice& s) {
+  const int lane = threadIdx.x & 31;
+  Row r;
+  r.state = st;
+  r.bad = st < 0 || st >= m.S;
+  r.nlev = 0; r.total = 0; r.acc_root = 0.f; r.fin = 0.f;
+  if (r.bad) return r;
+  if (kTable) {
+    // record = [header {nlev, acc_root, final, total}] + nlev x {begin, prefix, acc, 0}
+    const int4* rec = reinterpret_cast<const int4*>(m.chain) + (size_t)st * m.chain_slots;
+    int4 x = make_int4(0, 0, 0, 0);
+    if (lane < m.chain_slots) x = __ldg(rec + lane);
+    r.nlev = __shfl_sync(kFull, x.x, 0);
+    r.acc_root = __int_as_float(__shfl_sync(kFull, x.y, 0));
+    r.fin = __int_as_float(__shfl_sync(kFull, x.z, 0));
+    r.total = __shfl_sync(kFull, x.w, 0);
+    if (lane >= 1 && lane <= r.nlev) { s.beg[lane - 1] = x.x; s.pre[lane - 1] = x.y; s.acc[lane - 1] = __int_as_float(x.z); }
+    if (lane == 0) s.pre[r.nlev] = r.total;
+  } else {
+    // Algorithm 1 lines 67-82, serial by nature (pointer chase), lane 0
+    int32_t n = 0, pre = 0, bad = 0;
+    float acc = 0.f, fin = 0.f;
+    if (lane == 0) {
+      const int4* rec = reinterpret_cast<const int4*>(m.srec);
+      int32_t x = st;
+      for (; n < level_cap(m.order) && x != 0; ++n) {
+        const int4 q = __ldg(rec + x);  // {arc_begin, arc_end, boff_to, boff_w}
+        s.beg[n] = q.x;
+        s.pre[n] = pre;
+        s.acc[n] = acc;
+        pre += q.y - q.x;
+        acc = __fadd_rn(acc, __int_as_float(q.w));  // acc_boff += boff_weights[state]
+        x = q.z;                                     // state = boff_to_states[state]
+      }
+      s.pre[n] = pre;
+      bad = x != 0;
+      fin = bad ? 0.f : __ldg(&m.final_w[st]);
+    }
+    r.nlev = __shfl_sync(kFull, n, 0);
+    r.total = __shfl_sync(kFull, pre, 0);
+    r.acc_root = __shfl_sync(kFull, acc, 0);
+    r.fin = __shfl_sync(kFull, fin, 0);
+    r.bad = __shfl_sync(kFull, bad, 0);
+  }
+  return r;
+}
+
+// Warp 0 loads, everyone reads the result after one barrier.
+template <bool kTable>
+__device__ __forceinline__ Row row_levels(const DevModel& m, int32_t st_in, const Slice& s) {
+  if (threadIdx.x < 32) {
+    const Row rr = load_levels<kTable>(m, __shfl_sync(kFull, st_in, 0), s);
+    if (threadIdx.x == 0) *s.row = rr;
   }
   __syncthreads();
-  for (int32_t j = threadIdx.x; j < T; j += kThreads) {
-    int L = 0;
-    while (j >= c.pre[L + 1]) ++L;
-    const int32_t a = c.beg[L] + (j - c.pre[L]);
-    const int32_t tok = __ldg(&m.arc_tok[a]);
-    if (lvl[tok] == (uint32_t)L) {
-      ovr_s[tok] = __fadd_rn(c.acc[L], __ldg(&m.arc_w[a]));  // acc_boff + arc_weights
-      ovr_n[tok] = __ldg(&m.arc_to[a]);
+  return *s.row;
+}
+
+__device__ __forceinline__ int level_of(const Slice& s, int32_t j) {
+  int L = 0;
+  while (j >= s.pre[L + 1]) ++L;
+  return L;
+}
+
+struct Chunk {  // this thread's arcs of one chunk
+  uint32_t key[kUnroll];  // (level << 24) | token, kNone = no arc
+  float w[kUnroll];
+  int32_t to[kUnroll];
+};
+
+__device__ __forceinline__ void gather(const DevModel& m, const Slice& s, int32_t c0, int32_t T, Chunk& a) {
+  int L = 0;
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {  // all loads of the chunk in flight together
+    const int32_t j = c0 + u * kThreads + (int32_t)threadIdx.x;
+    a.key[u] = kNone;
+    if (j < T) {
+      while (j >= s.pre[L + 1]) ++L;
+      const int32_t arc = s.beg[L] + (j - s.pre[L]);
+      a.key[u] = ((uint32_t)L << 24) | (uint32_t)__ldg(&m.arc_tok[arc]);
+      a.w[u] = __ldg(&m.arc_w[arc]);
+      a.to[u] = __ldg(&m.arc_to[arc]);
     }
   }
-  __syncthreads();
 }
 
-__device__ __forceinline__ void init_lvl(uint32_t* lvl, int32_t V) {
-  for (int32_t v = threadIdx.x; v < V; v += kThreads) lvl[v] = kNone;
+// Step 3 for one chunk: levels from the highest index (lowest order) down.
+__device__ __forceinline__ void write_levels(const Slice& s, int32_t c0, int32_t T, const Chunk& a) {
+  const int Lhi = level_of(s, min(c0 + kChunk, T) - 1), Llo = level_of(s, c0);
+  for (int L = Lhi; L >= Llo; --L) {
+    const float acc = s.acc[L];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (a.key[u] == kNone || (int)(a.key[u] >> 24) != L) continue;
+      const uint32_t tok = a.key[u] & 0xFFFFFFu;
+      s.row_s[tok] = __fadd_rn(acc, a.w[u]);  // acc_boff + arc_weights (Alg. 1 line 74)
+      s.row_n[tok] = a.to[u];
+    }
+    __syncthreads();
+  }
 }
 
-// ---------------------------------------------------------------- advance
-template <bool kVec4>
-__global__ void __launch_bounds__(kThreads) advance_kernel(DevModel m, const int32_t* __restrict__ states,
-                                                           float* __restrict__ scores,
-                                                           int32_t* __restrict__ next,
-                                                           float* __restrict__ final_out) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int32_t V = m.V;
-  uint32_t* lvl = reinterpret_cast<uint32_t*>(smem);
-  float* ovr_s = reinterpret_cast<float*>(lvl + V);
-  int32_t* ovr_n = reinterpret_cast<int32_t*>(ovr_s + V);
-  __shared__ RowCtl c;
-  const int32_t b = blockIdx.x;
-  if (threadIdx.x == 0) {
-    walk_chain(m, __ldg(&states[b]), c);
-    if (c.bad) atomicMin(m.bad_row, (unsigned long long)b);
-    if (final_out) final_out[b] = c.bad ? __int_as_float(0x7fc00000) : __ldg(&m.final_w[c.state]);
-  }
-  init_lvl(lvl, V);
-  __syncthreads();
-  float* srow = scores + (size_t)b * V;
-  int32_t* nrow = next + (size_t)b * V;
-  if (c.bad) {
-    for (int32_t v = threadIdx.x; v < V; v += kThreads) { srow[v] = __int_as_float(0x7fc00000); nrow[v] = -1; }
-    return;
-  }
-  scatter_levels(m, c, lvl, ovr_s, ovr_n);
-  const float acc_root = c.acc_root;
-  if (kVec4) {
-    const float4* rw4 = reinterpret_cast<const float4*>(m.arc_w);  // root arcs = [0, V)
-    const int4* rt4 = reinterpret_cast<const int4*>(m.arc_to);
+// Steps 2-3: root slots get acc_root; non-root arcs overwrite, lowest order
+// first. Chunks run from the last (lowest-order) arcs to the first. The first
+// gather is issued before the root fix-up so their latencies overlap.
+__device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, const Row& r, bool tma) {
+  const int32_t V = m.V, T = r.total;
+  const float acc_root = r.acc_root;
+  int32_t c0 = T > 0 ? ((T - 1) / kChunk) * kChunk : 0;
+  Chunk a;
+  if (T > 0) gather(m, s, c0, T, a);
+  if (tma) mbar_wait(s.bar, 0);
+  if ((V & 3) == 0 && tma) {
+    float4* s4 = reinterpret_cast<float4*>(s.row_s);
     for (int32_t q = threadIdx.x; q < V / 4; q += kThreads) {
-      const uint4 l = reinterpret_cast<const uint4*>(lvl)[q];
-      const float4 rw = __ldg(rw4 + q);
-      const int4 rt = __ldg(rt4 + q);
-      const int32_t v = q * 4;
-      float4 o;
-      int4 n;
-      o.x = l.x != kNone ? ovr_s[v + 0] : __fadd_rn(acc_root, rw.x);
-      o.y = l.y != kNone ? ovr_s[v + 1] : __fadd_rn(acc_root, rw.y);
-      o.z = l.z != kNone ? ovr_s[v + 2] : __fadd_rn(acc_root, rw.z);
-      o.w = l.w != kNone ? ovr_s[v + 3] : __fadd_rn(acc_root, rw.w);
-      n.x = l.x != kNone ? ovr_n[v + 0] : rt.x;
-      n.y = l.y != kNone ? ovr_n[v + 1] : rt.y;
-      n.z = l.z != kNone ? ovr_n[v + 2] : rt.z;
-      n.w = l.w != kNone ? ovr_n[v + 3] : rt.w;
-      __stcs(reinterpret_cast<float4*>(srow) + q, o);
-      __stcs(reinterpret_cast<int4*>(nrow) + q, n);
+      float4 x = s4[q];
+      x.x = __fadd_rn(acc_root, x.x);  // root level: acc_root + root weight
+      x.y = __fadd_rn(acc_root, x.y);
+      x.z = __fadd_rn(acc_root, x.z);
+      x.w = __fadd_rn(acc_root, x.w);
+      s4[q] = x;
     }
   } else {
     for (int32_t v = threadIdx.x; v < V; v += kThreads) {
-      const bool hit = lvl[v] != kNone;
-      __stcs(srow + v, hit ? ovr_s[v] : __fadd_rn(acc_root, __ldg(&m.arc_w[v])));
-      __stcs(nrow + v, hit ? ovr_n[v] : __ldg(&m.arc_to[v]));
+      s.row_s[v] = __fadd_rn(acc_root, __ldg(&m.arc_w[v]));
+      s.row_n[v] = __ldg(&m.arc_to[v]);
     }
   }
+  __syncthreads();
+  if (T == 0) return;
+  for (;;) {
+    write_levels(s, c0, T, a);
+    c0 -= kChunk;
+    if (c0 < 0) break;
+    gather(m, s, c0, T, a);
+  }
+}
+
+// ---------------------------------------------------------------- advance
+template <bool kVec4, bool kTable>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    advance_kernel(DevModel m, const int32_t* __restrict__ states, float* __restrict__ scores,
+                   int32_t* __restrict__ next, float* __restrict__ final_out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int32_t V = m.V, b = blockIdx.x;
+  const int t = threadIdx.x;
+  const Slice s = carve(smem, V, m.order);
+  PHASE(b, 0);
+  PHASE(b, 1);
+  pdl_trigger();
+  prologue(m, s, kVec4);
+  pdl_wait();
+  PHASE(b, 2);
+  const Row r = row_levels<kTable>(m, t == 0 ? __ldg(&states[b]) : 0, s);
+  PHASE(b, 5);
+  PHASE(b, 3);
+  if (t == 0) {
+    if (r.bad) atomicMin(m.bad_row, (unsigned long long)b);
+    if (final_out) final_out[b] = r.bad ? __int_as_float(0x7fc00000) : r.fin;
+  }
+  float* srow = scores + (size_t)b * V;
+  int32_t* nrow = next + (size_t)b * V;
+  if (r.bad) {
+    for (int32_t v = t; v < V; v += kThreads) { srow[v] = __int_as_float(0x7fc00000); nrow[v] = -1; }
+    if (kVec4) mbar_wait(s.bar, 0);  // no exit with the bulk copy in flight
+    return;
+  }
+  build_row(m, s, r, kVec4);
+  PHASE(b, 4);
+  if (kVec4) {
+    // step 4: the finished row leaves by TMA bulk stores (SASS: UBLKCP shared -> global)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> async proxy
+    __syncthreads();
+    if (t == 0) {
+      const uint32_t bytes = (uint32_t)V * 4u;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(srow),
+                   "r"(smem_u32(s.row_s)), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(nrow),
+                   "r"(smem_u32(s.row_n)), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem stays valid until read
+    }
+  } else {
+    for (int32_t v = t; v < V; v += kThreads) {
+      __stcs(srow + v, s.row_s[v]);
+      __stcs(nrow + v, s.row_n[v]);
+    }
+  }
+  PHASE(b, 6);
+  PHASE(b, 7);
 }
 
 // ---------------------------------------------------------------- final
 __global__ void final_kernel(DevModel m, const int32_t* __restrict__ states, int32_t B,
                              float* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int32_t b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const int32_t s = __ldg(&states[b]);
@@ -173,174 +374,180 @@ __device__ __forceinline__ bool better(float v2, int32_t c2, float v, int32_t c)
   return v2 > v || (v2 == v && c2 < c);
 }
 
-__device__ __forceinline__ void block_argmax(float& v, int32_t& c, float* sv, int32_t* sc) {
+// argmax over the CTA: warp shuffles, then the warp winners via smem.
+__device__ __forceinline__ void cta_argmax(float& v, int32_t& c, const Slice& s) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    const float v2 = __shfl_xor_sync(0xffffffffu, v, o);
-    const int32_t c2 = __shfl_xor_sync(0xffffffffu, c, o);
+    const float v2 = __shfl_xor_sync(kFull, v, o);
+    const int32_t c2 = __shfl_xor_sync(kFull, c, o);
     if (better(v2, c2, v, c)) { v = v2; c = c2; }
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) { sv[warp] = v; sc[warp] = c; }
+  if ((threadIdx.x & 31) == 0) { s.red_v[threadIdx.x >> 5] = v; s.red_c[threadIdx.x >> 5] = c; }
   __syncthreads();
-  if (warp == 0) {
-    v = lane < kWarps ? sv[lane] : -INFINITY;
-    c = lane < kWarps ? sc[lane] : INT_MAX;
+  v = s.red_v[0];
+  c = s.red_c[0];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const float v2 = __shfl_xor_sync(0xffffffffu, v, o);
-      const int32_t c2 = __shfl_xor_sync(0xffffffffu, c, o);
-      if (better(v2, c2, v, c)) { v = v2; c = c2; }
-    }
-    if (lane == 0) { sv[kWarps] = v; sc[kWarps] = c; }
-  }
-  __syncthreads();
-  v = sv[kWarps];
-  c = sc[kWarps];
+  for (int i = 1; i < kWarps; ++i)
+    if (better(s.red_v[i], s.red_c[i], v, c)) { v = s.red_v[i]; c = s.red_c[i]; }
+  __syncthreads();  // scratch reusable
 }
 
-template <int kMode>
-__global__ void __launch_bounds__(kThreads) fused_kernel(DevModel m, const float* __restrict__ logits,
-                                                         int64_t row_stride, int32_t* __restrict__ states,
-                                                         int32_t* __restrict__ prev,
-                                                         const uint8_t* __restrict__ active, float lambda,
-                                                         int32_t sp, int32_t* __restrict__ tokens_out) {
+template <int kMode, bool kTable>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    fused_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int32_t* __restrict__ states,
+                 int32_t* __restrict__ prev, const uint8_t* __restrict__ active, float lambda, int32_t sp,
+                 int32_t* __restrict__ tokens_out) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int32_t V = m.V, ncols = V + 1;
-  uint32_t* lvl = reinterpret_cast<uint32_t*>(smem);
-  float* ovr_s = reinterpret_cast<float*>(lvl + V);
-  int32_t* ovr_n = reinterpret_cast<int32_t*>(ovr_s + V);
-  __shared__ RowCtl c;
-  __shared__ float sv[kWarps + 1];
-  __shared__ int32_t sc[kWarps + 1];
-  const int32_t b = blockIdx.x;
+  const int32_t V = m.V, ncols = V + 1, b = blockIdx.x;
+  const int t = threadIdx.x;
+  const Slice s = carve(smem, V, m.order);
+  const bool tma = (V & 3) == 0;
+  pdl_trigger();
+  prologue(m, s, tma);
+  pdl_wait();
   if (active && !__ldg(&active[b])) {
-    if (threadIdx.x == 0) tokens_out[b] = -1;
+    if (t == 0) tokens_out[b] = -1;
+    __syncthreads();  // mbarrier init visible
+    if (tma) mbar_wait(s.bar, 0);
     return;
   }
   const float* row = logits + (size_t)b * row_stride;
-  if (threadIdx.x == 0) {
-    walk_chain(m, states[b], c);
-    if (c.bad) atomicMin(m.bad_row, (unsigned long long)b);
-    if (kMode == NGPULM_CTC) c.prevc = prev[b];
-    if (kMode == NGPULM_AED) c.fin = c.bad ? 0.f : __ldg(&m.final_w[c.state]);
-  }
-  init_lvl(lvl, V);
+  const int32_t pc = (kMode == NGPULM_CTC) ? prev[b] : -2;
+  float bv = -INFINITY;
+  int32_t bc = INT_MAX;
   if (kMode == NGPULM_RNNT) {
-    // stage 1: standard greedy prediction over all V+1 columns
-    float bv = -INFINITY;
-    int32_t bc = INT_MAX;
-    for (int32_t col = threadIdx.x; col < ncols; col += kThreads) {
+    // stage 1: standard greedy prediction over all V+1 columns,
+    // its loads issued before the row's levels are needed
+    for (int32_t col = t; col < ncols; col += kThreads) {
       const float a = __ldg(&row[col]);
       if (better(a, col, bv, bc)) { bv = a; bc = col; }
     }
-    block_argmax(bv, bc, sv, sc);  // includes __syncthreads: c is visible after it
-    if (c.bad) {
-      if (threadIdx.x == 0) tokens_out[b] = -1;
-      return;
-    }
-    if (bc == sp) {                // blank is retained: no LM work, state unchanged
-      if (threadIdx.x == 0) tokens_out[b] = sp;
-      return;
-    }
-  } else {
-    __syncthreads();
-    if (c.bad) {
-      if (threadIdx.x == 0) tokens_out[b] = -1;
-      return;
-    }
   }
-  scatter_levels(m, c, lvl, ovr_s, ovr_n);
-  const float acc_root = c.acc_root;
-  const int32_t pc = (kMode == NGPULM_CTC) ? c.prevc : -2;
-  float bv = -INFINITY;
-  int32_t bc = INT_MAX;
-  for (int32_t col = threadIdx.x; col < ncols; col += kThreads) {
+  const Row r = row_levels<kTable>(m, t == 0 ? states[b] : 0, s);
+  if (r.bad) {
+    if (t == 0) { tokens_out[b] = -1; atomicMin(m.bad_row, (unsigned long long)b); }
+    if (tma) mbar_wait(s.bar, 0);
+    return;
+  }
+  if (kMode == NGPULM_RNNT) {
+    cta_argmax(bv, bc, s);
+    if (bc == sp) {  // blank is retained: no LM work, state unchanged
+      if (t == 0) tokens_out[b] = sp;
+      if (tma) mbar_wait(s.bar, 0);
+      return;
+    }
+    bv = -INFINITY;
+    bc = INT_MAX;
+  }
+  build_row(m, s, r, tma);
+  for (int32_t col = t; col < ncols; col += kThreads) {
     const float a = __ldg(&row[col]);
     float val;
     if (col == sp) {
-      if (kMode == NGPULM_RNNT) continue;                  // stage 2: non-blank only
-      val = (kMode == NGPULM_AED) ? __fmaf_rn(lambda, c.fin, a) : a;  // eos <-> final / blank raw
+      if (kMode == NGPULM_RNNT) continue;                             // stage 2: non-blank only
+      val = (kMode == NGPULM_AED) ? __fmaf_rn(lambda, r.fin, a) : a;  // eos <-> final / blank raw
     } else if (kMode == NGPULM_CTC && col == pc) {
-      val = a;                                             // repeated token: not rescored
+      val = a;                                                        // repeated token: not rescored
     } else {
-      const int32_t v = col < sp ? col : col - 1;
-      const float lm = lvl[v] != kNone ? ovr_s[v] : __fadd_rn(acc_root, __ldg(&m.arc_w[v]));
-      val = __fmaf_rn(lambda, lm, a);                      // asr + lambda * lm, one rounding
+      val = __fmaf_rn(lambda, s.row_s[col < sp ? col : col - 1], a);  // asr + lambda * lm, one rounding
     }
     if (better(val, col, bv, bc)) { bv = val; bc = col; }
   }
-  block_argmax(bv, bc, sv, sc);
-  if (threadIdx.x == 0) {
-    if (bc < 0 || bc >= ncols) { tokens_out[b] = -1; return; }  // all-NaN row (unspecified)
-    tokens_out[b] = bc;
-    if (bc == sp) {
-      if (kMode == NGPULM_CTC) prev[b] = -1;
-      return;
+  cta_argmax(bv, bc, s);
+  if (t == 0) {
+    if (bc < 0 || bc >= ncols) {
+      tokens_out[b] = -1;  // all-NaN row (unspecified)
+    } else {
+      tokens_out[b] = bc;
+      if (bc == sp) {
+        if (kMode == NGPULM_CTC) prev[b] = -1;
+      } else if (!(kMode == NGPULM_CTC && bc == pc)) {  // a repeated CTC token: no LM advance
+        states[b] = s.row_n[bc < sp ? bc : bc - 1];
+        if (kMode == NGPULM_CTC) prev[b] = bc;
+      }
     }
-    if (kMode == NGPULM_CTC && bc == pc) return;            // collapsed: no LM advance
-    const int32_t v = bc < sp ? bc : bc - 1;
-    states[b] = lvl[v] != kNone ? ovr_n[v] : __ldg(&m.arc_to[v]);
-    if (kMode == NGPULM_CTC) prev[b] = bc;
   }
 }
 
-size_t row_smem(int32_t V) { return (size_t)V * 12; }
-
-int set_smem(const void* fn, size_t bytes) {
-  if (bytes <= 48 * 1024) return cudaSuccess;
-  return (int)cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+// ---------------------------------------------------------------- launch
+template <typename... KArgs, typename... Args>
+int launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
 }  // namespace
 
+#ifdef NGPULM_PHASE_TIMING
+extern "C" int ngpulm_debug_phases(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_phase, sizeof(unsigned long long) * (size_t)n);
+}
+#endif
+
 int max_vocab_supported() {
-  return (int)((227 * 1024 - (int)sizeof(RowCtl) - 2 * 64) / 12) & ~3;
+  int v = 32768;
+  while (v > 0 && row_smem(v, NGPULM_MAX_ORDER) > 227 * 1024) v -= 4;
+  return v;
 }
 
 int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* scores, int32_t* next,
                    float* final_out, void* stream) {
-  const size_t sm = row_smem(m.V);
+  const size_t sm = row_smem(m.V, m.order);
   const bool vec = (m.V % 4 == 0) && ((uintptr_t)scores % 16 == 0) && ((uintptr_t)next % 16 == 0);
+  const bool table = m.chain != nullptr;
   cudaStream_t st = (cudaStream_t)stream;
-  if (vec) {
-    if (int e = set_smem((const void*)advance_kernel<true>, sm)) return e;
-    advance_kernel<true><<<B, kThreads, sm, st>>>(m, states, scores, next, final_out);
-  } else {
-    if (int e = set_smem((const void*)advance_kernel<false>, sm)) return e;
-    advance_kernel<false><<<B, kThreads, sm, st>>>(m, states, scores, next, final_out);
-  }
-  return (int)cudaGetLastError();
+  const dim3 gd(B), bd(kThreads);
+  if (vec && table) return launch(advance_kernel<true, true>, gd, bd, sm, st, m, states, scores, next, final_out);
+  if (vec) return launch(advance_kernel<true, false>, gd, bd, sm, st, m, states, scores, next, final_out);
+  if (table) return launch(advance_kernel<false, true>, gd, bd, sm, st, m, states, scores, next, final_out);
+  return launch(advance_kernel<false, false>, gd, bd, sm, st, m, states, scores, next, final_out);
 }
 
 int launch_final(const DevModel& m, const int32_t* states, int32_t B, float* out, void* stream) {
-  final_kernel<<<(B + 255) / 256, 256, 0, (cudaStream_t)stream>>>(m, states, B, out);
-  return (int)cudaGetLastError();
+  return launch(final_kernel, dim3((B + 255) / 256), dim3(256), 0, (cudaStream_t)stream, m, states, B, out);
+}
+
+template <int kMode>
+int launch_fused_mode(const DevModel& m, const float* logits, int64_t row_stride, int32_t B, int32_t* states,
+                      int32_t* prev, const uint8_t* active, float lambda, int32_t blank, int32_t* tokens_out,
+                      cudaStream_t st) {
+  const size_t sm = row_smem(m.V, m.order);
+  const dim3 gd(B), bd(kThreads);
+  if (m.chain != nullptr)
+    return launch(fused_kernel<kMode, true>, gd, bd, sm, st, m, logits, row_stride, states, prev, active, lambda,
+                  blank, tokens_out);
+  return launch(fused_kernel<kMode, false>, gd, bd, sm, st, m, logits, row_stride, states, prev, active, lambda,
+                blank, tokens_out);
 }
 
 int launch_fused(const DevModel& m, int32_t mode, const float* logits, int64_t row_stride, int32_t B,
                  int32_t* states, int32_t* prev, const uint8_t* active, float lambda, int32_t blank,
                  int32_t* tokens_out, void* stream) {
-  const size_t sm = row_smem(m.V);
   cudaStream_t st = (cudaStream_t)stream;
   switch (mode) {
     case NGPULM_CTC:
-      if (int e = set_smem((const void*)fused_kernel<NGPULM_CTC>, sm)) return e;
-      fused_kernel<NGPULM_CTC><<<B, kThreads, sm, st>>>(m, logits, row_stride, states, prev, active, lambda,
-                                                        blank, tokens_out);
-      break;
+      return launch_fused_mode<NGPULM_CTC>(m, logits, row_stride, B, states, prev, active, lambda, blank,
+                                           tokens_out, st);
     case NGPULM_RNNT:
-      if (int e = set_smem((const void*)fused_kernel<NGPULM_RNNT>, sm)) return e;
-      fused_kernel<NGPULM_RNNT><<<B, kThreads, sm, st>>>(m, logits, row_stride, states, prev, active, lambda,
-                                                         blank, tokens_out);
-      break;
+      return launch_fused_mode<NGPULM_RNNT>(m, logits, row_stride, B, states, prev, active, lambda, blank,
+                                            tokens_out, st);
     default:
-      if (int e = set_smem((const void*)fused_kernel<NGPULM_AED>, sm)) return e;
-      fused_kernel<NGPULM_AED><<<B, kThreads, sm, st>>>(m, logits, row_stride, states, prev, active, lambda,
-                                                        blank, tokens_out);
-      break;
+      return launch_fused_mode<NGPULM_AED>(m, logits, row_stride, B, states, prev, active, lambda, blank,
+                                           tokens_out, st);
   }
-  return (int)cudaGetLastError();
 }
 
 }  // namespace ngpulm

@@ -38,6 +38,14 @@ struct HostModel {
 int build_from_arpa(const char* arpa_path, const char* vocab_path, int32_t vocab_size,
                     HostModel& out, std::string& err);
 
+// Load-time chain table (DESIGN.md §Kernels "chain table"): per state a fixed
+// record of `slots` int4: slot 0 = {nlev, acc_root, final, total_arcs}, slots
+// 1..nlev = {arc_begin, arc_prefix, acc_boff, 0} for every level of the
+// back-off chain that has arcs, in Algorithm 1 order; padding slots =
+// {0, total_arcs, 0, 0}. acc_boff is accumulated exactly as Algorithm 1 does
+// (left to right, float). slots = max(1, order).
+void build_chain_table(const HostModel& m, std::vector<int32_t>& out, int32_t& slots);
+
 // Device-side view passed to kernels by value.
 struct DevModel {
   const StateRec* srec;
@@ -45,6 +53,9 @@ struct DevModel {
   const int32_t* arc_tok;
   const float* arc_w;
   const int32_t* arc_to;
+  const int32_t* root_tag;  // [V] root arc targets with bit 31 set: "root level" tag (kernels.cu)
+  const void* chain;  // chain table (int4 records) or nullptr = walk the chain at query time
+  int32_t chain_slots;
   int32_t S, V, order;
   unsigned long long* bad_row;  // sticky min bad row (ULLONG_MAX = none)
 };

@@ -46,12 +46,18 @@ def gpu_advance(m, states_np):
     return s.cpu().numpy(), n.cpu().numpy(), f.cpu().numpy()
 
 
+@pytest.mark.parametrize("chain", [ng.CHAIN_TABLE, ng.CHAIN_WALK])
 @pytest.mark.parametrize("name", SMALL + ["fig1"])
-def test_advance_exhaustive_small(pairs, name):
-    """All states x all tokens of every small LM (config 0 = tiny3)."""
+def test_advance_exhaustive_small(pairs, name, chain):
+    """All states x all tokens of every small LM (config 0 = tiny3), both ways of
+    obtaining the back-off levels (load-time chain table / Algorithm 1 walk)."""
     m, o, _ = pairs[name]
+    m.set_chain_mode(chain)
     states = np.arange(o.num_states, dtype=np.int32)
-    s, n, f = gpu_advance(m, states)
+    try:
+        s, n, f = gpu_advance(m, states)
+    finally:
+        m.set_chain_mode(ng.CHAIN_TABLE)
     s32, s64, n_o, _ = o.rows(states)
     f32, f64 = o.finals(states)
     assert np.array_equal(n, n_o)
@@ -113,14 +119,19 @@ def trajectory_states(m, f, n, seed):
     return np.array([m.state_of(b, t) for b, t in ctx], dtype=np.int32), ctx
 
 
-def test_config1_b128_full_rows(lm6):
+@pytest.mark.parametrize("chain", [ng.CHAIN_TABLE, ng.CHAIN_WALK])
+def test_config1_b128_full_rows(lm6, chain):
     m, o, f = lm6
+    m.set_chain_mode(chain)
     assert m.info.num_arcs > 500_000 and 800_000 < sum(1 for _ in open(f.arpa)) < 1_300_000
     st_traj, ctx = trajectory_states(m, f, 96, seed=2)
     # the library's and the oracle's context -> state maps agree (R6, R7)
     assert [o.state_of(b, t) for b, t in ctx] == st_traj.tolist()
     states = np.concatenate([st_traj, synth.uniform_states(m.num_states, 32, seed=3)])
-    s, n, fin = gpu_advance(m, states)
+    try:
+        s, n, fin = gpu_advance(m, states)
+    finally:
+        m.set_chain_mode(ng.CHAIN_TABLE)
     s32, s64, n_o, lv = o.rows(states)
     f32, _ = o.finals(states)
     assert np.array_equal(n, n_o) and same_bits(s, s32) and same_bits(fin, f32)
@@ -179,11 +190,13 @@ def gpu_step(m, mode, logits_np, states, prev=None, active=None, lam=0.3, blank=
     return tok.cpu().numpy(), st.cpu().numpy(), (pv.cpu().numpy() if pv is not None else None)
 
 
+@pytest.mark.parametrize("chain", [ng.CHAIN_TABLE, ng.CHAIN_WALK])
 @pytest.mark.parametrize("mode", [CTC, RNNT, AED])
 @pytest.mark.parametrize("lam", [0.0, 0.3, 3.0])
 @pytest.mark.parametrize("name", ["tiny3", "five48", "ten24"])
-def test_fused_step_matches_oracle(pairs, mode, lam, name):
+def test_fused_step_matches_oracle(pairs, mode, lam, name, chain):
     m, o, _ = pairs[name]
+    m.set_chain_mode(chain)
     rng = np.random.default_rng(17)
     B = 300
     x = synth.rnnt_logits(B, 1, o.V, seed=9)[0]
@@ -192,7 +205,10 @@ def test_fused_step_matches_oracle(pairs, mode, lam, name):
     prev = rng.integers(-1, o.V + 1, size=B).astype(np.int32)
     prev[prev == o.V] = -1
     active = (rng.random(B) > 0.1).astype(np.uint8)
-    tg, sg, pg = gpu_step(m, mode, x, states, prev if mode == CTC else None, active, lam)
+    try:
+        tg, sg, pg = gpu_step(m, mode, x, states, prev if mode == CTC else None, active, lam)
+    finally:
+        m.set_chain_mode(ng.CHAIN_TABLE)
     to, so, po = o.fused_step(mode, x, states, prev=prev if mode == CTC else None, active=active, lam=lam)
     assert np.array_equal(tg, to) and np.array_equal(sg, so)
     if mode == CTC:

@@ -1,0 +1,41 @@
+"""Profiling driver: the bench's advance launch (6-gram, V=1024, B trajectory rows).
+Run under ncu on the GPU box, e.g.
+  ncu --set full --clock-control none --import-source on -k regex:advance -s 10 -c 3 \
+      -o gpurun_out/prof_adv python tools/prof_advance.py
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2505_22857_b200 as ng  # noqa: E402
+import synth  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--batch", type=int, default=1024)
+p.add_argument("--iters", type=int, default=20)
+p.add_argument("--mode", default="advance", choices=["advance", "ctc", "rnnt", "aed"])
+a = p.parse_args()
+f = synth.make_lm("/tmp/ngpulm_prof", 1024, 6, tokens=430000, seed=1, heldout=4000, tag="bench_6gram")
+m = ng.load_arpa(f.arpa, vocab_size=1024, device=0)
+ctx = synth.sample_contexts(synth.read_sentences(f.heldout), 6, a.batch * 4, seed=2)
+st_np = np.array([m.state_of(b, t) for b, t in ctx], dtype=np.int32).reshape(4, a.batch)
+st = torch.from_numpy(st_np).cuda()
+if a.mode == "advance":
+    sc = torch.empty((4, a.batch, 1024), dtype=torch.float32, device="cuda")
+    nx = torch.empty((4, a.batch, 1024), dtype=torch.int32, device="cuda")
+    fi = torch.empty((4, a.batch), dtype=torch.float32, device="cuda")
+    for i in range(a.iters):
+        m.advance(st[i % 4], sc[i % 4], nx[i % 4], fi[i % 4])
+else:
+    mode = {"ctc": ng.CTC, "rnnt": ng.RNNT, "aed": ng.AED}[a.mode]
+    x = torch.from_numpy(synth.rnnt_logits(a.batch, 4, 1024, seed=4)).cuda()
+    pv = torch.full((a.batch,), -1, dtype=torch.int32, device="cuda")
+    for i in range(a.iters):
+        s = st[i % 4].clone()
+        m.fused_greedy_step(mode, x[i % 4], s, prev=pv, lam=0.3)
+torch.cuda.synchronize()
+print("done")
