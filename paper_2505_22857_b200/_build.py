@@ -24,6 +24,15 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Tuning variants (tools/): same sources, other compile-time constants."""
+    out = os.path.join(LIBDIR, f"libngpulm_{name}.so")
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-o", out,
+           *[os.path.join(CSRC, s) for s in SOURCES]]
+    subprocess.run(cmd, check=True)
+    return out
+
+
 def build_phase_timing() -> str:
     """Debug variant with per-CTA phase stamps (tools/phase_timing.py); not the product."""
     out = os.path.join(LIBDIR, "libngpulm_timing.so")

@@ -41,12 +41,17 @@
 namespace ngpulm {
 namespace {
 
-constexpr int kThreads = 256;   // threads per row (CTA)
-constexpr int kMinBlocks = 8;   // CTAs per SM (32 registers per thread)
+#ifndef NGPULM_THREADS
+#define NGPULM_THREADS 256
+#endif
+#ifndef NGPULM_UNROLL
+#define NGPULM_UNROLL 4
+#endif
+constexpr int kThreads = NGPULM_THREADS;   // threads per row (CTA)
+constexpr int kMinBlocks = 2048 / kThreads;  // CTAs per SM: 64 warps, 32 registers per thread
 constexpr int kWarps = kThreads / 32;
-constexpr int kUnroll = 4;      // arcs gathered per thread per chunk
+constexpr int kUnroll = NGPULM_UNROLL;     // arcs gathered per thread per chunk
 constexpr int kChunk = kThreads * kUnroll;
-constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kFull = 0xffffffffu;
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) / 16 * 16; }
@@ -54,9 +59,9 @@ __host__ __device__ constexpr int32_t level_cap(int32_t order) { return order > 
 __host__ __device__ constexpr size_t levels_bytes(int32_t order) {  // beg[Lc] pre[Lc+1] acc[Lc]
   return align16(((size_t)3 * level_cap(order) + 1) * 4);
 }
-// row_s[V] | row_n[V] | scratch, barrier, row scalars | levels
+// row_s[V] | row_n[V] | st_tok/st_s/st_n[kChunk] | scratch, barrier, row scalars | levels
 __host__ __device__ constexpr size_t row_smem(int32_t V, int32_t order) {
-  return 2 * align16((size_t)V * 4) + 128 + levels_bytes(order);
+  return 2 * align16((size_t)V * 4) + (size_t)kChunk * 12 + 128 + levels_bytes(order);
 }
 
 struct Row {  // per-row scalars
@@ -71,6 +76,9 @@ struct Slice {     // the row in shared memory
   int32_t* red_c;
   uint64_t* bar;   // mbarrier of the root bulk copy
   Row* row;        // row scalars (written by warp 0)
+  int32_t* st_tok; // [kChunk] staged arcs of the current round: token
+  float* st_s;     //          acc_boff + arc weight
+  int32_t* st_n;   //          target
   int32_t* beg;    // levels: [Lc] first arc of level i
   int32_t* pre;    // [Lc+1] prefix count of arcs (pre[nlev] = total)
   float* acc;      // [Lc] acc_boff when level i is visited
@@ -83,6 +91,10 @@ __device__ __forceinline__ Slice carve(unsigned char* p, int32_t V, int32_t orde
   p += align16((size_t)V * 4);
   s.row_n = reinterpret_cast<int32_t*>(p);
   p += align16((size_t)V * 4);
+  s.st_tok = reinterpret_cast<int32_t*>(p);
+  s.st_s = reinterpret_cast<float*>(p + kChunk * 4);
+  s.st_n = reinterpret_cast<int32_t*>(p + kChunk * 8);
+  p += (size_t)kChunk * 12;
   s.red_v = reinterpret_cast<float*>(p);
   s.red_c = reinterpret_cast<int32_t*>(p + 32);
   s.bar = reinterpret_cast<uint64_t*>(p + 64);
@@ -96,26 +108,37 @@ __device__ __forceinline__ Slice carve(unsigned char* p, int32_t V, int32_t orde
 }
 
 #ifdef NGPULM_PHASE_TIMING
-// Debug build only (tools/phase_timing.py): per-row phase stamps (thread 0).
-__device__ unsigned long long g_phase[16384 * 8];
-__device__ __forceinline__ unsigned sm_id() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
-  return r;
+// Debug build only (tools/phase_timing.py): per-row stamps of thread 0, kept
+// in shared memory during the row (so the stamps add no global traffic) and
+// written out at the end: 0 entry (globaltimer ns), 1 entry, 2 after
+// griddepcontrol.wait, 3 levels published, 4 arcs staged, 5 root fix-up
+// barrier, 6 levels written, 7 stores issued (clock64), 8 end (ns), 9 SM id.
+__device__ unsigned long long g_phase[16384 * 16];
+__device__ __forceinline__ unsigned long long* stamp_buf() {
+  __shared__ unsigned long long buf[16];
+  return buf;
 }
-#define PHASE(row, i)                                                                 \
-  do {                                                                                \
-    if (threadIdx.x == 0 && (row) < 16384) {                                          \
-      unsigned long long t;                                                           \
-      if ((i) == 0 || (i) == 7) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); \
-      else if ((i) == 3) t = sm_id();                                                 \
-      else t = clock64();                                                             \
-      g_phase[(row) * 8 + (i)] = t;                                                   \
-    }                                                                                 \
+#define STAMP(i)                                                                        \
+  do {                                                                                  \
+    if (threadIdx.x == 0) {                                                             \
+      unsigned long long t;                                                             \
+      if ((i) == 0 || (i) == 8) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));   \
+      else if ((i) == 9) asm volatile("mov.u32 %0, %%smid;" : "=r"(*(unsigned*)&t));   \
+      else t = clock64();                                                               \
+      stamp_buf()[i] = t;                                                               \
+    }                                                                                   \
+  } while (0)
+#define STAMPS_OUT(row)                                                                 \
+  do {                                                                                  \
+    if (threadIdx.x == 0 && (row) < 16384)                                              \
+      for (int _i = 0; _i < 10; ++_i) g_phase[(row) * 16 + _i] = stamp_buf()[_i];       \
   } while (0)
 #else
-#define PHASE(row, i) \
-  do {                \
+#define STAMP(i) \
+  do {           \
+  } while (0)
+#define STAMPS_OUT(row) \
+  do {                  \
   } while (0)
 #endif
 
@@ -222,53 +245,60 @@ __device__ __forceinline__ int level_of(const Slice& s, int32_t j) {
   return L;
 }
 
-struct Chunk {  // this thread's arcs of one chunk
-  uint32_t key[kUnroll];  // (level << 24) | token, kNone = no arc
+// Step 2 for one round of arcs [lo, hi) (hi - lo <= kChunk): every thread
+// loads its (up to kUnroll) arcs — all loads in flight together — and stages
+// them in shared memory at slot j - lo as (token, acc_boff + weight, target).
+__device__ __forceinline__ void stage_arcs(const DevModel& m, const Slice& s, int32_t lo, int32_t hi) {
+  int32_t tk[kUnroll], to[kUnroll], Ls[kUnroll];
   float w[kUnroll];
-  int32_t to[kUnroll];
-};
-
-__device__ __forceinline__ void gather(const DevModel& m, const Slice& s, int32_t c0, int32_t T, Chunk& a) {
   int L = 0;
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {  // all loads of the chunk in flight together
-    const int32_t j = c0 + u * kThreads + (int32_t)threadIdx.x;
-    a.key[u] = kNone;
-    if (j < T) {
+  for (int u = 0; u < kUnroll; ++u) {
+    const int32_t j = lo + u * kThreads + (int32_t)threadIdx.x;
+    Ls[u] = -1;
+    if (j < hi) {
       while (j >= s.pre[L + 1]) ++L;
       const int32_t arc = s.beg[L] + (j - s.pre[L]);
-      a.key[u] = ((uint32_t)L << 24) | (uint32_t)__ldg(&m.arc_tok[arc]);
-      a.w[u] = __ldg(&m.arc_w[arc]);
-      a.to[u] = __ldg(&m.arc_to[arc]);
+      Ls[u] = L;
+      tk[u] = __ldg(&m.arc_tok[arc]);
+      w[u] = __ldg(&m.arc_w[arc]);
+      to[u] = __ldg(&m.arc_to[arc]);
     }
+  }
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    if (Ls[u] < 0) continue;
+    const int32_t slot = u * kThreads + (int32_t)threadIdx.x;
+    s.st_tok[slot] = tk[u];
+    s.st_s[slot] = __fadd_rn(s.acc[Ls[u]], w[u]);  // acc_boff + arc_weights (Alg. 1 line 74)
+    s.st_n[slot] = to[u];
   }
 }
 
-// Step 3 for one chunk: levels from the highest index (lowest order) down.
-__device__ __forceinline__ void write_levels(const Slice& s, int32_t c0, int32_t T, const Chunk& a) {
-  const int Lhi = level_of(s, min(c0 + kChunk, T) - 1), Llo = level_of(s, c0);
+// Step 3 for one round: levels from the highest index (lowest order) down,
+// one barrier each, threads strided over the level's staged slots.
+__device__ __forceinline__ void write_levels(const Slice& s, int32_t lo, int32_t hi, int Llo, int Lhi) {
   for (int L = Lhi; L >= Llo; --L) {
-    const float acc = s.acc[L];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (a.key[u] == kNone || (int)(a.key[u] >> 24) != L) continue;
-      const uint32_t tok = a.key[u] & 0xFFFFFFu;
-      s.row_s[tok] = __fadd_rn(acc, a.w[u]);  // acc_boff + arc_weights (Alg. 1 line 74)
-      s.row_n[tok] = a.to[u];
+    const int32_t j1 = min(hi, s.pre[L + 1]) - lo;
+    for (int32_t j = max(lo, s.pre[L]) - lo + (int32_t)threadIdx.x; j < j1; j += kThreads) {
+      const int32_t tok = s.st_tok[j];
+      s.row_s[tok] = s.st_s[j];
+      s.row_n[tok] = s.st_n[j];
     }
     __syncthreads();
   }
 }
 
 // Steps 2-3: root slots get acc_root; non-root arcs overwrite, lowest order
-// first. Chunks run from the last (lowest-order) arcs to the first. The first
-// gather is issued before the root fix-up so their latencies overlap.
+// first. Rounds of kChunk arcs run from the last (lowest-order) arcs to the
+// first; the first round's loads are issued before the root fix-up so their
+// latencies overlap.
 __device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, const Row& r, bool tma) {
   const int32_t V = m.V, T = r.total;
   const float acc_root = r.acc_root;
-  int32_t c0 = T > 0 ? ((T - 1) / kChunk) * kChunk : 0;
-  Chunk a;
-  if (T > 0) gather(m, s, c0, T, a);
+  int32_t lo = T > kChunk ? T - kChunk : 0;
+  if (T > 0) stage_arcs(m, s, lo, T);
+  STAMP(4);
   if (tma) mbar_wait(s.bar, 0);
   if ((V & 3) == 0 && tma) {
     float4* s4 = reinterpret_cast<float4*>(s.row_s);
@@ -287,13 +317,17 @@ __device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, con
     }
   }
   __syncthreads();
-  if (T == 0) return;
-  for (;;) {
-    write_levels(s, c0, T, a);
-    c0 -= kChunk;
-    if (c0 < 0) break;
-    gather(m, s, c0, T, a);
+  STAMP(5);
+  for (int32_t hi = T; hi > 0;) {
+    const int Llo = lo == 0 ? 0 : level_of(s, lo), Lhi = hi == T ? r.nlev - 1 : level_of(s, hi - 1);
+    write_levels(s, lo, hi, Llo, Lhi);
+    hi = lo;
+    if (hi == 0) break;
+    lo = hi > kChunk ? hi - kChunk : 0;
+    stage_arcs(m, s, lo, hi);
+    __syncthreads();
   }
+  STAMP(6);
 }
 
 // ---------------------------------------------------------------- advance
@@ -305,15 +339,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   const int32_t V = m.V, b = blockIdx.x;
   const int t = threadIdx.x;
   const Slice s = carve(smem, V, m.order);
-  PHASE(b, 0);
-  PHASE(b, 1);
+  STAMP(0);
+  STAMP(1);
+  STAMP(9);
   pdl_trigger();
   prologue(m, s, kVec4);
   pdl_wait();
-  PHASE(b, 2);
+  STAMP(2);
   const Row r = row_levels<kTable>(m, t == 0 ? __ldg(&states[b]) : 0, s);
-  PHASE(b, 5);
-  PHASE(b, 3);
+  STAMP(3);
   if (t == 0) {
     if (r.bad) atomicMin(m.bad_row, (unsigned long long)b);
     if (final_out) final_out[b] = r.bad ? __int_as_float(0x7fc00000) : r.fin;
@@ -326,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     return;
   }
   build_row(m, s, r, kVec4);
-  PHASE(b, 4);
+
   if (kVec4) {
     // step 4: the finished row leaves by TMA bulk stores (SASS: UBLKCP shared -> global)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> async proxy
@@ -340,6 +374,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
                    "r"(smem_u32(s.row_n)), "r"(bytes)
                    : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      STAMP(7);
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem stays valid until read
     }
   } else {
@@ -348,8 +383,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       __stcs(nrow + v, s.row_n[v]);
     }
   }
-  PHASE(b, 6);
-  PHASE(b, 7);
+  STAMP(8);
+  STAMPS_OUT(b);
 }
 
 // ---------------------------------------------------------------- final

@@ -54,8 +54,13 @@ def run(B, mode, n=400):
     return graph_us, statistics.median(single[5:])
 
 
+MODES = ((ng.CHAIN_TABLE, "table"), (ng.CHAIN_WALK, "walk"))
+BS = (1, 16, 128, 512, 1024, 2048, 4096)
+if os.environ.get("SWEEP_QUICK"):
+    MODES, BS = MODES[:1], (1, 128, 1024, 4096)
+print("lib", os.path.basename(ng.LIB_PATH))
 print("B, mode, graph_us_per_call, single_launch_us, GB/s(graph)")
-for mode, name in ((ng.CHAIN_TABLE, "table"), (ng.CHAIN_WALK, "walk")):
-    for B in (1, 16, 128, 512, 1024, 2048, 4096):
+for mode, name in MODES:
+    for B in BS:
         gus, sus = run(B, mode)
         print(f"{B:5d} {name:5s} {gus:8.2f} {sus:8.2f} {B*1024*8/gus/1e3:8.1f}", flush=True)
