@@ -193,6 +193,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2505_22857_b200 as ng
+    from paper_2505_22857_b200.dist import max_over_ranks
 
     rank, local, world = dist_env()
     torch.cuda.set_device(local)
@@ -265,11 +266,7 @@ def run_ours(args):
             e1.record(stream)
         stream.synchronize()
         barrier()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
+    ms = max_over_ranks(e0.elapsed_time(e1), dev)  # the job's time: the slowest rank
     ms_per_step = ms / K
     value = world * B * V * K / (ms / 1e3)
     bytes_step = 8 * B * V + 4 * B + 4 * B + touched
@@ -292,14 +289,11 @@ def run_ours(args):
         e1.record(stream)
     stream.synchronize()
     barrier()
-    ms_e = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms_e], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e = t.item()
+    ms_e = max_over_ranks(e0.elapsed_time(e1), dev)
     e2e = {"value": world * B * V * Ke / (ms_e / 1e3), "unit": "queries/s",
            "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": 8 * B * V + 4 * B, "steps": Ke}
 
+    variants = advance_variants(m, states, scores, nxt, fin, R, stream)
     fused = {}
     if not args.no_fused:
         fused = bench_fused(m, f, dev, stream, rank)
@@ -312,7 +306,7 @@ def run_ours(args):
 
     cpu = None
     if not args.no_cpu:
-        cpu = cpu_baseline(f, states_np[0], args.cpu_seconds)
+        cpu = cpu_baseline(f, states_np, args.cpu_seconds)
 
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_advance_traffic.json")
@@ -338,6 +332,7 @@ def run_ours(args):
         "gpu_launches": K,
         "e2e": e2e,
         "clocks": sampler.summary(),
+        "advance_us_per_call": variants,
         "fused_step_us": fused,
         "cpu_baseline": cpu,
     }
@@ -346,21 +341,44 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline(f, states0, seconds):
-    import numpy as np
+def cpu_baseline(f, states_all, seconds):
+    """The oracle as it stands, on all host cores, over a bounded sample of the
+    workload's rows (the first rows of the step batches, about `seconds` s)."""
     from oracle import Oracle
     o = Oracle(f.arpa, vocab_size=V)
     cores = len(os.sched_getaffinity(0))
+    flat = states_all.reshape(-1)
+    o.rows(flat[:cores], want64=False, nthreads=cores)  # warm-up
     t0 = time.perf_counter()
-    o.rows(states0[:cores], want64=False, nthreads=cores)
-    probe = time.perf_counter() - t0
-    rows = int(min(len(states0), max(cores, cores * seconds / max(probe, 1e-6))))
+    o.rows(flat[: 16 * cores], want64=False, nthreads=cores)
+    rate = 16 * cores / max(time.perf_counter() - t0, 1e-6)
+    rows = int(min(flat.size, max(cores, rate * seconds)))
     t0 = time.perf_counter()
-    o.rows(states0[:rows], want64=False, nthreads=cores)
+    o.rows(flat[:rows], want64=False, nthreads=cores)
     el = time.perf_counter() - t0
     return {"value": rows * V / el, "unit": "queries/s", "cores": cores, "kind": "oracle",
-            "sample": f"{rows} of the {len(states0)} rows of one step (full V={V} rows, score32+next), "
-                      f"{el:.1f} s on {cores} threads"}
+            "sample": f"{rows} trajectory rows of the workload ({rows / B_HEADLINE:.1f} steps of B={B_HEADLINE}, "
+                      f"full V={V} rows, score32 + next), {el:.1f} s on {cores} threads"}
+
+
+def advance_variants(m, states, scores, nxt, fin, R, stream):
+    """us per advance call (CUDA graph, rotating buffers) for the other shapes:
+    BASELINE configs[1] (B=128) and Algorithm 1's literal chain walk."""
+    import paper_2505_22857_b200 as ng
+    out = {}
+    for name, B, mode in (("b128_table", 128, ng.CHAIN_TABLE), ("b1024_table", states.shape[1], ng.CHAIN_TABLE),
+                          ("b1024_walk", states.shape[1], ng.CHAIN_WALK)):
+        m.set_chain_mode(mode)
+        n = 4 * R
+
+        def calls():
+            for k in range(n):
+                r = k % R
+                m.advance(states[r, :B], scores[r, :B], nxt[r, :B], fin[r, :B], stream=stream)
+
+        out[name] = _graph_time(calls, stream, None, reps=3, reset=lambda: None) * 1e3 / n
+    m.set_chain_mode(ng.CHAIN_TABLE)
+    return out
 
 
 def bench_fused(m, f, dev, stream, rank):
@@ -383,6 +401,13 @@ def bench_fused(m, f, dev, stream, rank):
     ms = _graph_time(ctc_all, stream, dev, reps=5, reset=lambda: (st.zero_(), pv.fill_(-1)))
     out["ctc_b256_t500_us_per_frame"] = ms * 1e3 / T
     out["ctc_b256_t500_ms_per_utterance_batch"] = ms
+
+    def plain_all():  # plain greedy CTC frame step (argmax only, no LM): torch library op
+        for t in range(T):
+            frames[t].copy_(torch.argmax(x[:, t], dim=1))
+
+    ms0 = _graph_time(plain_all, stream, dev, reps=3, reset=lambda: None)
+    out["ctc_plain_argmax_torch_us_per_frame"] = ms0 * 1e3 / T
     del x
     # --- RNN-T / AED: B=512 rows, per-step logits rotating over 16 buffers
     for name, mode, gen in (("rnnt", ng.RNNT, synth.rnnt_logits), ("aed", ng.AED, synth.aed_logits)):

@@ -63,8 +63,7 @@ int upload(ngpulm_model* m, int device) {
   std::vector<int32_t> chain;
   int32_t slots = 1;
   ngpulm::build_chain_table(h, chain, slots);
-  const size_t o_tag = align256(o_to + A * 4);
-  const size_t o_chain = align256(o_tag + (size_t)h.V * 4);
+  const size_t o_chain = align256(o_to + A * 4);
   const size_t o_bad = align256(o_chain + chain.size() * 4);
   const size_t total = align256(o_bad + 8);
   std::vector<unsigned char> stage(total, 0);
@@ -76,8 +75,6 @@ int upload(ngpulm_model* m, int device) {
   std::memcpy(stage.data() + o_w, h.arc_w.data(), A * 4);
   std::memcpy(stage.data() + o_to, h.arc_to.data(), A * 4);
   std::memcpy(stage.data() + o_chain, chain.data(), chain.size() * 4);
-  auto* tag = reinterpret_cast<int32_t*>(stage.data() + o_tag);
-  for (int32_t v = 0; v < h.V; ++v) tag[v] = (int32_t)((uint32_t)h.arc_to[v] | 0x80000000u);
   std::memset(stage.data() + o_bad, 0xff, 8);
 
   DeviceGuard g(device);
@@ -96,7 +93,6 @@ int upload(ngpulm_model* m, int device) {
   m->dm.arc_w = reinterpret_cast<const float*>(base + o_w);
   m->dm.arc_to = reinterpret_cast<const int32_t*>(base + o_to);
   m->dm.bad_row = reinterpret_cast<unsigned long long*>(base + o_bad);
-  m->dm.root_tag = reinterpret_cast<const int32_t*>(base + o_tag);
   m->chain_dev = base + o_chain;
   m->dm.chain = m->chain_mode == NGPULM_CHAIN_TABLE ? m->chain_dev : nullptr;
   m->dm.chain_slots = slots;

@@ -53,7 +53,6 @@ struct DevModel {
   const int32_t* arc_tok;
   const float* arc_w;
   const int32_t* arc_to;
-  const int32_t* root_tag;  // [V] root arc targets with bit 31 set: "root level" tag (kernels.cu)
   const void* chain;  // chain table (int4 records) or nullptr = walk the chain at query time
   int32_t chain_slots;
   int32_t S, V, order;
