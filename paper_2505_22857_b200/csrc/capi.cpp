@@ -310,6 +310,13 @@ int ngpulm_advance_host(ngpulm_model* m, const int32_t* states_host, int32_t B, 
   return NGPULM_OK;
 }
 
+#ifdef NGPULM_PHASE_TIMING
+int ngpulm_debug_probe(const ngpulm::DevModel* m, const int32_t* states, int32_t B, long long* out_dev);
+int ngpulm_debug_probe_model(const ngpulm_model* m, const int32_t* states, int32_t B, long long* out_dev) {
+  return ngpulm_debug_probe(&m->dm, states, B, out_dev);
+}
+#endif
+
 int ngpulm_touched_bytes(const ngpulm_model* m, const int32_t* states_host, int32_t B, int64_t* out_bytes) {
   if (!m || !out_bytes || B < 0 || (B > 0 && !states_host)) return err(NGPULM_EUSAGE, "bad argument");
   std::unordered_set<int32_t> seen;

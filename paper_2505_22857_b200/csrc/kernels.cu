@@ -114,6 +114,7 @@ __device__ __forceinline__ Slice carve(unsigned char* p, int32_t V, int32_t orde
 // griddepcontrol.wait, 3 levels published, 4 arcs staged, 5 root fix-up
 // barrier, 6 levels written, 7 stores issued (clock64), 8 end (ns), 9 SM id.
 __device__ unsigned long long g_phase[16384 * 16];
+__device__ int g_skip;  // bit 0: no TMA prologue
 __device__ __forceinline__ unsigned long long* stamp_buf() {
   __shared__ unsigned long long buf[16];
   return buf;
@@ -131,7 +132,7 @@ __device__ __forceinline__ unsigned long long* stamp_buf() {
 #define STAMPS_OUT(row)                                                                 \
   do {                                                                                  \
     if (threadIdx.x == 0 && (row) < 16384)                                              \
-      for (int _i = 0; _i < 10; ++_i) g_phase[(row) * 16 + _i] = stamp_buf()[_i];       \
+      for (int _i = 0; _i < 12; ++_i) g_phase[(row) * 16 + _i] = stamp_buf()[_i];       \
   } while (0)
 #else
 #define STAMP(i) \
@@ -181,18 +182,26 @@ __device__ __forceinline__ void prologue(const DevModel& m, const Slice& s, bool
 
 // Step 1, warp 0: the row's levels into shared memory + the Row scalars.
 template <bool kTable>
-__device__ __forceinline__ Row load_levels(const DevModel& m, int32_t st, const Slice& s) {
+__device__ __forceinline__ Row load_levels(const DevModel& m, const int32_t* state_ptr, const Slice& s) {
   const int lane = threadIdx.x & 31;
   Row r;
+  // Kernel parameters sit in the constant bank; a constant-cache miss costs an
+  // L2 round trip. Read the ones this step needs into registers now, before
+  // the state arrives (volatile asm pins them here), so their misses overlap
+  // the state load instead of following it.
+  const int4* table = reinterpret_cast<const int4*>(m.chain) + lane;
+  int32_t slots = m.chain_slots, S = m.S;
+  asm volatile("" : "+l"(table), "+r"(slots), "+r"(S));
+  const int32_t st = __shfl_sync(kFull, lane == 0 ? __ldg(state_ptr) : 0, 0);
+  STAMP(10);
   r.state = st;
-  r.bad = st < 0 || st >= m.S;
+  r.bad = st < 0 || st >= S;
   r.nlev = 0; r.total = 0; r.acc_root = 0.f; r.fin = 0.f;
   if (r.bad) return r;
   if (kTable) {
     // record = [header {nlev, acc_root, final, total}] + nlev x {begin, prefix, acc, 0}
-    const int4* rec = reinterpret_cast<const int4*>(m.chain) + (size_t)st * m.chain_slots;
     int4 x = make_int4(0, 0, 0, 0);
-    if (lane < m.chain_slots) x = __ldg(rec + lane);
+    if (lane < slots) x = __ldg(table + (size_t)st * slots);
     r.nlev = __shfl_sync(kFull, x.x, 0);
     r.acc_root = __int_as_float(__shfl_sync(kFull, x.y, 0));
     r.fin = __int_as_float(__shfl_sync(kFull, x.z, 0));
@@ -230,9 +239,10 @@ __device__ __forceinline__ Row load_levels(const DevModel& m, int32_t st, const 
 
 // Warp 0 loads, everyone reads the result after one barrier.
 template <bool kTable>
-__device__ __forceinline__ Row row_levels(const DevModel& m, int32_t st_in, const Slice& s) {
+__device__ __forceinline__ Row row_levels(const DevModel& m, const int32_t* state_ptr, const Slice& s) {
   if (threadIdx.x < 32) {
-    const Row rr = load_levels<kTable>(m, __shfl_sync(kFull, st_in, 0), s);
+    const Row rr = load_levels<kTable>(m, state_ptr, s);
+    STAMP(11);
     if (threadIdx.x == 0) *s.row = rr;
   }
   __syncthreads();
@@ -343,10 +353,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   STAMP(1);
   STAMP(9);
   pdl_trigger();
-  prologue(m, s, kVec4);
+#ifdef NGPULM_PHASE_TIMING
+  const bool use_tma = kVec4 && !(g_skip & 1);
+#else
+  const bool use_tma = kVec4;
+#endif
+  prologue(m, s, use_tma);
   pdl_wait();
   STAMP(2);
-  const Row r = row_levels<kTable>(m, t == 0 ? __ldg(&states[b]) : 0, s);
+  const Row r = row_levels<kTable>(m, states + b, s);
   STAMP(3);
   if (t == 0) {
     if (r.bad) atomicMin(m.bad_row, (unsigned long long)b);
@@ -356,10 +371,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   int32_t* nrow = next + (size_t)b * V;
   if (r.bad) {
     for (int32_t v = t; v < V; v += kThreads) { srow[v] = __int_as_float(0x7fc00000); nrow[v] = -1; }
-    if (kVec4) mbar_wait(s.bar, 0);  // no exit with the bulk copy in flight
+    if (use_tma) mbar_wait(s.bar, 0);  // no exit with the bulk copy in flight
     return;
   }
-  build_row(m, s, r, kVec4);
+  build_row(m, s, r, use_tma);
 
   if (kVec4) {
     // step 4: the finished row leaves by TMA bulk stores (SASS: UBLKCP shared -> global)
@@ -458,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       if (better(a, col, bv, bc)) { bv = a; bc = col; }
     }
   }
-  const Row r = row_levels<kTable>(m, t == 0 ? states[b] : 0, s);
+  const Row r = row_levels<kTable>(m, states + b, s);
   if (r.bad) {
     if (t == 0) { tokens_out[b] = -1; atomicMin(m.bad_row, (unsigned long long)b); }
     if (tma) mbar_wait(s.bar, 0);
@@ -527,6 +542,23 @@ int launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStrea
 }  // namespace
 
 #ifdef NGPULM_PHASE_TIMING
+// lat3-style probe on the model's own data: states[b] -> chain record, by warp 0.
+__global__ void probe_kernel(DevModel m, const int32_t* __restrict__ states, long long* out) {
+  const int b = blockIdx.x, lane = threadIdx.x & 31;
+  long long t0 = clock64();
+  const int32_t st = __shfl_sync(kFull, lane == 0 ? __ldg(&states[b]) : 0, 0);
+  long long t1 = clock64();
+  int4 x = make_int4(0, 0, 0, 0);
+  if (lane < m.chain_slots) x = __ldg(reinterpret_cast<const int4*>(m.chain) + (size_t)st * m.chain_slots + lane);
+  const int v = __shfl_sync(kFull, x.x + x.y, 0);
+  long long t2 = clock64();
+  if (lane == 0) { out[b * 3] = t1 - t0; out[b * 3 + 1] = t2 - t1; out[b * 3 + 2] = v; }
+}
+extern "C" int ngpulm_debug_probe(const DevModel* m, const int32_t* states, int32_t B, long long* out_dev) {
+  probe_kernel<<<B, 32>>>(*m, states, out_dev);
+  return (int)cudaDeviceSynchronize();
+}
+extern "C" int ngpulm_debug_skip(int bits) { return (int)cudaMemcpyToSymbol(g_skip, &bits, sizeof bits); }
 extern "C" int ngpulm_debug_phases(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, g_phase, sizeof(unsigned long long) * (size_t)n);
 }

@@ -49,7 +49,7 @@ def q(a):
 
 
 def report(tag, ph, Ts=None):
-    names = [("wait", 1, 2), ("levels", 2, 3), ("stage", 3, 4), ("fixup", 4, 5), ("write", 5, 6), ("store", 6, 7)]
+    names = [("wait", 1, 2), ("st", 2, 10), ("rec", 10, 11), ("bar", 11, 3), ("stage", 3, 4), ("fixup", 4, 5), ("write", 5, 6), ("store", 6, 7)]
     parts = " ".join(f"{n} {q(ph[:, b] - ph[:, a])}" for n, a, b in names)
     g0 = ph[:, 0].min()
     print(f"{tag}: med/p90/max cycles: {parts} | entry ns {q(ph[:, 0] - g0)} end ns {q(ph[:, 8] - g0)} "
@@ -87,3 +87,30 @@ for B in (1, 128, 1024, 4096):
     stream.synchronize()
     Ts = np.array([total_arcs(x) for x in allst[:B]]) if B <= 1024 else None
     report(f"B={B:5d} single          ", phases(B), Ts)
+    with torch.cuda.stream(stream):
+        m.advance(st[0], sc[0], nx[0], want_final=False, stream=stream)
+    stream.synchronize()
+    report(f"B={B:5d} single, repeat  ", phases(B))
+
+# probe: the same two dependent loads on the model's own data, in isolation
+L.ngpulm_debug_probe_model.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+for B in (128, 1024):
+    st = torch.from_numpy(allst[:B].copy()).cuda()
+    o = torch.zeros(B * 3, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        L.ngpulm_debug_probe_model(m._h, st.data_ptr(), B, o.data_ptr())
+    r = o.view(B, 3).cpu().numpy()
+    print(f"probe B={B}: states load {q(r[:, 0])}  record load {q(r[:, 1])}")
+
+# bisect: the same single launch without the TMA prologue
+L.ngpulm_debug_skip.argtypes = [C.c_int]
+L.ngpulm_debug_skip(1)
+for B in (128, 1024):
+    st = torch.from_numpy(allst[:B].copy()).cuda()
+    sc = torch.empty((B, 1024), dtype=torch.float32, device="cuda")
+    nx = torch.empty((B, 1024), dtype=torch.int32, device="cuda")
+    for _ in range(2):
+        m.advance(st, sc, nx, want_final=False)
+        torch.cuda.synchronize()
+    report(f"B={B:5d} single, no TMA prologue", phases(B))
+L.ngpulm_debug_skip(0)
