@@ -434,6 +434,16 @@ void build_chain_table(const HostModel& m, std::vector<int32_t>& out, int32_t& s
       acc = acc + m.boff_w[x];
       x = m.boff_to[x];
     }
+    // field 3 of a level: (first slot << 16) | quads, for the one-warp-per-row
+    // kernel: level i covers the 16-byte quads [begin/4, (begin+count-1)/4],
+    // cut into slots of 32 quads; slots are numbered from the last level.
+    for (int32_t i = n - 1, start = 0; i >= 0; --i) {
+      int32_t* lv = rec + (size_t)(i + 1) * 4;
+      const int32_t b = lv[0], cnt = (i + 1 < n ? lv[4 + 1] : pre) - lv[1];
+      const int32_t nq = ((b + cnt - 1) >> 2) - (b >> 2) + 1;
+      lv[3] = (start << 16) | nq;
+      start += (nq + 31) >> 5;
+    }
     rec[0] = n;
     std::memcpy(&rec[1], &acc, 4);
     std::memcpy(&rec[2], &m.final_w[s], 4);

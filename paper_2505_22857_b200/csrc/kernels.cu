@@ -35,6 +35,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 #include "ngpulm_internal.h"
 
@@ -114,7 +115,7 @@ __device__ __forceinline__ Slice carve(unsigned char* p, int32_t V, int32_t orde
 // griddepcontrol.wait, 3 levels published, 4 arcs staged, 5 root fix-up
 // barrier, 6 levels written, 7 stores issued (clock64), 8 end (ns), 9 SM id.
 __device__ unsigned long long g_phase[16384 * 16];
-__device__ int g_skip;  // bit 0: no TMA prologue
+__device__ int g_skip;  // bit 0: no TMA prologue (CTA kernel); warp kernel: bit 1 no stores, bit 2 no arcs, bit 3 no fill
 __device__ __forceinline__ unsigned long long* stamp_buf() {
   __shared__ unsigned long long buf[16];
   return buf;
@@ -132,7 +133,7 @@ __device__ __forceinline__ unsigned long long* stamp_buf() {
 #define STAMPS_OUT(row)                                                                 \
   do {                                                                                  \
     if (threadIdx.x == 0 && (row) < 16384)                                              \
-      for (int _i = 0; _i < 12; ++_i) g_phase[(row) * 16 + _i] = stamp_buf()[_i];       \
+      for (int _i = 0; _i < 16; ++_i) g_phase[(row) * 16 + _i] = stamp_buf()[_i];       \
   } while (0)
 #else
 #define STAMP(i) \
@@ -182,7 +183,8 @@ __device__ __forceinline__ void prologue(const DevModel& m, const Slice& s, bool
 
 // Step 1, warp 0: the row's levels into shared memory + the Row scalars.
 template <bool kTable>
-__device__ __forceinline__ Row load_levels(const DevModel& m, const int32_t* state_ptr, const Slice& s) {
+__device__ __forceinline__ Row load_levels(const DevModel& m, const int32_t* state_ptr, int32_t* beg, int32_t* pre_,
+                                           float* accs) {
   const int lane = threadIdx.x & 31;
   Row r;
   // Kernel parameters sit in the constant bank; a constant-cache miss costs an
@@ -206,8 +208,8 @@ __device__ __forceinline__ Row load_levels(const DevModel& m, const int32_t* sta
     r.acc_root = __int_as_float(__shfl_sync(kFull, x.y, 0));
     r.fin = __int_as_float(__shfl_sync(kFull, x.z, 0));
     r.total = __shfl_sync(kFull, x.w, 0);
-    if (lane >= 1 && lane <= r.nlev) { s.beg[lane - 1] = x.x; s.pre[lane - 1] = x.y; s.acc[lane - 1] = __int_as_float(x.z); }
-    if (lane == 0) s.pre[r.nlev] = r.total;
+    if (lane >= 1 && lane <= r.nlev) { beg[lane - 1] = x.x; pre_[lane - 1] = x.y; accs[lane - 1] = __int_as_float(x.z); }
+    if (lane == 0) pre_[r.nlev] = r.total;
   } else {
     // Algorithm 1 lines 67-82, serial by nature (pointer chase), lane 0
     int32_t n = 0, pre = 0, bad = 0;
@@ -217,14 +219,14 @@ __device__ __forceinline__ Row load_levels(const DevModel& m, const int32_t* sta
       int32_t x = st;
       for (; n < level_cap(m.order) && x != 0; ++n) {
         const int4 q = __ldg(rec + x);  // {arc_begin, arc_end, boff_to, boff_w}
-        s.beg[n] = q.x;
-        s.pre[n] = pre;
-        s.acc[n] = acc;
+        beg[n] = q.x;
+        pre_[n] = pre;
+        accs[n] = acc;
         pre += q.y - q.x;
         acc = __fadd_rn(acc, __int_as_float(q.w));  // acc_boff += boff_weights[state]
         x = q.z;                                     // state = boff_to_states[state]
       }
-      s.pre[n] = pre;
+      pre_[n] = pre;
       bad = x != 0;
       fin = bad ? 0.f : __ldg(&m.final_w[st]);
     }
@@ -241,7 +243,7 @@ __device__ __forceinline__ Row load_levels(const DevModel& m, const int32_t* sta
 template <bool kTable>
 __device__ __forceinline__ Row row_levels(const DevModel& m, const int32_t* state_ptr, const Slice& s) {
   if (threadIdx.x < 32) {
-    const Row rr = load_levels<kTable>(m, state_ptr, s);
+    const Row rr = load_levels<kTable>(m, state_ptr, s.beg, s.pre, s.acc);
     STAMP(11);
     if (threadIdx.x == 0) *s.row = rr;
   }
@@ -402,6 +404,330 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   STAMPS_OUT(b);
 }
 
+// ---------------------------------------------------------------- advance, one warp per row
+// A CTA of R warps answers R rows, one per warp; the CTA shares one copy of
+// the root level (bulk-copied once per CTA, before griddepcontrol.wait).
+// Lane l+1 of a warp holds level l of its row (the chain-table record is
+// already laid out that way). Every level is cut into "slots" of 32 16-byte
+// quads (lane i of a slot loads quad i: up to four consecutive arcs of that
+// level; every model array is padded in the blob, so a quad never leaves it).
+// Slots are numbered from the last level (lowest order) to the first, so
+// writing them in slot order, with a __syncwarp where the level changes, lets
+// the highest order found win — Algorithm 1 lines 77-79 — with plain
+// shared-memory stores. kSlots slots are in flight at once (all their loads
+// issued together); rows with more slots take more windows. Masked-off arc
+// lanes store into a trash word behind the row, so the write loop has no
+// branches. No CTA-wide barrier after the prologue: rows never wait for each
+// other.
+#ifndef NGPULM_STORE_HINT
+#define NGPULM_STORE_HINT 1
+#endif
+
+__host__ __device__ constexpr size_t wrow_bytes(int32_t V) { return align16((size_t)V * 4 + 4); }  // + trash word
+__host__ __device__ constexpr size_t wslice_bytes(int32_t V, int32_t order) {
+  return 2 * wrow_bytes(V) + levels_bytes(order);
+}
+// root_w[V] | root_to[V] | mbarrier | R x (row_s[V+1] | row_n[V+1] | levels)
+__host__ __device__ constexpr size_t wcta_smem(int32_t V, int32_t order, int R) {
+  return 2 * align16((size_t)V * 4) + 16 + (size_t)R * wslice_bytes(V, order);
+}
+
+struct WSlice {
+  float* row_s;  // [V] + trash
+  int32_t* row_n;
+  int32_t* beg;  // levels (walk mode: written by lane 0)
+  int32_t* pre;
+  float* acc;
+};
+
+__device__ __forceinline__ WSlice wcarve(unsigned char* p, int32_t V, int32_t order) {
+  const int32_t Lc = level_cap(order);
+  WSlice s;
+  s.row_s = reinterpret_cast<float*>(p);
+  p += wrow_bytes(V);
+  s.row_n = reinterpret_cast<int32_t*>(p);
+  p += wrow_bytes(V);
+  int32_t* l = reinterpret_cast<int32_t*>(p);
+  s.beg = l;
+  s.pre = l + Lc;
+  s.acc = reinterpret_cast<float*>(l + 2 * Lc + 1);
+  return s;
+}
+
+struct WLevel {  // lane l+1: level l of the row
+  int32_t beg, end;  // arcs [beg, end)
+  int32_t info;      // (first slot << 16) | quads
+  int32_t eslot;     // one past the level's last slot (INT_MAX on lanes without a level)
+  float acc;         // acc_boff at the level
+};
+
+// The row's state, header and levels (Algorithm 1 lines 67-82).
+template <bool kTable>
+__device__ __forceinline__ Row warp_row(const DevModel& m, const int32_t* state_ptr, const WSlice& s, WLevel& lv,
+                                        int32_t& nslots) {
+  const int lane = threadIdx.x & 31;
+  Row r;
+  lv.beg = 0; lv.end = 0; lv.info = 0; lv.eslot = INT_MAX; lv.acc = 0.f;
+  nslots = 0;
+  if (kTable) {
+    const int4* table = reinterpret_cast<const int4*>(m.chain) + lane;
+    int32_t slots = m.chain_slots, S = m.S;
+    asm volatile("" : "+l"(table), "+r"(slots), "+r"(S));  // parameters read before the state arrives
+    const int32_t st = __shfl_sync(kFull, lane == 0 ? __ldg(state_ptr) : 0, 0);
+    STAMP(10);
+    r.state = st;
+    r.bad = st < 0 || st >= S;
+    r.nlev = 0; r.total = 0; r.acc_root = 0.f; r.fin = 0.f;
+    if (r.bad) return r;
+    int4 x = make_int4(0, 0, 0, 0);
+    if (lane < slots) x = __ldg(table + (size_t)st * slots);
+    r.nlev = __shfl_sync(kFull, x.x, 0);
+    r.acc_root = __int_as_float(__shfl_sync(kFull, x.y, 0));
+    r.fin = __int_as_float(__shfl_sync(kFull, x.z, 0));
+    r.total = __shfl_sync(kFull, x.w, 0);
+    const int32_t npre = __shfl_down_sync(kFull, x.y, 1);
+    if (lane >= 1 && lane <= r.nlev) {
+      lv.beg = x.x;
+      lv.end = x.x + ((lane == r.nlev ? r.total : npre) - x.y);
+      lv.acc = __int_as_float(x.z);
+      lv.info = x.w;
+    }
+  } else {
+    r = load_levels<false>(m, state_ptr, s.beg, s.pre, s.acc);
+    if (r.bad) return r;
+    __syncwarp();
+    int32_t nq = 0;
+    if (lane >= 1 && lane <= r.nlev) {
+      lv.beg = s.beg[lane - 1];
+      lv.end = lv.beg + (s.pre[lane] - s.pre[lane - 1]);
+      lv.acc = s.acc[lane - 1];
+      nq = lv.end > lv.beg ? ((lv.end - 1) >> 2) - (lv.beg >> 2) + 1 : 0;
+    }
+    int32_t inc = (nq + 31) >> 5;  // slots of levels >= this one, then exclusive
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_down_sync(kFull, inc, o);
+      if (lane + o < 32) inc += y;
+    }
+    lv.info = ((inc - ((nq + 31) >> 5)) << 16) | nq;
+  }
+  if (lane >= 1 && lane <= r.nlev) lv.eslot = (lv.info >> 16) + (((lv.info & 0xffff) + 31) >> 5);
+  nslots = r.nlev > 0 ? __shfl_sync(kFull, lv.eslot, 1) : 0;
+  return r;
+}
+
+// One window of kW slots, in registers, processed in groups of 8 slots; a
+// group wholly past the row's last slot is skipped (uniform branch).
+template <int kW>
+struct Window {
+  using Mask = typename std::conditional<(kW <= 8), uint32_t, uint64_t>::type;
+  int4 tok[kW];
+  float4 w[kW];
+  int4 to[kW];
+  float acc[kW];   // acc_boff of the slot's level
+  Mask mask;       // 4 bits per slot: which of this lane's quad's arcs belong to the level
+};
+
+// Within a group everything is branch-free, so the group's shuffles and loads
+// are scheduled together: a dead slot or lane loads quad 0 (harmless) and
+// gets an empty mask.
+template <int kW>
+__device__ __forceinline__ void load_window(const DevModel& m, const WLevel& lv, int32_t nlev, int32_t k0,
+                                            int32_t nslots, Window<kW>& a) {
+  using Mask = typename Window<kW>::Mask;
+  const int lane = threadIdx.x & 31;
+  const int4* tok4 = reinterpret_cast<const int4*>(m.arc_tok);
+  const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
+  const int4* to4 = reinterpret_cast<const int4*>(m.arc_to);
+  a.mask = 0;
+#pragma unroll
+  for (int g = 0; g < kW; g += 8) {
+    if (g > 0 && k0 + g >= nslots) break;
+    int32_t qv[8];
+    Mask mask = 0;
+#pragma unroll
+    for (int u = g; u < g + 8; ++u) {
+      const int32_t k = k0 + u;
+      // levels entirely before slot k (in slot order) are the levels after its own
+      const int32_t L = nlev - 1 - __popc(__ballot_sync(kFull, lv.eslot <= k));
+      const int src = L + 1;
+      const int32_t info = __shfl_sync(kFull, lv.info, src), b = __shfl_sync(kFull, lv.beg, src);
+      const int32_t e = __shfl_sync(kFull, lv.end, src);
+      a.acc[u] = __shfl_sync(kFull, lv.acc, src);
+      const int32_t i = (k - (info >> 16)) * 32 + lane;
+      const bool act = k < nslots && i < (info & 0xffff);
+      const int32_t q = (b >> 2) + i;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        mask |= (act && 4 * q + j >= b && 4 * q + j < e) ? (Mask)1 << (4 * u + j) : (Mask)0;
+      qv[u - g] = act ? q : 0;
+    }
+    a.mask |= mask;
+#pragma unroll
+    for (int u = g; u < g + 8; ++u) {
+      a.tok[u] = __ldg(tok4 + qv[u - g]);
+      a.w[u] = __ldg(w4 + qv[u - g]);
+      a.to[u] = __ldg(to4 + qv[u - g]);
+    }
+  }
+}
+
+template <int kW>
+__device__ __forceinline__ void write_window(const WSlice& s, const Window<kW>& a, int32_t k0, int32_t nslots,
+                                             int32_t V) {
+#pragma unroll
+  for (int g = 0; g < kW; g += 8) {
+    if (g > 0 && k0 + g >= nslots) break;
+#pragma unroll
+    for (int u = g; u < g + 8; ++u) {
+      if (u > 0) __syncwarp();  // slots in level order: a lower order is done before a higher one
+      const int32_t tk[4] = {a.tok[u].x, a.tok[u].y, a.tok[u].z, a.tok[u].w};
+      const float ww[4] = {a.w[u].x, a.w[u].y, a.w[u].z, a.w[u].w};
+      const int32_t nn[4] = {a.to[u].x, a.to[u].y, a.to[u].z, a.to[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int32_t at = (a.mask >> (4 * u + j)) & 1 ? tk[j] : V;  // V = trash word
+        s.row_s[at] = __fadd_rn(a.acc[u], ww[j]);                     // acc_boff + arc_weights (Alg. 1 line 74)
+        s.row_n[at] = nn[j];
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// Root level into the row: score = acc_root + root weight, next = root
+// target; all loads of a batch issued before its stores.
+__device__ __forceinline__ void root_fill(const WSlice& s, const float* root_w, const int32_t* root_to, float ar,
+                                          int32_t V) {
+  const int lane = threadIdx.x & 31;
+  const float4* w4 = reinterpret_cast<const float4*>(root_w);
+  const int4* t4 = reinterpret_cast<const int4*>(root_to);
+  float4* s4 = reinterpret_cast<float4*>(s.row_s);
+  int4* n4 = reinterpret_cast<int4*>(s.row_n);
+  const int32_t nq4 = V / 4;
+  for (int32_t q0 = lane; q0 < nq4; q0 += 256) {
+    float4 y[8];
+    int4 z[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (q0 + 32 * j < nq4) { y[j] = w4[q0 + 32 * j]; z[j] = t4[q0 + 32 * j]; }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (q0 + 32 * j < nq4) {
+        y[j].x = __fadd_rn(ar, y[j].x);
+        y[j].y = __fadd_rn(ar, y[j].y);
+        y[j].z = __fadd_rn(ar, y[j].z);
+        y[j].w = __fadd_rn(ar, y[j].w);
+        s4[q0 + 32 * j] = y[j];
+        n4[q0 + 32 * j] = z[j];
+      }
+  }
+}
+
+template <bool kTable, int kW>
+__global__ void __launch_bounds__(256)
+    advance_warp_kernel(DevModel m, const int32_t* __restrict__ states, int32_t B, float* __restrict__ scores,
+                        int32_t* __restrict__ next, float* __restrict__ final_out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int32_t V = m.V;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, R = blockDim.x >> 5;
+  const size_t rb = align16((size_t)V * 4);
+  const float* root_w = reinterpret_cast<const float*>(smem);
+  const int32_t* root_to = reinterpret_cast<const int32_t*>(smem + rb);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * rb);
+  const WSlice s = wcarve(smem + 2 * rb + 16 + (size_t)w * wslice_bytes(V, m.order), V, m.order);
+  STAMP(0);
+  STAMP(1);
+  STAMP(9);
+  pdl_trigger();
+  if (threadIdx.x == 0) {  // step 0: the root level, once per CTA (immutable model data: before the wait)
+    const uint32_t b = smem_u32(bar), bytes = (uint32_t)V * 4u;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(2u * bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(root_w)),
+                 "l"(m.arc_w), "r"(bytes), "r"(b)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(root_to)),
+                 "l"(m.arc_to), "r"(bytes), "r"(b)
+                 : "memory");
+  }
+  __syncthreads();  // barrier inits visible to every warp
+  pdl_wait();
+  STAMP(2);
+  const int32_t row = (int32_t)blockIdx.x * R + w;
+  if (row >= B) return;  // warp 0 always has a row and waits for the bulk copy
+#ifdef NGPULM_PHASE_TIMING
+  const int skip = g_skip;
+#else
+  constexpr int skip = 0;
+#endif
+  WLevel lv;
+  int32_t nslots;
+  const Row r = warp_row<kTable>(m, states + row, s, lv, nslots);
+  STAMP(11);
+  float* srow = scores + (size_t)row * V;
+  int32_t* nrow = next + (size_t)row * V;
+  if (lane == 0) {
+    if (r.bad) atomicMin(m.bad_row, (unsigned long long)row);
+    if (final_out) final_out[row] = r.bad ? __int_as_float(0x7fc00000) : r.fin;
+  }
+  if (r.bad) {
+    for (int32_t v = lane; v < V; v += 32) { srow[v] = __int_as_float(0x7fc00000); nrow[v] = -1; }
+    if (w == 0) mbar_wait(bar, 0);
+    return;
+  }
+  mbar_wait(bar, 0);  // the CTA's root level has landed (long ago, normally)
+  STAMP(3);
+  Window<kW> a;
+  // the root fill goes first: its shared-memory loads would otherwise return
+  // behind the arc gathers
+  if (!(skip & 8)) root_fill(s, root_w, root_to, r.acc_root, V);
+  STAMP(12);
+  if (skip & 4) nslots = 0;
+  if (!(skip & 4)) load_window<kW>(m, lv, r.nlev, 0, nslots, a);
+  STAMP(4);
+  __syncwarp();
+  STAMP(5);
+  for (int32_t k0 = 0; k0 < nslots;) {
+    write_window<kW>(s, a, k0, nslots, V);
+    k0 += kW;
+    if (k0 < nslots) load_window<kW>(m, lv, r.nlev, k0, nslots, a);
+  }
+  STAMP(6);
+  // step 4: the row leaves by two bulk stores issued by lane 0
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0 && !(skip & 2)) {
+    const uint32_t bytes = (uint32_t)V * 4u;
+#if NGPULM_STORE_HINT
+    // outputs are streamed: first to leave L2, so the trie stays resident
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(srow),
+                 "r"(smem_u32(s.row_s)), "r"(bytes), "l"(pol)
+                 : "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(nrow),
+                 "r"(smem_u32(s.row_n)), "r"(bytes), "l"(pol)
+                 : "memory");
+#else
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(srow), "r"(smem_u32(s.row_s)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(nrow), "r"(smem_u32(s.row_n)),
+                 "r"(bytes)
+                 : "memory");
+#endif
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    STAMP(7);
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+  STAMP(8);
+  if (w == 0) STAMPS_OUT(row);
+}
+
 // ---------------------------------------------------------------- final
 __global__ void final_kernel(DevModel m, const int32_t* __restrict__ states, int32_t B,
                              float* __restrict__ out) {
@@ -539,7 +865,11 @@ int launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStrea
   return (int)cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+int g_row_mode = 1;  // advance: 1 = one warp per row (when it fits), 0 = one CTA per row
+
 }  // namespace
+
+extern "C" int ngpulm_debug_row_mode(int mode) { g_row_mode = mode; return 0; }
 
 #ifdef NGPULM_PHASE_TIMING
 // lat3-style probe on the model's own data: states[b] -> chain record, by warp 0.
@@ -560,7 +890,12 @@ extern "C" int ngpulm_debug_probe(const DevModel* m, const int32_t* states, int3
 }
 extern "C" int ngpulm_debug_skip(int bits) { return (int)cudaMemcpyToSymbol(g_skip, &bits, sizeof bits); }
 extern "C" int ngpulm_debug_phases(unsigned long long* host, int n) {
-  return (int)cudaMemcpyFromSymbol(host, g_phase, sizeof(unsigned long long) * (size_t)n);
+  const int e = (int)cudaMemcpyFromSymbol(host, g_phase, sizeof(unsigned long long) * (size_t)n);
+  void* p = nullptr;
+  cudaGetSymbolAddress(&p, g_phase);
+  cudaMemset(p, 0, sizeof(g_phase));  // rows a launch does not stamp read as 0 next time
+  cudaDeviceSynchronize();
+  return e;
 }
 #endif
 
@@ -572,10 +907,27 @@ int max_vocab_supported() {
 
 int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* scores, int32_t* next,
                    float* final_out, void* stream) {
-  const size_t sm = row_smem(m.V, m.order);
   const bool vec = (m.V % 4 == 0) && ((uintptr_t)scores % 16 == 0) && ((uintptr_t)next % 16 == 0);
   const bool table = m.chain != nullptr;
   cudaStream_t st = (cudaStream_t)stream;
+  if (vec && g_row_mode == 1) {
+    int R = (B + 147) / 148;
+    R = R < 1 ? 1 : (R > 8 ? 8 : R);
+    while (R > 1 && wcta_smem(m.V, m.order, R) > 227 * 1024) --R;
+    if (wcta_smem(m.V, m.order, R) <= 227 * 1024) {
+      const size_t wsm = wcta_smem(m.V, m.order, R);
+      const dim3 wg((B + R - 1) / R), wb(32 * R);
+      // up to 8 rows per SM: 16-slot windows (almost every row in one window);
+      // more rows per SM: 8-slot windows (registers for occupancy)
+      if (B <= 8 * 148) {
+        if (table) return launch(advance_warp_kernel<true, 16>, wg, wb, wsm, st, m, states, B, scores, next, final_out);
+        return launch(advance_warp_kernel<false, 16>, wg, wb, wsm, st, m, states, B, scores, next, final_out);
+      }
+      if (table) return launch(advance_warp_kernel<true, 8>, wg, wb, wsm, st, m, states, B, scores, next, final_out);
+      return launch(advance_warp_kernel<false, 8>, wg, wb, wsm, st, m, states, B, scores, next, final_out);
+    }
+  }
+  const size_t sm = row_smem(m.V, m.order);
   const dim3 gd(B), bd(kThreads);
   if (vec && table) return launch(advance_kernel<true, true>, gd, bd, sm, st, m, states, scores, next, final_out);
   if (vec) return launch(advance_kernel<true, false>, gd, bd, sm, st, m, states, scores, next, final_out);

@@ -40,10 +40,12 @@ int build_from_arpa(const char* arpa_path, const char* vocab_path, int32_t vocab
 
 // Load-time chain table (DESIGN.md §Kernels "chain table"): per state a fixed
 // record of `slots` int4: slot 0 = {nlev, acc_root, final, total_arcs}, slots
-// 1..nlev = {arc_begin, arc_prefix, acc_boff, 0} for every level of the
-// back-off chain that has arcs, in Algorithm 1 order; padding slots =
-// {0, total_arcs, 0, 0}. acc_boff is accumulated exactly as Algorithm 1 does
-// (left to right, float). slots = max(1, order).
+// 1..nlev = {arc_begin, arc_prefix, acc_boff, (first_slot << 16) | quads} for
+// every level of the back-off chain that has arcs, in Algorithm 1 order
+// (quads: 16-byte groups the level's arcs span; slots: 32-quad groups,
+// numbered from the last level); padding slots = {0, total_arcs, 0, 0}.
+// acc_boff is accumulated exactly as Algorithm 1 does (left to right, float).
+// slots = max(1, order).
 void build_chain_table(const HostModel& m, std::vector<int32_t>& out, int32_t& slots);
 
 // Device-side view passed to kernels by value.

@@ -21,6 +21,7 @@ import synth  # noqa: E402
 
 L = ng.lib()
 L.ngpulm_debug_phases.argtypes = [C.c_void_p, C.c_int]
+L.ngpulm_debug_row_mode(int(os.environ.get("ROW_MODE", "1")))
 f = synth.make_lm("/tmp/ngpulm_prof", 1024, 6, tokens=430000, seed=1, heldout=4000, tag="bench_6gram")
 m = ng.load_arpa(f.arpa, vocab_size=1024, device=0)
 ctx = synth.sample_contexts(synth.read_sentences(f.heldout), 6, 4096 * 16, seed=2)
@@ -49,7 +50,13 @@ def q(a):
 
 
 def report(tag, ph, Ts=None):
+    keep = ph[:, 8] > 0  # rows that carry stamps (warp kernel: warp 0's rows only)
+    ph = ph[keep]
+    if Ts is not None:
+        Ts = Ts[keep]
     names = [("wait", 1, 2), ("st", 2, 10), ("rec", 10, 11), ("bar", 11, 3), ("stage", 3, 4), ("fixup", 4, 5), ("write", 5, 6), ("store", 6, 7)]
+    if (ph[:, 12] > 0).all():  # warp kernel: stage = root fill + window loads issued
+        names[4:5] = [("fill", 3, 12), ("issue", 12, 4)]
     parts = " ".join(f"{n} {q(ph[:, b] - ph[:, a])}" for n, a, b in names)
     g0 = ph[:, 0].min()
     print(f"{tag}: med/p90/max cycles: {parts} | entry ns {q(ph[:, 0] - g0)} end ns {q(ph[:, 8] - g0)} "
