@@ -413,7 +413,20 @@ int build_from_arpa(const char* arpa_path, const char* vocab_path, int32_t V, Ho
   return NGPULM_OK;
 }
 
-void build_chain_table(const HostModel& m, std::vector<int32_t>& out, int32_t& slots) {
+size_t device_arc_layout(const HostModel& m, std::vector<int32_t>& arc_begin, int32_t& pad_quad) {
+  const int32_t S = m.num_states;
+  arc_begin.assign((size_t)S, 0);
+  size_t cur = 0;
+  for (int32_t s = 0; s < S; ++s) {
+    arc_begin[(size_t)s] = (int32_t)cur;
+    cur = (cur + (size_t)(m.arc_off[s + 1] - m.arc_off[s]) + 3) & ~(size_t)3;
+  }
+  pad_quad = (int32_t)(cur / 4);
+  return cur + 4;
+}
+
+void build_chain_table(const HostModel& m, const std::vector<int32_t>& arc_begin, std::vector<int32_t>& out,
+                       int32_t& slots) {
   slots = std::max(1, m.order);
   const int32_t S = m.num_states;
   out.assign((size_t)S * slots * 4, 0);
@@ -422,13 +435,13 @@ void build_chain_table(const HostModel& m, std::vector<int32_t>& out, int32_t& s
     float acc = 0.0f;
     int32_t n = 0, pre = 0, x = s;
     for (int it = 0; it < slots && x != 0; ++it) {  // Algorithm 1 lines 72-82, at load time
-      const int32_t b = m.arc_off[x], e = m.arc_off[x + 1];
-      if (e > b && n + 1 < slots) {
+      const int32_t cnt = m.arc_off[x + 1] - m.arc_off[x];
+      if (cnt > 0 && n + 1 < slots) {
         int32_t* lv = rec + (size_t)(n + 1) * 4;
-        lv[0] = b;
+        lv[0] = arc_begin[x];
         lv[1] = pre;
         std::memcpy(&lv[2], &acc, 4);
-        pre += e - b;
+        pre += cnt;
         ++n;
       }
       acc = acc + m.boff_w[x];

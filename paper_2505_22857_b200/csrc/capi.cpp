@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -54,7 +55,11 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 // One allocation holds the whole resident model.
 int upload(ngpulm_model* m, int device) {
   const ngpulm::HostModel& h = m->h;
-  const size_t S = (size_t)h.num_states, A = h.arc_tok.size();
+  const size_t S = (size_t)h.num_states;
+  std::vector<int32_t> dbeg;
+  int32_t pad_quad = 0;
+  const size_t A = ngpulm::device_arc_layout(h, dbeg, pad_quad);  // padded arc count
+  if (A > (size_t)INT32_MAX) return err(NGPULM_EUSAGE, "too many arcs for 32-bit arc indices");
   const size_t o_srec = 0;
   const size_t o_fin = align256(o_srec + S * sizeof(ngpulm::StateRec));
   const size_t o_tok = align256(o_fin + S * 4);
@@ -62,18 +67,24 @@ int upload(ngpulm_model* m, int device) {
   const size_t o_to = align256(o_w + A * 4);
   std::vector<int32_t> chain;
   int32_t slots = 1;
-  ngpulm::build_chain_table(h, chain, slots);
+  ngpulm::build_chain_table(h, dbeg, chain, slots);
   const size_t o_chain = align256(o_to + A * 4);
   const size_t o_bad = align256(o_chain + chain.size() * 4);
   const size_t total = align256(o_bad + 8);
   std::vector<unsigned char> stage(total, 0);
   auto* rec = reinterpret_cast<ngpulm::StateRec*>(stage.data() + o_srec);
-  for (size_t s = 0; s < S; ++s)
-    rec[s] = {h.arc_off[s], h.arc_off[s + 1], h.boff_to[s], h.boff_w[s]};
+  auto* tok = reinterpret_cast<int32_t*>(stage.data() + o_tok);
+  auto* wt = reinterpret_cast<float*>(stage.data() + o_w);
+  auto* to = reinterpret_cast<int32_t*>(stage.data() + o_to);
+  std::fill(tok, tok + A, h.V);  // padding arcs: token V = the kernels' trash column
+  for (size_t s = 0; s < S; ++s) {
+    const int32_t b = h.arc_off[s], cnt = h.arc_off[s + 1] - b;
+    rec[s] = {dbeg[s], dbeg[s] + cnt, h.boff_to[s], h.boff_w[s]};
+    std::memcpy(tok + dbeg[s], h.arc_tok.data() + b, (size_t)cnt * 4);
+    std::memcpy(wt + dbeg[s], h.arc_w.data() + b, (size_t)cnt * 4);
+    std::memcpy(to + dbeg[s], h.arc_to.data() + b, (size_t)cnt * 4);
+  }
   std::memcpy(stage.data() + o_fin, h.final_w.data(), S * 4);
-  std::memcpy(stage.data() + o_tok, h.arc_tok.data(), A * 4);
-  std::memcpy(stage.data() + o_w, h.arc_w.data(), A * 4);
-  std::memcpy(stage.data() + o_to, h.arc_to.data(), A * 4);
   std::memcpy(stage.data() + o_chain, chain.data(), chain.size() * 4);
   std::memset(stage.data() + o_bad, 0xff, 8);
 
@@ -99,6 +110,7 @@ int upload(ngpulm_model* m, int device) {
   m->dm.S = h.num_states;
   m->dm.V = h.V;
   m->dm.order = h.order;
+  m->dm.pad_quad = pad_quad;
   return NGPULM_OK;
 }
 

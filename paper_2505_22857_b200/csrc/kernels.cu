@@ -425,11 +425,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 
 __host__ __device__ constexpr size_t wrow_bytes(int32_t V) { return align16((size_t)V * 4 + 4); }  // + trash word
 __host__ __device__ constexpr size_t wslice_bytes(int32_t V, int32_t order) {
-  return 2 * wrow_bytes(V) + levels_bytes(order);
+  return 2 * wrow_bytes(V) + levels_bytes(order) + 16;
 }
-// root_w[V] | root_to[V] | mbarrier | R x (row_s[V+1] | row_n[V+1] | levels)
+// root_w[V] | mbarrier | R x (row_s[V+1] | row_n[V+1] | levels | mbarrier)
 __host__ __device__ constexpr size_t wcta_smem(int32_t V, int32_t order, int R) {
-  return 2 * align16((size_t)V * 4) + 16 + (size_t)R * wslice_bytes(V, order);
+  return align16((size_t)V * 4) + 16 + (size_t)R * wslice_bytes(V, order);
 }
 
 struct WSlice {
@@ -438,6 +438,7 @@ struct WSlice {
   int32_t* beg;  // levels (walk mode: written by lane 0)
   int32_t* pre;
   float* acc;
+  uint64_t* bar;  // the root targets' bulk copy into row_n
 };
 
 __device__ __forceinline__ WSlice wcarve(unsigned char* p, int32_t V, int32_t order) {
@@ -451,11 +452,12 @@ __device__ __forceinline__ WSlice wcarve(unsigned char* p, int32_t V, int32_t or
   s.beg = l;
   s.pre = l + Lc;
   s.acc = reinterpret_cast<float*>(l + 2 * Lc + 1);
+  s.bar = reinterpret_cast<uint64_t*>(p + levels_bytes(order));
   return s;
 }
 
 struct WLevel {  // lane l+1: level l of the row
-  int32_t beg, end;  // arcs [beg, end)
+  int32_t beg;       // first arc (16-byte aligned in the device layout)
   int32_t info;      // (first slot << 16) | quads
   int32_t eslot;     // one past the level's last slot (INT_MAX on lanes without a level)
   float acc;         // acc_boff at the level
@@ -467,7 +469,7 @@ __device__ __forceinline__ Row warp_row(const DevModel& m, const int32_t* state_
                                         int32_t& nslots) {
   const int lane = threadIdx.x & 31;
   Row r;
-  lv.beg = 0; lv.end = 0; lv.info = 0; lv.eslot = INT_MAX; lv.acc = 0.f;
+  lv.beg = 0; lv.info = 0; lv.eslot = INT_MAX; lv.acc = 0.f;
   nslots = 0;
   if (kTable) {
     const int4* table = reinterpret_cast<const int4*>(m.chain) + lane;
@@ -485,10 +487,8 @@ __device__ __forceinline__ Row warp_row(const DevModel& m, const int32_t* state_
     r.acc_root = __int_as_float(__shfl_sync(kFull, x.y, 0));
     r.fin = __int_as_float(__shfl_sync(kFull, x.z, 0));
     r.total = __shfl_sync(kFull, x.w, 0);
-    const int32_t npre = __shfl_down_sync(kFull, x.y, 1);
     if (lane >= 1 && lane <= r.nlev) {
       lv.beg = x.x;
-      lv.end = x.x + ((lane == r.nlev ? r.total : npre) - x.y);
       lv.acc = __int_as_float(x.z);
       lv.info = x.w;
     }
@@ -499,9 +499,8 @@ __device__ __forceinline__ Row warp_row(const DevModel& m, const int32_t* state_
     int32_t nq = 0;
     if (lane >= 1 && lane <= r.nlev) {
       lv.beg = s.beg[lane - 1];
-      lv.end = lv.beg + (s.pre[lane] - s.pre[lane - 1]);
       lv.acc = s.acc[lane - 1];
-      nq = lv.end > lv.beg ? ((lv.end - 1) >> 2) - (lv.beg >> 2) + 1 : 0;
+      nq = (s.pre[lane] - s.pre[lane - 1] + 3) >> 2;
     }
     int32_t inc = (nq + 31) >> 5;  // slots of levels >= this one, then exclusive
 #pragma unroll
@@ -520,31 +519,27 @@ __device__ __forceinline__ Row warp_row(const DevModel& m, const int32_t* state_
 // group wholly past the row's last slot is skipped (uniform branch).
 template <int kW>
 struct Window {
-  using Mask = typename std::conditional<(kW <= 8), uint32_t, uint64_t>::type;
   int4 tok[kW];
   float4 w[kW];
   int4 to[kW];
-  float acc[kW];   // acc_boff of the slot's level
-  Mask mask;       // 4 bits per slot: which of this lane's quad's arcs belong to the level
+  float acc[kW];  // acc_boff of the slot's level
 };
 
 // Within a group everything is branch-free, so the group's shuffles and loads
-// are scheduled together: a dead slot or lane loads quad 0 (harmless) and
-// gets an empty mask.
+// are scheduled together. A level starts on a quad boundary and the rest of
+// its last quad is padding (token V), so a quad needs no mask; an idle lane
+// loads the all-padding quad. Padding tokens write the trash word.
 template <int kW>
 __device__ __forceinline__ void load_window(const DevModel& m, const WLevel& lv, int32_t nlev, int32_t k0,
-                                            int32_t nslots, Window<kW>& a) {
-  using Mask = typename Window<kW>::Mask;
+                                            int32_t nslots, int32_t pad_quad, Window<kW>& a) {
   const int lane = threadIdx.x & 31;
   const int4* tok4 = reinterpret_cast<const int4*>(m.arc_tok);
   const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
   const int4* to4 = reinterpret_cast<const int4*>(m.arc_to);
-  a.mask = 0;
 #pragma unroll
   for (int g = 0; g < kW; g += 8) {
     if (g > 0 && k0 + g >= nslots) break;
     int32_t qv[8];
-    Mask mask = 0;
 #pragma unroll
     for (int u = g; u < g + 8; ++u) {
       const int32_t k = k0 + u;
@@ -552,17 +547,10 @@ __device__ __forceinline__ void load_window(const DevModel& m, const WLevel& lv,
       const int32_t L = nlev - 1 - __popc(__ballot_sync(kFull, lv.eslot <= k));
       const int src = L + 1;
       const int32_t info = __shfl_sync(kFull, lv.info, src), b = __shfl_sync(kFull, lv.beg, src);
-      const int32_t e = __shfl_sync(kFull, lv.end, src);
       a.acc[u] = __shfl_sync(kFull, lv.acc, src);
       const int32_t i = (k - (info >> 16)) * 32 + lane;
-      const bool act = k < nslots && i < (info & 0xffff);
-      const int32_t q = (b >> 2) + i;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        mask |= (act && 4 * q + j >= b && 4 * q + j < e) ? (Mask)1 << (4 * u + j) : (Mask)0;
-      qv[u - g] = act ? q : 0;
+      qv[u - g] = (k < nslots && i < (info & 0xffff)) ? (b >> 2) + i : pad_quad;
     }
-    a.mask |= mask;
 #pragma unroll
     for (int u = g; u < g + 8; ++u) {
       a.tok[u] = __ldg(tok4 + qv[u - g]);
@@ -573,8 +561,7 @@ __device__ __forceinline__ void load_window(const DevModel& m, const WLevel& lv,
 }
 
 template <int kW>
-__device__ __forceinline__ void write_window(const WSlice& s, const Window<kW>& a, int32_t k0, int32_t nslots,
-                                             int32_t V) {
+__device__ __forceinline__ void write_window(const WSlice& s, const Window<kW>& a, int32_t k0, int32_t nslots) {
 #pragma unroll
   for (int g = 0; g < kW; g += 8) {
     if (g > 0 && k0 + g >= nslots) break;
@@ -586,31 +573,27 @@ __device__ __forceinline__ void write_window(const WSlice& s, const Window<kW>& 
       const int32_t nn[4] = {a.to[u].x, a.to[u].y, a.to[u].z, a.to[u].w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int32_t at = (a.mask >> (4 * u + j)) & 1 ? tk[j] : V;  // V = trash word
-        s.row_s[at] = __fadd_rn(a.acc[u], ww[j]);                     // acc_boff + arc_weights (Alg. 1 line 74)
-        s.row_n[at] = nn[j];
+        s.row_s[tk[j]] = __fadd_rn(a.acc[u], ww[j]);  // acc_boff + arc_weights (Alg. 1 line 74)
+        s.row_n[tk[j]] = nn[j];
       }
     }
   }
   __syncwarp();
 }
 
-// Root level into the row: score = acc_root + root weight, next = root
-// target; all loads of a batch issued before its stores.
-__device__ __forceinline__ void root_fill(const WSlice& s, const float* root_w, const int32_t* root_to, float ar,
-                                          int32_t V) {
+// Root level into the row's scores: acc_root + root weight;
+// all loads of a batch issued before its stores. (The root targets reach the
+// next-state slots by a bulk copy.)
+__device__ __forceinline__ void root_fill(const WSlice& s, const float* root_w, float ar, int32_t V) {
   const int lane = threadIdx.x & 31;
   const float4* w4 = reinterpret_cast<const float4*>(root_w);
-  const int4* t4 = reinterpret_cast<const int4*>(root_to);
   float4* s4 = reinterpret_cast<float4*>(s.row_s);
-  int4* n4 = reinterpret_cast<int4*>(s.row_n);
   const int32_t nq4 = V / 4;
   for (int32_t q0 = lane; q0 < nq4; q0 += 256) {
     float4 y[8];
-    int4 z[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      if (q0 + 32 * j < nq4) { y[j] = w4[q0 + 32 * j]; z[j] = t4[q0 + 32 * j]; }
+      if (q0 + 32 * j < nq4) y[j] = w4[q0 + 32 * j];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       if (q0 + 32 * j < nq4) {
@@ -619,9 +602,15 @@ __device__ __forceinline__ void root_fill(const WSlice& s, const float* root_w, 
         y[j].z = __fadd_rn(ar, y[j].z);
         y[j].w = __fadd_rn(ar, y[j].w);
         s4[q0 + 32 * j] = y[j];
-        n4[q0 + 32 * j] = z[j];
       }
   }
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 template <bool kTable, int kW>
@@ -633,32 +622,32 @@ __global__ void __launch_bounds__(256)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, R = blockDim.x >> 5;
   const size_t rb = align16((size_t)V * 4);
   const float* root_w = reinterpret_cast<const float*>(smem);
-  const int32_t* root_to = reinterpret_cast<const int32_t*>(smem + rb);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * rb);
-  const WSlice s = wcarve(smem + 2 * rb + 16 + (size_t)w * wslice_bytes(V, m.order), V, m.order);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + rb);
+  const WSlice s = wcarve(smem + rb + 16 + (size_t)w * wslice_bytes(V, m.order), V, m.order);
+  const int32_t row = (int32_t)blockIdx.x * R + w;
+  const uint32_t bytes = (uint32_t)V * 4u;
   STAMP(0);
   STAMP(1);
   STAMP(9);
   pdl_trigger();
-  if (threadIdx.x == 0) {  // step 0: the root level, once per CTA (immutable model data: before the wait)
-    const uint32_t b = smem_u32(bar), bytes = (uint32_t)V * 4u;
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+  // step 0, on immutable model data, so before the wait: the root weights
+  // once per CTA, and the root targets straight into every row's next-state
+  // slots (the root has an arc for every token, [0, V)).
+  if (lane == 0 && row < B) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(s.bar)) : "memory");
+    if (w == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(2u * bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(root_w)),
-                 "l"(m.arc_w), "r"(bytes), "r"(b)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(root_to)),
-                 "l"(m.arc_to), "r"(bytes), "r"(b)
-                 : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)), "r"(bytes) : "memory");
+    bulk_g2s(s.row_n, m.arc_to, bytes, s.bar);
+    if (w == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+      bulk_g2s(const_cast<float*>(root_w), m.arc_w, bytes, bar);
+    }
   }
-  __syncthreads();  // barrier inits visible to every warp
+  __syncthreads();  // the CTA barrier's init visible to every warp
   pdl_wait();
   STAMP(2);
-  const int32_t row = (int32_t)blockIdx.x * R + w;
-  if (row >= B) return;  // warp 0 always has a row and waits for the bulk copy
+  if (row >= B) return;  // warp 0 always has a row and waits for the CTA's bulk copy
 #ifdef NGPULM_PHASE_TIMING
   const int skip = g_skip;
 #else
@@ -676,32 +665,33 @@ __global__ void __launch_bounds__(256)
   }
   if (r.bad) {
     for (int32_t v = lane; v < V; v += 32) { srow[v] = __int_as_float(0x7fc00000); nrow[v] = -1; }
+    mbar_wait(s.bar, 0);  // no exit with a bulk copy in flight
     if (w == 0) mbar_wait(bar, 0);
     return;
   }
-  mbar_wait(bar, 0);  // the CTA's root level has landed (long ago, normally)
+  mbar_wait(bar, 0);  // the CTA's root weights have landed (long ago, normally)
   STAMP(3);
   Window<kW> a;
   // the root fill goes first: its shared-memory loads would otherwise return
   // behind the arc gathers
-  if (!(skip & 8)) root_fill(s, root_w, root_to, r.acc_root, V);
+  if (!(skip & 8)) root_fill(s, root_w, r.acc_root, V);
   STAMP(12);
   if (skip & 4) nslots = 0;
-  if (!(skip & 4)) load_window<kW>(m, lv, r.nlev, 0, nslots, a);
+  if (!(skip & 4)) load_window<kW>(m, lv, r.nlev, 0, nslots, m.pad_quad, a);
   STAMP(4);
+  mbar_wait(s.bar, 0);  // root targets in row_n
   __syncwarp();
   STAMP(5);
   for (int32_t k0 = 0; k0 < nslots;) {
-    write_window<kW>(s, a, k0, nslots, V);
+    write_window<kW>(s, a, k0, nslots);
     k0 += kW;
-    if (k0 < nslots) load_window<kW>(m, lv, r.nlev, k0, nslots, a);
+    if (k0 < nslots) load_window<kW>(m, lv, r.nlev, k0, nslots, m.pad_quad, a);
   }
   STAMP(6);
   // step 4: the row leaves by two bulk stores issued by lane 0
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
   if (lane == 0 && !(skip & 2)) {
-    const uint32_t bytes = (uint32_t)V * 4u;
 #if NGPULM_STORE_HINT
     // outputs are streamed: first to leave L2, so the trie stays resident
     uint64_t pol;

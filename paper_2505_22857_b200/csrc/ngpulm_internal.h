@@ -38,6 +38,13 @@ struct HostModel {
 int build_from_arpa(const char* arpa_path, const char* vocab_path, int32_t vocab_size,
                     HostModel& out, std::string& err);
 
+// Device arc layout: state s's arcs start at
+// arc_begin[s], a multiple of 4 (one 16-byte quad); the gap before the next
+// state holds padding arcs {token V, weight 0, target 0} (V is the kernels'
+// trash column), and one all-padding quad (pad_quad) follows the last state.
+// Returns the padded arc count (pad quad included).
+size_t device_arc_layout(const HostModel& m, std::vector<int32_t>& arc_begin, int32_t& pad_quad);
+
 // Load-time chain table (DESIGN.md §Kernels "chain table"): per state a fixed
 // record of `slots` int4: slot 0 = {nlev, acc_root, final, total_arcs}, slots
 // 1..nlev = {arc_begin, arc_prefix, acc_boff, (first_slot << 16) | quads} for
@@ -46,7 +53,9 @@ int build_from_arpa(const char* arpa_path, const char* vocab_path, int32_t vocab
 // numbered from the last level); padding slots = {0, total_arcs, 0, 0}.
 // acc_boff is accumulated exactly as Algorithm 1 does (left to right, float).
 // slots = max(1, order).
-void build_chain_table(const HostModel& m, std::vector<int32_t>& out, int32_t& slots);
+// Arc begins are the device layout's.
+void build_chain_table(const HostModel& m, const std::vector<int32_t>& arc_begin, std::vector<int32_t>& out,
+                       int32_t& slots);
 
 // Device-side view passed to kernels by value.
 struct DevModel {
@@ -58,6 +67,7 @@ struct DevModel {
   const void* chain;  // chain table (int4 records) or nullptr = walk the chain at query time
   int32_t chain_slots;
   int32_t S, V, order;
+  int32_t pad_quad;             // an all-padding quad (tokens V): target of idle gather lanes
   unsigned long long* bad_row;  // sticky min bad row (ULLONG_MAX = none)
 };
 
