@@ -47,6 +47,7 @@ enum { NGPULM_OK = 0, NGPULM_EDOMAIN = 1, NGPULM_EUSAGE = 2, NGPULM_ECUDA = 3, N
 enum { NGPULM_CTC = 0, NGPULM_RNNT = 1, NGPULM_AED = 2 };
 enum { NGPULM_MAX_ORDER = 32 };
 enum { NGPULM_CHAIN_TABLE = 0, NGPULM_CHAIN_WALK = 1 };
+enum { NGPULM_ADVANCE_AUTO = 0, NGPULM_ADVANCE_WARP = 1, NGPULM_ADVANCE_CTA = 2 };
 
 typedef struct {
   int32_t order;          /* N, highest n-gram order in the ARPA */
@@ -61,6 +62,8 @@ typedef struct {
   int64_t device_bytes;   /* bytes of the resident model on the device */
   int32_t max_vocab;      /* largest V the kernels accept */
   int32_t chain_mode;     /* NGPULM_CHAIN_TABLE or NGPULM_CHAIN_WALK */
+  int32_t advance_kernel; /* NGPULM_ADVANCE_* as set (AUTO by default) */
+  int32_t packed_arcs;    /* 1: the device also holds arcs packed as (target << bits) | token */
 } ngpulm_info;
 
 /* Read-only view of the model's host copy of the flat arrays.
@@ -103,6 +106,18 @@ void ngpulm_free(ngpulm_model* model);
  * Both give bit-identical results. Not to be called concurrently with hot-path
  * calls on the same model (it changes what later launches read). */
 int ngpulm_set_chain_mode(ngpulm_model* model, int32_t mode);
+
+/* Which kernel ngpulm_advance runs; all give
+ * bit-identical results:
+ *   NGPULM_ADVANCE_AUTO (default): one warp per row, reading the arcs packed as
+ *     (target << ceil(log2 V)) | token beside the weights when every target
+ *     fits (info.packed_arcs), else as NGPULM_ADVANCE_WARP;
+ *   NGPULM_ADVANCE_WARP: one warp per row over the token/weight/target arrays;
+ *   NGPULM_ADVANCE_CTA: one 256-thread CTA per row.
+ * The warp kernels need V % 4 == 0 and 16-byte aligned outputs; otherwise
+ * (and always for CTA) the CTA kernel runs. Same concurrency rule as
+ * ngpulm_set_chain_mode. EUSAGE for an unknown kind. */
+int ngpulm_set_advance_kernel(ngpulm_model* model, int32_t kind);
 int ngpulm_get_info(const ngpulm_model* model, ngpulm_info* out);
 int ngpulm_host_view_get(const ngpulm_model* model, ngpulm_host_view* out);
 const char* ngpulm_last_error(void);

@@ -21,6 +21,7 @@ LIB_PATH = os.environ.get("NGPULM_LIB") or os.path.join(HERE, "lib", "libngpulm.
 NGPULM_OK, NGPULM_EDOMAIN, NGPULM_EUSAGE, NGPULM_ECUDA, NGPULM_EIO = 0, 1, 2, 3, 4
 CTC, RNNT, AED = 0, 1, 2
 CHAIN_TABLE, CHAIN_WALK = 0, 1
+ADVANCE_AUTO, ADVANCE_WARP, ADVANCE_CTA = 0, 1, 2
 MAX_ORDER = 32
 
 
@@ -34,7 +35,8 @@ class Info(C.Structure):
     _fields_ = [("order", C.c_int32), ("vocab_size", C.c_int32), ("num_states", C.c_int32),
                 ("root_state", C.c_int32), ("bos_state", C.c_int32), ("device", C.c_int32),
                 ("num_arcs", C.c_int64), ("num_unk_filled", C.c_int64), ("num_dropped", C.c_int64),
-                ("device_bytes", C.c_int64), ("max_vocab", C.c_int32), ("chain_mode", C.c_int32)]
+                ("device_bytes", C.c_int64), ("max_vocab", C.c_int32), ("chain_mode", C.c_int32),
+                ("advance_kernel", C.c_int32), ("packed_arcs", C.c_int32)]
 
 
 class HostView(C.Structure):
@@ -51,6 +53,7 @@ SIGNATURES = {
     "ngpulm_replicate": (C.c_int, [_P, _I32, C.POINTER(_P)]),
     "ngpulm_free": (None, [_P]),
     "ngpulm_set_chain_mode": (C.c_int, [_P, _I32]),
+    "ngpulm_set_advance_kernel": (C.c_int, [_P, _I32]),
     "ngpulm_get_info": (C.c_int, [_P, C.POINTER(Info)]),
     "ngpulm_host_view_get": (C.c_int, [_P, C.POINTER(HostView)]),
     "ngpulm_last_error": (C.c_char_p, []),
@@ -133,6 +136,12 @@ class NgpuLM:
         """CHAIN_TABLE (load-time chain records, default) or CHAIN_WALK (Algorithm 1 walk)."""
         _check(lib().ngpulm_set_chain_mode(self._h, mode))
         self.info.chain_mode = mode
+
+    def set_advance_kernel(self, kind: int) -> None:
+        """ADVANCE_AUTO (default: one warp per row, packed arcs when they fit),
+        ADVANCE_WARP (one warp per row, three arc arrays) or ADVANCE_CTA (one CTA per row)."""
+        _check(lib().ngpulm_set_advance_kernel(self._h, kind))
+        self.info.advance_kernel = kind
 
     def replicate(self, device: int) -> "NgpuLM":
         out = C.c_void_p()
@@ -261,6 +270,7 @@ ngpulm_fused_greedy_step = NgpuLM.fused_greedy_step
 ngpulm_check = NgpuLM.check
 ngpulm_replicate = NgpuLM.replicate
 ngpulm_set_chain_mode = NgpuLM.set_chain_mode
+ngpulm_set_advance_kernel = NgpuLM.set_advance_kernel
 ngpulm_state_of = NgpuLM.state_of
 ngpulm_advance_host = NgpuLM.advance_host
 ngpulm_touched_bytes = NgpuLM.touched_bytes

@@ -413,7 +413,7 @@ int build_from_arpa(const char* arpa_path, const char* vocab_path, int32_t V, Ho
   return NGPULM_OK;
 }
 
-size_t device_arc_layout(const HostModel& m, std::vector<int32_t>& arc_begin, int32_t& pad_quad) {
+size_t device_arc_layout(const HostModel& m, std::vector<int32_t>& arc_begin) {
   const int32_t S = m.num_states;
   arc_begin.assign((size_t)S, 0);
   size_t cur = 0;
@@ -421,8 +421,18 @@ size_t device_arc_layout(const HostModel& m, std::vector<int32_t>& arc_begin, in
     arc_begin[(size_t)s] = (int32_t)cur;
     cur = (cur + (size_t)(m.arc_off[s + 1] - m.arc_off[s]) + 3) & ~(size_t)3;
   }
-  pad_quad = (int32_t)(cur / 4);
-  return cur + 4;
+  return cur;
+}
+
+int32_t packed_token_bits(int32_t V) {
+  int32_t b = 1;
+  while ((int64_t)1 << b < (int64_t)V) ++b;
+  return b;
+}
+
+bool packable(const HostModel& m) {
+  const int32_t b = packed_token_bits(m.V);
+  return b < 32 && (int64_t)m.num_states <= ((int64_t)1 << (32 - b));
 }
 
 void build_chain_table(const HostModel& m, const std::vector<int32_t>& arc_begin, std::vector<int32_t>& out,

@@ -57,8 +57,9 @@ int upload(ngpulm_model* m, int device) {
   const ngpulm::HostModel& h = m->h;
   const size_t S = (size_t)h.num_states;
   std::vector<int32_t> dbeg;
-  int32_t pad_quad = 0;
-  const size_t A = ngpulm::device_arc_layout(h, dbeg, pad_quad);  // padded arc count
+  const size_t A = ngpulm::device_arc_layout(h, dbeg);  // padded arc count
+  const bool pack = ngpulm::packable(h);
+  const int32_t pk_bits = ngpulm::packed_token_bits(h.V);
   if (A > (size_t)INT32_MAX) return err(NGPULM_EUSAGE, "too many arcs for 32-bit arc indices");
   const size_t o_srec = 0;
   const size_t o_fin = align256(o_srec + S * sizeof(ngpulm::StateRec));
@@ -68,7 +69,8 @@ int upload(ngpulm_model* m, int device) {
   std::vector<int32_t> chain;
   int32_t slots = 1;
   ngpulm::build_chain_table(h, dbeg, chain, slots);
-  const size_t o_chain = align256(o_to + A * 4);
+  const size_t o_pk = align256(o_to + A * 4);
+  const size_t o_chain = align256(o_pk + (pack ? A * 4 : 0));
   const size_t o_bad = align256(o_chain + chain.size() * 4);
   const size_t total = align256(o_bad + 8);
   std::vector<unsigned char> stage(total, 0);
@@ -76,13 +78,18 @@ int upload(ngpulm_model* m, int device) {
   auto* tok = reinterpret_cast<int32_t*>(stage.data() + o_tok);
   auto* wt = reinterpret_cast<float*>(stage.data() + o_w);
   auto* to = reinterpret_cast<int32_t*>(stage.data() + o_to);
-  std::fill(tok, tok + A, h.V);  // padding arcs: token V = the kernels' trash column
+  auto* pk = reinterpret_cast<uint32_t*>(stage.data() + o_pk);
   for (size_t s = 0; s < S; ++s) {
     const int32_t b = h.arc_off[s], cnt = h.arc_off[s + 1] - b;
     rec[s] = {dbeg[s], dbeg[s] + cnt, h.boff_to[s], h.boff_w[s]};
-    std::memcpy(tok + dbeg[s], h.arc_tok.data() + b, (size_t)cnt * 4);
-    std::memcpy(wt + dbeg[s], h.arc_w.data() + b, (size_t)cnt * 4);
-    std::memcpy(to + dbeg[s], h.arc_to.data() + b, (size_t)cnt * 4);
+    const int32_t end = s + 1 < S ? dbeg[s + 1] : (int32_t)A;
+    for (int32_t j = 0; j < end - dbeg[s]; ++j) {  // the padding repeats the last arc
+      const int32_t src = b + std::min(j, cnt - 1);
+      tok[dbeg[s] + j] = h.arc_tok[src];
+      wt[dbeg[s] + j] = h.arc_w[src];
+      to[dbeg[s] + j] = h.arc_to[src];
+      if (pack) pk[dbeg[s] + j] = ((uint32_t)h.arc_to[src] << pk_bits) | (uint32_t)h.arc_tok[src];
+    }
   }
   std::memcpy(stage.data() + o_fin, h.final_w.data(), S * 4);
   std::memcpy(stage.data() + o_chain, chain.data(), chain.size() * 4);
@@ -110,7 +117,9 @@ int upload(ngpulm_model* m, int device) {
   m->dm.S = h.num_states;
   m->dm.V = h.V;
   m->dm.order = h.order;
-  m->dm.pad_quad = pad_quad;
+  m->dm.arc_pk = pack ? reinterpret_cast<const uint32_t*>(base + o_pk) : nullptr;
+  m->dm.pk_bits = pk_bits;
+  m->dm.adv_kind = NGPULM_ADVANCE_AUTO;
   return NGPULM_OK;
 }
 
@@ -174,6 +183,14 @@ void ngpulm_free(ngpulm_model* m) {
   delete m;
 }
 
+int ngpulm_set_advance_kernel(ngpulm_model* m, int32_t kind) {
+  if (!m) return err(NGPULM_EUSAGE, "model is NULL");
+  if (kind != NGPULM_ADVANCE_AUTO && kind != NGPULM_ADVANCE_WARP && kind != NGPULM_ADVANCE_CTA)
+    return err(NGPULM_EUSAGE, "bad advance kernel kind");
+  m->dm.adv_kind = kind;
+  return NGPULM_OK;
+}
+
 int ngpulm_set_chain_mode(ngpulm_model* m, int32_t mode) {
   if (!m) return err(NGPULM_EUSAGE, "model is NULL");
   if (mode != NGPULM_CHAIN_TABLE && mode != NGPULM_CHAIN_WALK) return err(NGPULM_EUSAGE, "bad chain mode");
@@ -197,6 +214,8 @@ int ngpulm_get_info(const ngpulm_model* m, ngpulm_info* out) {
   out->device_bytes = (int64_t)m->blob_bytes;
   out->max_vocab = ngpulm::max_vocab_supported();
   out->chain_mode = m->chain_mode;
+  out->advance_kernel = m->dm.adv_kind;
+  out->packed_arcs = m->dm.arc_pk != nullptr;
   return NGPULM_OK;
 }
 

@@ -516,24 +516,29 @@ __device__ __forceinline__ Row warp_row(const DevModel& m, const int32_t* state_
 }
 
 // One window of kW slots, in registers, processed in groups of 8 slots; a
-// group wholly past the row's last slot is skipped (uniform branch).
-template <int kW>
+// group wholly past the row's last slot is skipped (uniform branch). Arcs are
+// either packed ((target << pk_bits) | token next to the weight: two 16-byte
+// loads per quad) or three arrays (three loads per quad).
+template <int kW, bool kPacked>
 struct Window {
-  int4 tok[kW];
   float4 w[kW];
-  int4 to[kW];
+  int4 tok[kW];  // packed: (target << pk_bits) | token
+  int4 to[kPacked ? 1 : kW];
   float acc[kW];  // acc_boff of the slot's level
 };
 
 // Within a group everything is branch-free, so the group's shuffles and loads
 // are scheduled together. A level starts on a quad boundary and the rest of
-// its last quad is padding (token V), so a quad needs no mask; an idle lane
-// loads the all-padding quad. Padding tokens write the trash word.
-template <int kW>
+// its last quad repeats its last arc, so whole quads are written; an idle lane
+// (past its level's quads) loads the level's first quad again, and a slot
+// past the row's last one repeats the last slot (of the highest order, which
+// is written last anyway): rewriting an arc of the same level stores the
+// value already there.
+template <int kW, bool kPacked>
 __device__ __forceinline__ void load_window(const DevModel& m, const WLevel& lv, int32_t nlev, int32_t k0,
-                                            int32_t nslots, int32_t pad_quad, Window<kW>& a) {
+                                            int32_t nslots, Window<kW, kPacked>& a) {
   const int lane = threadIdx.x & 31;
-  const int4* tok4 = reinterpret_cast<const int4*>(m.arc_tok);
+  const int4* tok4 = kPacked ? reinterpret_cast<const int4*>(m.arc_pk) : reinterpret_cast<const int4*>(m.arc_tok);
   const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
   const int4* to4 = reinterpret_cast<const int4*>(m.arc_to);
 #pragma unroll
@@ -542,39 +547,49 @@ __device__ __forceinline__ void load_window(const DevModel& m, const WLevel& lv,
     int32_t qv[8];
 #pragma unroll
     for (int u = g; u < g + 8; ++u) {
-      const int32_t k = k0 + u;
+      const int32_t k = min(k0 + u, nslots - 1);  // a slot past the last one repeats the last one
       // levels entirely before slot k (in slot order) are the levels after its own
       const int32_t L = nlev - 1 - __popc(__ballot_sync(kFull, lv.eslot <= k));
       const int src = L + 1;
       const int32_t info = __shfl_sync(kFull, lv.info, src), b = __shfl_sync(kFull, lv.beg, src);
       a.acc[u] = __shfl_sync(kFull, lv.acc, src);
       const int32_t i = (k - (info >> 16)) * 32 + lane;
-      qv[u - g] = (k < nslots && i < (info & 0xffff)) ? (b >> 2) + i : pad_quad;
+      qv[u - g] = (b >> 2) + (i < (info & 0xffff) ? i : 0);
     }
 #pragma unroll
     for (int u = g; u < g + 8; ++u) {
       a.tok[u] = __ldg(tok4 + qv[u - g]);
       a.w[u] = __ldg(w4 + qv[u - g]);
-      a.to[u] = __ldg(to4 + qv[u - g]);
+      if (!kPacked) a.to[u] = __ldg(to4 + qv[u - g]);
     }
   }
 }
 
-template <int kW>
-__device__ __forceinline__ void write_window(const WSlice& s, const Window<kW>& a, int32_t k0, int32_t nslots) {
+template <int kW, bool kPacked>
+__device__ __forceinline__ void write_window(const WSlice& s, const Window<kW, kPacked>& a, int32_t k0,
+                                             int32_t nslots, int32_t pk_bits) {
+  const uint32_t tmask = (1u << pk_bits) - 1u;
 #pragma unroll
   for (int g = 0; g < kW; g += 8) {
     if (g > 0 && k0 + g >= nslots) break;
 #pragma unroll
     for (int u = g; u < g + 8; ++u) {
       if (u > 0) __syncwarp();  // slots in level order: a lower order is done before a higher one
-      const int32_t tk[4] = {a.tok[u].x, a.tok[u].y, a.tok[u].z, a.tok[u].w};
+      const int32_t x[4] = {a.tok[u].x, a.tok[u].y, a.tok[u].z, a.tok[u].w};
       const float ww[4] = {a.w[u].x, a.w[u].y, a.w[u].z, a.w[u].w};
-      const int32_t nn[4] = {a.to[u].x, a.to[u].y, a.to[u].z, a.to[u].w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        s.row_s[tk[j]] = __fadd_rn(a.acc[u], ww[j]);  // acc_boff + arc_weights (Alg. 1 line 74)
-        s.row_n[tk[j]] = nn[j];
+        int32_t tk, nx;
+        if (kPacked) {
+          tk = (int32_t)((uint32_t)x[j] & tmask);
+          nx = (int32_t)((uint32_t)x[j] >> pk_bits);
+        } else {
+          const int32_t t4[4] = {a.to[u].x, a.to[u].y, a.to[u].z, a.to[u].w};
+          tk = x[j];
+          nx = t4[j];
+        }
+        s.row_s[tk] = __fadd_rn(a.acc[u], ww[j]);  // acc_boff + arc_weights (Alg. 1 line 74)
+        s.row_n[tk] = nx;
       }
     }
   }
@@ -613,7 +628,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-template <bool kTable, int kW>
+template <bool kTable, int kW, bool kPacked>
 __global__ void __launch_bounds__(256)
     advance_warp_kernel(DevModel m, const int32_t* __restrict__ states, int32_t B, float* __restrict__ scores,
                         int32_t* __restrict__ next, float* __restrict__ final_out) {
@@ -671,21 +686,21 @@ __global__ void __launch_bounds__(256)
   }
   mbar_wait(bar, 0);  // the CTA's root weights have landed (long ago, normally)
   STAMP(3);
-  Window<kW> a;
+  Window<kW, kPacked> a;
   // the root fill goes first: its shared-memory loads would otherwise return
   // behind the arc gathers
   if (!(skip & 8)) root_fill(s, root_w, r.acc_root, V);
   STAMP(12);
   if (skip & 4) nslots = 0;
-  if (!(skip & 4)) load_window<kW>(m, lv, r.nlev, 0, nslots, m.pad_quad, a);
+  if (!(skip & 4)) load_window<kW, kPacked>(m, lv, r.nlev, 0, nslots, a);
   STAMP(4);
   mbar_wait(s.bar, 0);  // root targets in row_n
   __syncwarp();
   STAMP(5);
   for (int32_t k0 = 0; k0 < nslots;) {
-    write_window<kW>(s, a, k0, nslots);
+    write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
     k0 += kW;
-    if (k0 < nslots) load_window<kW>(m, lv, r.nlev, k0, nslots, m.pad_quad, a);
+    if (k0 < nslots) load_window<kW, kPacked>(m, lv, r.nlev, k0, nslots, a);
   }
   STAMP(6);
   // step 4: the row leaves by two bulk stores issued by lane 0
@@ -855,11 +870,7 @@ int launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStrea
   return (int)cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-int g_row_mode = 1;  // advance: 1 = one warp per row (when it fits), 0 = one CTA per row
-
 }  // namespace
-
-extern "C" int ngpulm_debug_row_mode(int mode) { g_row_mode = mode; return 0; }
 
 #ifdef NGPULM_PHASE_TIMING
 // lat3-style probe on the model's own data: states[b] -> chain record, by warp 0.
@@ -900,7 +911,7 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
   const bool vec = (m.V % 4 == 0) && ((uintptr_t)scores % 16 == 0) && ((uintptr_t)next % 16 == 0);
   const bool table = m.chain != nullptr;
   cudaStream_t st = (cudaStream_t)stream;
-  if (vec && g_row_mode == 1) {
+  if (vec && m.adv_kind != NGPULM_ADVANCE_CTA) {
     int R = (B + 147) / 148;
     R = R < 1 ? 1 : (R > 8 ? 8 : R);
     while (R > 1 && wcta_smem(m.V, m.order, R) > 227 * 1024) --R;
@@ -909,12 +920,18 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
       const dim3 wg((B + R - 1) / R), wb(32 * R);
       // up to 8 rows per SM: 16-slot windows (almost every row in one window);
       // more rows per SM: 8-slot windows (registers for occupancy)
-      if (B <= 8 * 148) {
-        if (table) return launch(advance_warp_kernel<true, 16>, wg, wb, wsm, st, m, states, B, scores, next, final_out);
-        return launch(advance_warp_kernel<false, 16>, wg, wb, wsm, st, m, states, B, scores, next, final_out);
+      const bool wide = B <= 8 * 148, pk = m.arc_pk != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO;
+#define NGPULM_WARP_LAUNCH(T, W, P) \
+  return launch(advance_warp_kernel<T, W, P>, wg, wb, wsm, st, m, states, B, scores, next, final_out)
+      if (table) {
+        if (wide) { if (pk) NGPULM_WARP_LAUNCH(true, 16, true); NGPULM_WARP_LAUNCH(true, 16, false); }
+        if (pk) NGPULM_WARP_LAUNCH(true, 8, true);
+        NGPULM_WARP_LAUNCH(true, 8, false);
       }
-      if (table) return launch(advance_warp_kernel<true, 8>, wg, wb, wsm, st, m, states, B, scores, next, final_out);
-      return launch(advance_warp_kernel<false, 8>, wg, wb, wsm, st, m, states, B, scores, next, final_out);
+      if (wide) { if (pk) NGPULM_WARP_LAUNCH(false, 16, true); NGPULM_WARP_LAUNCH(false, 16, false); }
+      if (pk) NGPULM_WARP_LAUNCH(false, 8, true);
+      NGPULM_WARP_LAUNCH(false, 8, false);
+#undef NGPULM_WARP_LAUNCH
     }
   }
   const size_t sm = row_smem(m.V, m.order);

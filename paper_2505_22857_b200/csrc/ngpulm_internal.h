@@ -40,10 +40,15 @@ int build_from_arpa(const char* arpa_path, const char* vocab_path, int32_t vocab
 
 // Device arc layout: state s's arcs start at
 // arc_begin[s], a multiple of 4 (one 16-byte quad); the gap before the next
-// state holds padding arcs {token V, weight 0, target 0} (V is the kernels'
-// trash column), and one all-padding quad (pad_quad) follows the last state.
-// Returns the padded arc count (pad quad included).
-size_t device_arc_layout(const HostModel& m, std::vector<int32_t>& arc_begin, int32_t& pad_quad);
+// state repeats the state's last arc, so a whole quad can be written into a
+// row (a repeated arc rewrites the value it already wrote). Returns the
+// padded arc count.
+size_t device_arc_layout(const HostModel& m, std::vector<int32_t>& arc_begin);
+
+// Bits of the token field in a packed arc ((target << bits) | token), and
+// whether every target fits the remaining bits.
+int32_t packed_token_bits(int32_t V);
+bool packable(const HostModel& m);
 
 // Load-time chain table (DESIGN.md §Kernels "chain table"): per state a fixed
 // record of `slots` int4: slot 0 = {nlev, acc_root, final, total_arcs}, slots
@@ -67,7 +72,9 @@ struct DevModel {
   const void* chain;  // chain table (int4 records) or nullptr = walk the chain at query time
   int32_t chain_slots;
   int32_t S, V, order;
-  int32_t pad_quad;             // an all-padding quad (tokens V): target of idle gather lanes
+  const uint32_t* arc_pk;       // packed arcs (target << pk_bits) | token, or nullptr (targets too large)
+  int32_t pk_bits;
+  int32_t adv_kind;             // NGPULM_ADVANCE_*
   unsigned long long* bad_row;  // sticky min bad row (ULLONG_MAX = none)
 };
 

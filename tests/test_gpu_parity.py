@@ -39,6 +39,24 @@ def pairs(small_lms, fig1_paths):
     return out
 
 
+KERNELS = [ng.ADVANCE_AUTO, ng.ADVANCE_WARP, ng.ADVANCE_CTA]
+
+
+class using:
+    """Temporarily select the chain mode / advance kernel of a model."""
+
+    def __init__(self, m, chain=ng.CHAIN_TABLE, kernel=ng.ADVANCE_AUTO):
+        self.m, self.chain, self.kernel = m, chain, kernel
+
+    def __enter__(self):
+        self.m.set_chain_mode(self.chain)
+        self.m.set_advance_kernel(self.kernel)
+
+    def __exit__(self, *exc):
+        self.m.set_chain_mode(ng.CHAIN_TABLE)
+        self.m.set_advance_kernel(ng.ADVANCE_AUTO)
+
+
 def gpu_advance(m, states_np):
     st = torch.from_numpy(np.ascontiguousarray(states_np, np.int32)).to(dev())
     s, n, f = m.advance(st)
@@ -46,18 +64,17 @@ def gpu_advance(m, states_np):
     return s.cpu().numpy(), n.cpu().numpy(), f.cpu().numpy()
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("chain", [ng.CHAIN_TABLE, ng.CHAIN_WALK])
 @pytest.mark.parametrize("name", SMALL + ["fig1"])
-def test_advance_exhaustive_small(pairs, name, chain):
+def test_advance_exhaustive_small(pairs, name, chain, kernel):
     """All states x all tokens of every small LM (config 0 = tiny3), both ways of
-    obtaining the back-off levels (load-time chain table / Algorithm 1 walk)."""
+    obtaining the back-off levels (load-time chain table / Algorithm 1 walk),
+    every advance kernel."""
     m, o, _ = pairs[name]
-    m.set_chain_mode(chain)
     states = np.arange(o.num_states, dtype=np.int32)
-    try:
+    with using(m, chain, kernel):
         s, n, f = gpu_advance(m, states)
-    finally:
-        m.set_chain_mode(ng.CHAIN_TABLE)
     s32, s64, n_o, _ = o.rows(states)
     f32, f64 = o.finals(states)
     assert np.array_equal(n, n_o)
@@ -119,19 +136,18 @@ def trajectory_states(m, f, n, seed):
     return np.array([m.state_of(b, t) for b, t in ctx], dtype=np.int32), ctx
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("chain", [ng.CHAIN_TABLE, ng.CHAIN_WALK])
-def test_config1_b128_full_rows(lm6, chain):
+def test_config1_b128_full_rows(lm6, chain, kernel):
     m, o, f = lm6
-    m.set_chain_mode(chain)
     assert m.info.num_arcs > 500_000 and 800_000 < sum(1 for _ in open(f.arpa)) < 1_300_000
+    assert m.info.packed_arcs == 1
     st_traj, ctx = trajectory_states(m, f, 96, seed=2)
     # the library's and the oracle's context -> state maps agree (R6, R7)
     assert [o.state_of(b, t) for b, t in ctx] == st_traj.tolist()
     states = np.concatenate([st_traj, synth.uniform_states(m.num_states, 32, seed=3)])
-    try:
+    with using(m, chain, kernel):
         s, n, fin = gpu_advance(m, states)
-    finally:
-        m.set_chain_mode(ng.CHAIN_TABLE)
     s32, s64, n_o, lv = o.rows(states)
     f32, _ = o.finals(states)
     assert np.array_equal(n, n_o) and same_bits(s, s32) and same_bits(fin, f32)
@@ -139,11 +155,13 @@ def test_config1_b128_full_rows(lm6, chain):
     assert lv.max() <= 6
 
 
-def test_headline_b1024_sampled_rows(lm6):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_headline_b1024_sampled_rows(lm6, kernel):
     """The bench launch (B=1024 trajectory rows) checked on sampled rows."""
     m, o, f = lm6
     states, _ = trajectory_states(m, f, 1024, seed=2)
-    s, n, fin = gpu_advance(m, states)
+    with using(m, kernel=kernel):
+        s, n, fin = gpu_advance(m, states)
     rows = np.random.default_rng(5).choice(1024, 48, replace=False)
     s32, s64, n_o, _ = o.rows(states[rows])
     assert np.array_equal(n[rows], n_o) and same_bits(s[rows], s32)
@@ -152,9 +170,32 @@ def test_headline_b1024_sampled_rows(lm6):
     tot = np.exp(s.astype(np.float64)).sum(1) + np.exp(fin.astype(np.float64))
     assert np.max(np.abs(tot - 1)) < 1e-4
     # sharded == unsharded, bit for bit (rows are independent)
-    parts = [gpu_advance(m, states[i:i + 256]) for i in range(0, 1024, 256)]
+    with using(m, kernel=kernel):
+        parts = [gpu_advance(m, states[i:i + 256]) for i in range(0, 1024, 256)]
     assert same_bits(np.concatenate([p[0] for p in parts]), s)
     assert np.array_equal(np.concatenate([p[1] for p in parts]), n)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_large_batch_b4096_sampled_rows(lm6, kernel):
+    """More rows than 8 per SM (the warp kernel's 8-slot windows) and the heaviest rows."""
+    m, o, f = lm6
+    states, _ = trajectory_states(m, f, 4096, seed=4)
+    with using(m, kernel=kernel):
+        s, n, _ = gpu_advance(m, states)
+    h = m.host_arrays()
+    off, bt = h["arc_offsets"], h["boff_to_states"]
+
+    def total(x):
+        t = 0
+        while x != 0:
+            t += int(off[x + 1] - off[x])
+            x = int(bt[x])
+        return t
+    T = np.array([total(int(x)) for x in states])
+    rows = np.unique(np.concatenate([np.argsort(-T)[:24], np.random.default_rng(8).choice(4096, 24, replace=False)]))
+    s32, _, n_o, _ = o.rows(states[rows], want64=False)
+    assert np.array_equal(n[rows], n_o) and same_bits(s[rows], s32)
 
 
 def test_advance_host_and_replica_and_streams(lm6):

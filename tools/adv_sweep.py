@@ -60,15 +60,15 @@ if os.environ.get("SWEEP_QUICK"):
     MODES, BS = MODES[:1], (1, 128, 1024, 4096)
 print("lib", os.path.basename(ng.LIB_PATH))
 print("B, kernel, mode, graph_us_per_call, single_launch_us, GB/s(graph)")
-ROW_MODES = [int(x) for x in os.environ.get("SWEEP_ROW_MODES", "1,0").split(",")]
+KINDS = [int(x) for x in os.environ.get("SWEEP_KERNELS", "0,1,2").split(",")]
 if os.environ.get("SWEEP_SKIP"):  # debug build only: parts of the warp kernel switched off (timing only)
     ng.lib().ngpulm_debug_skip(int(os.environ["SWEEP_SKIP"]))
     print("skip bits", os.environ["SWEEP_SKIP"])
-for rm in ROW_MODES:
-    ng.lib().ngpulm_debug_row_mode(rm)
+for kind in KINDS:
+    m.set_advance_kernel(kind)
     for mode, name in MODES:
         for B in BS:
             gus, sus = run(B, mode)
-            print(f"{B:5d} {'warp' if rm else 'cta ':4s} {name:5s} {gus:8.2f} {sus:8.2f} {B*1024*8/gus/1e3:8.1f}",
-                  flush=True)
-ng.lib().ngpulm_debug_row_mode(1)
+            print(f"{B:5d} {['auto', 'warp', 'cta'][kind]:4s} {name:5s} {gus:8.2f} {sus:8.2f} "
+                  f"{B*1024*8/gus/1e3:8.1f}", flush=True)
+m.set_advance_kernel(ng.ADVANCE_AUTO)

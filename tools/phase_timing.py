@@ -21,9 +21,9 @@ import synth  # noqa: E402
 
 L = ng.lib()
 L.ngpulm_debug_phases.argtypes = [C.c_void_p, C.c_int]
-L.ngpulm_debug_row_mode(int(os.environ.get("ROW_MODE", "1")))
 f = synth.make_lm("/tmp/ngpulm_prof", 1024, 6, tokens=430000, seed=1, heldout=4000, tag="bench_6gram")
 m = ng.load_arpa(f.arpa, vocab_size=1024, device=0)
+m.set_advance_kernel(int(os.environ.get("ADVANCE_KERNEL", "0")))
 ctx = synth.sample_contexts(synth.read_sentences(f.heldout), 6, 4096 * 16, seed=2)
 allst = np.array([m.state_of(b, t) for b, t in ctx], dtype=np.int32)
 stream = torch.cuda.Stream()
