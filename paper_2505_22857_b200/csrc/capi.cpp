@@ -69,8 +69,8 @@ int upload(ngpulm_model* m, int device) {
   std::vector<int32_t> chain;
   int32_t slots = 1;
   ngpulm::build_chain_table(h, dbeg, chain, slots);
-  const size_t o_pk = align256(o_to + A * 4);
-  const size_t o_chain = align256(o_pk + (pack ? A * 4 : 0));
+  const size_t o_q = align256(o_to + A * 4);
+  const size_t o_chain = align256(o_q + (pack ? A * 8 : 0));
   const size_t o_bad = align256(o_chain + chain.size() * 4);
   const size_t total = align256(o_bad + 8);
   std::vector<unsigned char> stage(total, 0);
@@ -78,7 +78,7 @@ int upload(ngpulm_model* m, int device) {
   auto* tok = reinterpret_cast<int32_t*>(stage.data() + o_tok);
   auto* wt = reinterpret_cast<float*>(stage.data() + o_w);
   auto* to = reinterpret_cast<int32_t*>(stage.data() + o_to);
-  auto* pk = reinterpret_cast<uint32_t*>(stage.data() + o_pk);
+  auto* aq = reinterpret_cast<uint32_t*>(stage.data() + o_q);  // [A/4][8]
   for (size_t s = 0; s < S; ++s) {
     const int32_t b = h.arc_off[s], cnt = h.arc_off[s + 1] - b;
     rec[s] = {dbeg[s], dbeg[s] + cnt, h.boff_to[s], h.boff_w[s]};
@@ -88,7 +88,11 @@ int upload(ngpulm_model* m, int device) {
       tok[dbeg[s] + j] = h.arc_tok[src];
       wt[dbeg[s] + j] = h.arc_w[src];
       to[dbeg[s] + j] = h.arc_to[src];
-      if (pack) pk[dbeg[s] + j] = ((uint32_t)h.arc_to[src] << pk_bits) | (uint32_t)h.arc_tok[src];
+      if (pack) {
+        const size_t a = (size_t)dbeg[s] + j, unit = a / 4, k = a % 4;
+        aq[unit * 8 + k] = ((uint32_t)h.arc_to[src] << pk_bits) | (uint32_t)h.arc_tok[src];
+        std::memcpy(&aq[unit * 8 + 4 + k], &h.arc_w[src], 4);
+      }
     }
   }
   std::memcpy(stage.data() + o_fin, h.final_w.data(), S * 4);
@@ -117,7 +121,7 @@ int upload(ngpulm_model* m, int device) {
   m->dm.S = h.num_states;
   m->dm.V = h.V;
   m->dm.order = h.order;
-  m->dm.arc_pk = pack ? reinterpret_cast<const uint32_t*>(base + o_pk) : nullptr;
+  m->dm.arc_q = pack ? static_cast<const void*>(base + o_q) : nullptr;
   m->dm.pk_bits = pk_bits;
   m->dm.adv_kind = NGPULM_ADVANCE_AUTO;
   return NGPULM_OK;
@@ -215,7 +219,7 @@ int ngpulm_get_info(const ngpulm_model* m, ngpulm_info* out) {
   out->max_vocab = ngpulm::max_vocab_supported();
   out->chain_mode = m->chain_mode;
   out->advance_kernel = m->dm.adv_kind;
-  out->packed_arcs = m->dm.arc_pk != nullptr;
+  out->packed_arcs = m->dm.arc_q != nullptr;
   return NGPULM_OK;
 }
 

@@ -424,12 +424,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #endif
 
 __host__ __device__ constexpr size_t wrow_bytes(int32_t V) { return align16((size_t)V * 4 + 4); }  // + trash word
-__host__ __device__ constexpr size_t wslice_bytes(int32_t V, int32_t order) {
-  return 2 * wrow_bytes(V) + levels_bytes(order) + 16;
+// staged arcs: kStageQuads packed arc quads (32 bytes each)
+constexpr int kStageQuads = 512;
+#ifndef NGPULM_STAGE_MAX_B
+#define NGPULM_STAGE_MAX_B 148  // batches of 2 .. one row per SM stage their arcs by bulk copy (measured)
+#endif
+__host__ __device__ constexpr size_t wslice_bytes(int32_t V, int32_t order, int stage_q) {
+  return 2 * wrow_bytes(V) + levels_bytes(order) + 16 + (size_t)stage_q * 32;
 }
-// root_w[V] | mbarrier | R x (row_s[V+1] | row_n[V+1] | levels | mbarrier)
-__host__ __device__ constexpr size_t wcta_smem(int32_t V, int32_t order, int R) {
-  return align16((size_t)V * 4) + 16 + (size_t)R * wslice_bytes(V, order);
+// root_w[V] | mbarrier | R x (row_s[V+1] | row_n[V+1] | levels | 2 mbarriers | staged arcs)
+__host__ __device__ constexpr size_t wcta_smem(int32_t V, int32_t order, int R, int stage_q) {
+  return align16((size_t)V * 4) + 16 + (size_t)R * wslice_bytes(V, order, stage_q);
 }
 
 struct WSlice {
@@ -438,10 +443,12 @@ struct WSlice {
   int32_t* beg;  // levels (walk mode: written by lane 0)
   int32_t* pre;
   float* acc;
-  uint64_t* bar;  // the root targets' bulk copy into row_n
+  uint64_t* bar;   // the root targets' bulk copy into row_n
+  uint64_t* abar;  // the arcs' bulk copies into the staging area
+  int4* st_q;      // [stage_q][2] staged packed arc quads
 };
 
-__device__ __forceinline__ WSlice wcarve(unsigned char* p, int32_t V, int32_t order) {
+__device__ __forceinline__ WSlice wcarve(unsigned char* p, int32_t V, int32_t order, int stage_q) {
   const int32_t Lc = level_cap(order);
   WSlice s;
   s.row_s = reinterpret_cast<float*>(p);
@@ -453,11 +460,14 @@ __device__ __forceinline__ WSlice wcarve(unsigned char* p, int32_t V, int32_t or
   s.pre = l + Lc;
   s.acc = reinterpret_cast<float*>(l + 2 * Lc + 1);
   s.bar = reinterpret_cast<uint64_t*>(p + levels_bytes(order));
+  s.abar = s.bar + 1;
+  s.st_q = reinterpret_cast<int4*>(p + levels_bytes(order) + 16);
   return s;
 }
 
 struct WLevel {  // lane l+1: level l of the row
   int32_t beg;       // first arc (16-byte aligned in the device layout)
+  int32_t qbase;     // first quad of the level where the gathers read it (global arrays or staging)
   int32_t info;      // (first slot << 16) | quads
   int32_t eslot;     // one past the level's last slot (INT_MAX on lanes without a level)
   float acc;         // acc_boff at the level
@@ -469,7 +479,7 @@ __device__ __forceinline__ Row warp_row(const DevModel& m, const int32_t* state_
                                         int32_t& nslots) {
   const int lane = threadIdx.x & 31;
   Row r;
-  lv.beg = 0; lv.info = 0; lv.eslot = INT_MAX; lv.acc = 0.f;
+  lv.beg = 0; lv.qbase = 0; lv.info = 0; lv.eslot = INT_MAX; lv.acc = 0.f;
   nslots = 0;
   if (kTable) {
     const int4* table = reinterpret_cast<const int4*>(m.chain) + lane;
@@ -511,6 +521,7 @@ __device__ __forceinline__ Row warp_row(const DevModel& m, const int32_t* state_
     lv.info = ((inc - ((nq + 31) >> 5)) << 16) | nq;
   }
   if (lane >= 1 && lane <= r.nlev) lv.eslot = (lv.info >> 16) + (((lv.info & 0xffff) + 31) >> 5);
+  lv.qbase = lv.beg >> 2;
   nslots = r.nlev > 0 ? __shfl_sync(kFull, lv.eslot, 1) : 0;
   return r;
 }
@@ -534,11 +545,13 @@ struct Window {
 // past the row's last one repeats the last slot (of the highest order, which
 // is written last anyway): rewriting an arc of the same level stores the
 // value already there.
-template <int kW, bool kPacked>
-__device__ __forceinline__ void load_window(const DevModel& m, const WLevel& lv, int32_t nlev, int32_t k0,
-                                            int32_t nslots, Window<kW, kPacked>& a) {
+// kSmem: the quads come from the row's staging area (bulk-copied there),
+// else from the global arrays.
+template <int kW, bool kPacked, bool kSmem = false>
+__device__ __forceinline__ void load_window(const DevModel& m, const WSlice& s, const WLevel& lv, int32_t nlev,
+                                            int32_t k0, int32_t nslots, Window<kW, kPacked>& a) {
   const int lane = threadIdx.x & 31;
-  const int4* tok4 = kPacked ? reinterpret_cast<const int4*>(m.arc_pk) : reinterpret_cast<const int4*>(m.arc_tok);
+  const int4* tok4 = reinterpret_cast<const int4*>(m.arc_tok);
   const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
   const int4* to4 = reinterpret_cast<const int4*>(m.arc_to);
 #pragma unroll
@@ -551,16 +564,31 @@ __device__ __forceinline__ void load_window(const DevModel& m, const WLevel& lv,
       // levels entirely before slot k (in slot order) are the levels after its own
       const int32_t L = nlev - 1 - __popc(__ballot_sync(kFull, lv.eslot <= k));
       const int src = L + 1;
-      const int32_t info = __shfl_sync(kFull, lv.info, src), b = __shfl_sync(kFull, lv.beg, src);
+      const int32_t info = __shfl_sync(kFull, lv.info, src), qb = __shfl_sync(kFull, lv.qbase, src);
       a.acc[u] = __shfl_sync(kFull, lv.acc, src);
       const int32_t i = (k - (info >> 16)) * 32 + lane;
-      qv[u - g] = (b >> 2) + (i < (info & 0xffff) ? i : 0);
+      qv[u - g] = qb + (i < (info & 0xffff) ? i : 0);
     }
 #pragma unroll
     for (int u = g; u < g + 8; ++u) {
-      a.tok[u] = __ldg(tok4 + qv[u - g]);
-      a.w[u] = __ldg(w4 + qv[u - g]);
-      if (!kPacked) a.to[u] = __ldg(to4 + qv[u - g]);
+      if (kSmem) {  // two 16-byte shared loads of the staged quad
+        a.tok[u] = s.st_q[2 * qv[u - g]];
+        const int4 x = s.st_q[2 * qv[u - g] + 1];
+        a.w[u] = make_float4(__int_as_float(x.x), __int_as_float(x.y), __int_as_float(x.z), __int_as_float(x.w));
+      } else if (kPacked) {  // one 32-byte load: 4 packed arcs + 4 weights
+        const uint4* p = reinterpret_cast<const uint4*>(m.arc_q) + 2 * (size_t)qv[u - g];
+        int4 t;
+        float4 x;
+        asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w), "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                     : "l"(p));
+        a.tok[u] = t;
+        a.w[u] = x;
+      } else {
+        a.tok[u] = __ldg(tok4 + qv[u - g]);
+        a.w[u] = __ldg(w4 + qv[u - g]);
+        a.to[u] = __ldg(to4 + qv[u - g]);
+      }
     }
   }
 }
@@ -628,7 +656,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-template <bool kTable, int kW, bool kPacked>
+// kRegRoot (V <= 1024): every lane keeps its 32 root weights in registers,
+// loaded before the wait, so the root fill is register -> shared stores that
+// overlap the arc gathers (shared-memory loads issued after the gathers would
+// return behind them).
+// kStage (packed arcs, register root): the row's arcs are bulk-copied level by
+// level into the warp's staging area (when they fit), so the gathers do not
+// queue in the SM's load pipeline; the write loop then reads shared memory.
+template <bool kTable, int kW, bool kPacked, bool kRegRoot, bool kStage>
 __global__ void __launch_bounds__(256)
     advance_warp_kernel(DevModel m, const int32_t* __restrict__ states, int32_t B, float* __restrict__ scores,
                         int32_t* __restrict__ next, float* __restrict__ final_out) {
@@ -638,7 +673,9 @@ __global__ void __launch_bounds__(256)
   const size_t rb = align16((size_t)V * 4);
   const float* root_w = reinterpret_cast<const float*>(smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + rb);
-  const WSlice s = wcarve(smem + rb + 16 + (size_t)w * wslice_bytes(V, m.order), V, m.order);
+  constexpr int kSQ = kStage ? kStageQuads : 0;
+  static_assert(!kStage || (kPacked && kRegRoot), "staging holds packed arcs");
+  const WSlice s = wcarve(smem + rb + 16 + (size_t)w * wslice_bytes(V, m.order, kSQ), V, m.order, kSQ);
   const int32_t row = (int32_t)blockIdx.x * R + w;
   const uint32_t bytes = (uint32_t)V * 4u;
   STAMP(0);
@@ -650,16 +687,24 @@ __global__ void __launch_bounds__(256)
   // slots (the root has an arc for every token, [0, V)).
   if (lane == 0 && row < B) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(s.bar)) : "memory");
-    if (w == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    if (kStage) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(s.abar)) : "memory");
+    if (w == 0 && !kRegRoot) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)), "r"(bytes) : "memory");
     bulk_g2s(s.row_n, m.arc_to, bytes, s.bar);
-    if (w == 0) {
+    if (w == 0 && !kRegRoot) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
       bulk_g2s(const_cast<float*>(root_w), m.arc_w, bytes, bar);
     }
   }
-  __syncthreads();  // the CTA barrier's init visible to every warp
+  float4 rw[kRegRoot ? 8 : 1];
+  if (kRegRoot && row < B) {
+    const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (lane + 32 * j < V / 4) rw[j] = __ldg(w4 + lane + 32 * j);
+  }
+  if (!kRegRoot) __syncthreads();  // the CTA barrier's init visible to every warp
   pdl_wait();
   STAMP(2);
   if (row >= B) return;  // warp 0 always has a row and waits for the CTA's bulk copy
@@ -681,26 +726,79 @@ __global__ void __launch_bounds__(256)
   if (r.bad) {
     for (int32_t v = lane; v < V; v += 32) { srow[v] = __int_as_float(0x7fc00000); nrow[v] = -1; }
     mbar_wait(s.bar, 0);  // no exit with a bulk copy in flight
-    if (w == 0) mbar_wait(bar, 0);
+    if (w == 0 && !kRegRoot) mbar_wait(bar, 0);
     return;
   }
-  mbar_wait(bar, 0);  // the CTA's root weights have landed (long ago, normally)
   STAMP(3);
   Window<kW, kPacked> a;
-  // the root fill goes first: its shared-memory loads would otherwise return
-  // behind the arc gathers
-  if (!(skip & 8)) root_fill(s, root_w, r.acc_root, V);
-  STAMP(12);
-  if (skip & 4) nslots = 0;
-  if (!(skip & 4)) load_window<kW, kPacked>(m, lv, r.nlev, 0, nslots, a);
+  bool staged = false;
+  if (kStage) {
+    // staging offsets: levels in slot order (the last level first), packed tight
+    const int32_t nq = lv.info & 0xffff;
+    int32_t inc = nq;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_down_sync(kFull, inc, o);
+      if (lane + o < 32) inc += y;
+    }
+    const int32_t total = __shfl_sync(kFull, inc, 0);
+    staged = total <= kSQ && !(skip & 4);
+    if (staged) {
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.abar)),
+                     "r"((uint32_t)total * 32u)
+                     : "memory");
+      __syncwarp();
+      const int32_t off = inc - nq;
+      if (nq > 0)  // lanes 1..nlev: one bulk copy per level
+        bulk_g2s(s.st_q + 2 * off, reinterpret_cast<const uint4*>(m.arc_q) + 2 * (lv.beg >> 2), (uint32_t)nq * 32u,
+                 s.abar);
+      lv.qbase = off;
+    }
+  }
+  if (kRegRoot) {
+    if (skip & 4) nslots = 0;
+    if (!staged && !(skip & 4)) load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
+    STAMP(12);
+    if (!(skip & 8)) {  // root scores: acc_root + root weight, while the gathers fly
+      float4* s4 = reinterpret_cast<float4*>(s.row_s);
+      const float ar = r.acc_root;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (lane + 32 * j < V / 4) {
+          float4 y = rw[j];
+          y.x = __fadd_rn(ar, y.x);
+          y.y = __fadd_rn(ar, y.y);
+          y.z = __fadd_rn(ar, y.z);
+          y.w = __fadd_rn(ar, y.w);
+          s4[lane + 32 * j] = y;
+        }
+    }
+  } else {
+    mbar_wait(bar, 0);  // the CTA's root weights have landed (long ago, normally)
+    // the root fill goes first: its shared-memory loads would otherwise return
+    // behind the arc gathers
+    if (!(skip & 8)) root_fill(s, root_w, r.acc_root, V);
+    STAMP(12);
+    if (skip & 4) nslots = 0;
+    if (!(skip & 4)) load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
+  }
   STAMP(4);
   mbar_wait(s.bar, 0);  // root targets in row_n
   __syncwarp();
   STAMP(5);
-  for (int32_t k0 = 0; k0 < nslots;) {
-    write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
-    k0 += kW;
-    if (k0 < nslots) load_window<kW, kPacked>(m, lv, r.nlev, k0, nslots, a);
+  if (staged) {
+    mbar_wait(s.abar, 0);  // the row's arcs are in the staging area
+    for (int32_t k0 = 0; k0 < nslots; k0 += kW) {
+      load_window<kW, kPacked, true>(m, s, lv, r.nlev, k0, nslots, a);
+      write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
+    }
+  } else {
+    for (int32_t k0 = 0; k0 < nslots;) {
+      write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
+      k0 += kW;
+      if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
+    }
   }
   STAMP(6);
   // step 4: the row leaves by two bulk stores issued by lane 0
@@ -912,17 +1010,26 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
   const bool table = m.chain != nullptr;
   cudaStream_t st = (cudaStream_t)stream;
   if (vec && m.adv_kind != NGPULM_ADVANCE_CTA) {
+    // up to 8 rows per SM: 16-slot windows (almost every row in one window),
+    // packed arcs bulk-copied into a staging area; more rows per SM: 8-slot
+    // windows of direct gathers (registers and shared memory for occupancy)
+    const bool wide = B <= 8 * 148, pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO;
+    const bool small_v = m.V <= 1024, stage = B >= 2 && B <= NGPULM_STAGE_MAX_B && pk && small_v && table;
+    const int sq = stage ? kStageQuads : 0;
     int R = (B + 147) / 148;
     R = R < 1 ? 1 : (R > 8 ? 8 : R);
-    while (R > 1 && wcta_smem(m.V, m.order, R) > 227 * 1024) --R;
-    if (wcta_smem(m.V, m.order, R) <= 227 * 1024) {
-      const size_t wsm = wcta_smem(m.V, m.order, R);
+    while (R > 1 && wcta_smem(m.V, m.order, R, sq) > 227 * 1024) --R;
+    if (wcta_smem(m.V, m.order, R, sq) <= 227 * 1024) {
+      const size_t wsm = wcta_smem(m.V, m.order, R, sq);
       const dim3 wg((B + R - 1) / R), wb(32 * R);
-      // up to 8 rows per SM: 16-slot windows (almost every row in one window);
-      // more rows per SM: 8-slot windows (registers for occupancy)
-      const bool wide = B <= 8 * 148, pk = m.arc_pk != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO;
-#define NGPULM_WARP_LAUNCH(T, W, P) \
-  return launch(advance_warp_kernel<T, W, P>, wg, wb, wsm, st, m, states, B, scores, next, final_out)
+      if (stage)
+        return launch(advance_warp_kernel<true, 16, true, true, true>, wg, wb, wsm, st, m, states, B, scores, next,
+                      final_out);
+#define NGPULM_WARP_LAUNCH(T, W, P)                                                                               \
+  return small_v ? launch(advance_warp_kernel<T, W, P, true, false>, wg, wb, wsm, st, m, states, B, scores, next, \
+                          final_out)                                                                                \
+                 : launch(advance_warp_kernel<T, W, P, false, false>, wg, wb, wsm, st, m, states, B, scores, next,  \
+                          final_out)
       if (table) {
         if (wide) { if (pk) NGPULM_WARP_LAUNCH(true, 16, true); NGPULM_WARP_LAUNCH(true, 16, false); }
         if (pk) NGPULM_WARP_LAUNCH(true, 8, true);

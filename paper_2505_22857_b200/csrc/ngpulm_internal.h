@@ -72,7 +72,9 @@ struct DevModel {
   const void* chain;  // chain table (int4 records) or nullptr = walk the chain at query time
   int32_t chain_slots;
   int32_t S, V, order;
-  const uint32_t* arc_pk;       // packed arcs (target << pk_bits) | token, or nullptr (targets too large)
+  // packed arc quads, or nullptr (targets too large): 32-byte units, one per
+  // 4 arcs of the device layout: {u32 (target << pk_bits) | token [4], f32 weight [4]}
+  const void* arc_q;
   int32_t pk_bits;
   int32_t adv_kind;             // NGPULM_ADVANCE_*
   unsigned long long* bad_row;  // sticky min bad row (ULLONG_MAX = none)
