@@ -474,9 +474,15 @@ struct WLevel {  // lane l+1: level l of the row
 };
 
 // The row's state, header and levels (Algorithm 1 lines 67-82).
-template <bool kTable>
+struct NoOp {
+  __device__ void operator()() const {}
+};
+
+// after_issue() runs once the chain-record load is in flight (table mode) or
+// before the walk: independent loads issued there overlap its latency.
+template <bool kTable, typename F = NoOp>
 __device__ __forceinline__ Row warp_row(const DevModel& m, const int32_t* state_ptr, const WSlice& s, WLevel& lv,
-                                        int32_t& nslots) {
+                                        int32_t& nslots, F after_issue = F()) {
   const int lane = threadIdx.x & 31;
   Row r;
   lv.beg = 0; lv.qbase = 0; lv.info = 0; lv.eslot = INT_MAX; lv.acc = 0.f;
@@ -493,6 +499,7 @@ __device__ __forceinline__ Row warp_row(const DevModel& m, const int32_t* state_
     if (r.bad) return r;
     int4 x = make_int4(0, 0, 0, 0);
     if (lane < slots) x = __ldg(table + (size_t)st * slots);
+    after_issue();
     r.nlev = __shfl_sync(kFull, x.x, 0);
     r.acc_root = __int_as_float(__shfl_sync(kFull, x.y, 0));
     r.fin = __int_as_float(__shfl_sync(kFull, x.z, 0));
@@ -503,6 +510,7 @@ __device__ __forceinline__ Row warp_row(const DevModel& m, const int32_t* state_
       lv.info = x.w;
     }
   } else {
+    after_issue();
     r = load_levels<false>(m, state_ptr, s.beg, s.pre, s.acc);
     if (r.bad) return r;
     __syncwarp();
@@ -664,7 +672,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // level into the warp's staging area (when they fit), so the gathers do not
 // queue in the SM's load pipeline; the write loop then reads shared memory.
 template <bool kTable, int kW, bool kPacked, bool kRegRoot, bool kStage>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 1)
     advance_warp_kernel(DevModel m, const int32_t* __restrict__ states, int32_t B, float* __restrict__ scores,
                         int32_t* __restrict__ next, float* __restrict__ final_out) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -948,6 +956,202 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   }
 }
 
+// ---------------------------------------------------------------- fused greedy step, one warp per row
+// The LM row is built in shared memory exactly as advance_warp_kernel builds
+// it (root targets by bulk copy, root scores from registers, quad gathers in
+// 8-slot windows, level-ordered writes) and never leaves the SM. The row's
+// logits (V+1 columns) are bulk-copied into shared memory as soon as the wait
+// allows — off the load pipeline, so they do not delay the state, record and
+// arc loads queued behind them — except the <= 3 columns on each side of the
+// copy's 16-byte-aligned interior, which two lanes load directly. The fused
+// values are reduced with warp shuffles.
+__device__ __forceinline__ void warp_argmax(float& v, int32_t& c) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float v2 = __shfl_xor_sync(kFull, v, o);
+    const int32_t c2 = __shfl_xor_sync(kFull, c, o);
+    if (better(v2, c2, v, c)) { v = v2; c = c2; }
+  }
+}
+
+constexpr int kMaxColsPerLane = 33;  // (1024 + 1 + 31) / 32
+
+// per warp: row_s | row_n | levels | 2 mbarriers | logits (V+1 floats + 16-byte slack)
+__host__ __device__ constexpr size_t fslice_bytes(int32_t V, int32_t order) {
+  return wslice_bytes(V, order, 0) + align16((size_t)(V + 1) * 4 + 16);
+}
+
+struct LogitsRow {  // where column c of the row sits in shared memory: buf[h + c]
+  const float* buf;
+  int32_t h, head, tail;  // head/tail: columns [0, head) and [tail, ncols) not in the bulk copy
+};
+
+__device__ __forceinline__ LogitsRow start_logits(const float* lrow, int32_t ncols, float* buf, uint64_t* lbar) {
+  const uintptr_t src = reinterpret_cast<uintptr_t>(lrow);
+  const uintptr_t lo = (src + 15) & ~(uintptr_t)15, hi = (src + (uintptr_t)ncols * 4) & ~(uintptr_t)15;
+  LogitsRow L;
+  L.buf = buf;
+  L.h = (int32_t)((src & 15) / 4);
+  const bool bulk = hi > lo;
+  L.head = bulk ? (int32_t)((lo - src) / 4) : ncols;
+  L.tail = bulk ? (int32_t)((hi - src) / 4) : ncols;
+  if ((threadIdx.x & 31) == 0) {
+    const uint32_t bytes = bulk ? (uint32_t)(hi - lo) : 0u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(lbar)), "r"(bytes) : "memory");
+    if (bulk) bulk_g2s(buf + L.h + L.head, reinterpret_cast<const void*>(lo), bytes, lbar);
+  }
+  return L;
+}
+
+// the columns outside the bulk copy: lanes 0..5 (<= 3 on each side)
+__device__ __forceinline__ void edge_logits(const float* lrow, int32_t ncols, const LogitsRow& L) {
+  const int lane = threadIdx.x & 31;
+  int32_t c = -1;
+  if (lane < L.head) c = lane;
+  else if (lane >= 8 && lane - 8 < ncols - L.tail) c = L.tail + lane - 8;
+  if (c >= 0) const_cast<float*>(L.buf)[L.h + c] = __ldg(&lrow[c]);
+}
+
+template <int kMode, bool kTable, bool kPacked>
+__global__ void __launch_bounds__(256, 1)
+    fused_warp_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int32_t B,
+                      int32_t* __restrict__ states, int32_t* __restrict__ prev, const uint8_t* __restrict__ active,
+                      float lambda, int32_t sp, int32_t* __restrict__ tokens_out) {
+  constexpr int kW = 8;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int32_t V = m.V, ncols = V + 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, R = blockDim.x >> 5;
+  unsigned char* base = smem + (size_t)w * fslice_bytes(V, m.order);
+  const WSlice s = wcarve(base, V, m.order, 0);
+  uint64_t* lbar = s.abar;
+  float* lbuf = reinterpret_cast<float*>(base + wslice_bytes(V, m.order, 0));
+  const int32_t row = (int32_t)blockIdx.x * R + w;
+  STAMP(0);
+  STAMP(1);
+  STAMP(9);
+  pdl_trigger();
+  if (row >= B) return;
+  if (lane == 0) {  // root targets -> the row's next-state slots (immutable model data: before the wait)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(s.bar)) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(lbar)) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)), "r"((uint32_t)V * 4u)
+                 : "memory");
+    bulk_g2s(s.row_n, m.arc_to, (uint32_t)V * 4u, s.bar);
+  }
+  float4 rw[8];
+  {
+    const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (lane + 32 * j < V / 4) rw[j] = __ldg(w4 + lane + 32 * j);
+  }
+  pdl_wait();
+  STAMP(2);
+  const float* lrow = logits + (size_t)row * row_stride;
+  const bool on = !active || __ldg(&active[row]);  // used only after the state and record loads are issued
+  const int32_t pc = (kMode == NGPULM_CTC) ? __ldg(&prev[row]) : -2;
+  WLevel lv;
+  int32_t nslots;
+  LogitsRow L{lbuf, 0, 0, 0};
+  bool started = false;
+  auto begin_logits = [&]() {  // the logits' bulk copy, issued once the chain record is in flight
+    L = start_logits(lrow, ncols, lbuf, lbar);
+    started = true;
+  };
+  const Row r = warp_row<kTable>(m, states + row, s, lv, nslots, begin_logits);
+  STAMP(11);
+  if (!on || r.bad) {  // inactive rows are untouched (their state is not even checked)
+    if (lane == 0) {
+      tokens_out[row] = -1;
+      if (on) atomicMin(m.bad_row, (unsigned long long)row);
+    }
+    mbar_wait(s.bar, 0);  // no exit with a bulk copy in flight
+    if (started) mbar_wait(lbar, 0);
+    return;
+  }
+  // (RNN-T: the LM row is built before stage 1 is known — it waits for the
+  // logits — and is simply not used when blank wins)
+  Window<kW, kPacked> a;
+  load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
+  edge_logits(lrow, ncols, L);  // queued behind the gathers, needed last
+  STAMP(3);
+  {  // root scores: acc_root + root weight, while the gathers fly
+    float4* s4 = reinterpret_cast<float4*>(s.row_s);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (lane + 32 * j < V / 4) {
+        float4 y = rw[j];
+        y.x = __fadd_rn(r.acc_root, y.x);
+        y.y = __fadd_rn(r.acc_root, y.y);
+        y.z = __fadd_rn(r.acc_root, y.z);
+        y.w = __fadd_rn(r.acc_root, y.w);
+        s4[lane + 32 * j] = y;
+      }
+  }
+  STAMP(4);
+  mbar_wait(s.bar, 0);
+  __syncwarp();
+  STAMP(5);
+  for (int32_t k0 = 0; k0 < nslots;) {
+    write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
+    k0 += kW;
+    if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
+  }
+  STAMP(6);
+  mbar_wait(lbar, 0);
+  __syncwarp();
+  STAMP(12);
+  // fused values and the row's argmax (R13, R14, R19):
+  // lane i takes columns i, i+32, ... (at most 33 at V <= 1024), all loads
+  // first. Within a lane the columns ascend, so a strict > keeps the lowest
+  // column on ties; the bc == INT_MAX clause takes a first -inf (R14), and a
+  // NaN is never taken (as in better()).
+  float bv = -INFINITY, rv = -INFINITY;
+  int32_t bc = INT_MAX, rc = INT_MAX;
+  {
+    float xs[kMaxColsPerLane], lm[kMaxColsPerLane];
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j) {
+      const int32_t col = lane + 32 * j;
+      xs[j] = col < ncols ? L.buf[L.h + col] : __int_as_float(0x7fc00000);  // NaN: never taken
+      lm[j] = col < ncols ? s.row_s[col - (col > sp)] : 0.f;                   // col == sp: unused
+    }
+    const float sp_val = (kMode == NGPULM_AED) ? r.fin : 0.f;  // eos <-> final (lambda * final + asr)
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j) {
+      const int32_t col = lane + 32 * j;
+      const float x = xs[j];
+      if (kMode == NGPULM_RNNT && (x > rv || (rc == INT_MAX && x == rv))) { rv = x; rc = col; }  // stage 1
+      float val = __fmaf_rn(lambda, col == sp ? sp_val : lm[j], x);  // asr + lambda * lm, one rounding
+      if (kMode == NGPULM_CTC && (col == sp || col == pc)) val = x;  // blank raw, repeated token not rescored
+      if (kMode == NGPULM_RNNT && col == sp) val = __int_as_float(0x7fc00000);  // stage 2: non-blank only
+      if (val > bv || (bc == INT_MAX && val == bv)) { bv = val; bc = col; }
+    }
+  }
+  warp_argmax(bv, bc);
+  if (kMode == NGPULM_RNNT) {
+    warp_argmax(rv, rc);
+    if (rc == sp) bc = sp;  // stage 1 keeps blank: no LM advance
+  }
+  STAMP(7);
+  if (lane == 0) {
+    if (bc < 0 || bc >= ncols) {
+      tokens_out[row] = -1;  // all-NaN row (unspecified)
+    } else {
+      tokens_out[row] = bc;
+      if (bc == sp) {
+        if (kMode == NGPULM_CTC) prev[row] = -1;
+      } else if (!(kMode == NGPULM_CTC && bc == pc)) {  // a repeated CTC token: no LM advance
+        states[row] = s.row_n[bc < sp ? bc : bc - 1];
+        if (kMode == NGPULM_CTC) prev[row] = bc;
+      }
+    }
+  }
+  STAMP(8);
+  if (w == 0) STAMPS_OUT(row);
+}
+
 // ---------------------------------------------------------------- launch
 template <typename... KArgs, typename... Args>
 int launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
@@ -1057,6 +1261,20 @@ template <int kMode>
 int launch_fused_mode(const DevModel& m, const float* logits, int64_t row_stride, int32_t B, int32_t* states,
                       int32_t* prev, const uint8_t* active, float lambda, int32_t blank, int32_t* tokens_out,
                       cudaStream_t st) {
+  if (m.V % 4 == 0 && m.V <= 1024 && m.adv_kind != NGPULM_ADVANCE_CTA) {
+    int R = (B + 147) / 148;
+    R = R < 1 ? 1 : (R > 8 ? 8 : R);
+    const size_t wsm = (size_t)R * fslice_bytes(m.V, m.order);
+    const dim3 wg((B + R - 1) / R), wb(32 * R);
+    const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
+#define NGPULM_FUSED_LAUNCH(T, P)                                                                              \
+  return launch(fused_warp_kernel<kMode, T, P>, wg, wb, wsm, st, m, logits, row_stride, B, states, prev, active, \
+                lambda, blank, tokens_out)
+    if (table) { if (pk) NGPULM_FUSED_LAUNCH(true, true); NGPULM_FUSED_LAUNCH(true, false); }
+    if (pk) NGPULM_FUSED_LAUNCH(false, true);
+    NGPULM_FUSED_LAUNCH(false, false);
+#undef NGPULM_FUSED_LAUNCH
+  }
   const size_t sm = row_smem(m.V, m.order);
   const dim3 gd(B), bd(kThreads);
   if (m.chain != nullptr)

@@ -231,13 +231,15 @@ def gpu_step(m, mode, logits_np, states, prev=None, active=None, lam=0.3, blank=
     return tok.cpu().numpy(), st.cpu().numpy(), (pv.cpu().numpy() if pv is not None else None)
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("chain", [ng.CHAIN_TABLE, ng.CHAIN_WALK])
 @pytest.mark.parametrize("mode", [CTC, RNNT, AED])
 @pytest.mark.parametrize("lam", [0.0, 0.3, 3.0])
 @pytest.mark.parametrize("name", ["tiny3", "five48", "ten24"])
-def test_fused_step_matches_oracle(pairs, mode, lam, name, chain):
+def test_fused_step_matches_oracle(pairs, mode, lam, name, chain, kernel):
     m, o, _ = pairs[name]
     m.set_chain_mode(chain)
+    m.set_advance_kernel(kernel)
     rng = np.random.default_rng(17)
     B = 300
     x = synth.rnnt_logits(B, 1, o.V, seed=9)[0]
@@ -250,6 +252,7 @@ def test_fused_step_matches_oracle(pairs, mode, lam, name, chain):
         tg, sg, pg = gpu_step(m, mode, x, states, prev if mode == CTC else None, active, lam)
     finally:
         m.set_chain_mode(ng.CHAIN_TABLE)
+        m.set_advance_kernel(ng.ADVANCE_AUTO)
     to, so, po = o.fused_step(mode, x, states, prev=prev if mode == CTC else None, active=active, lam=lam)
     assert np.array_equal(tg, to) and np.array_equal(sg, so)
     if mode == CTC:
