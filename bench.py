@@ -402,6 +402,18 @@ def bench_fused(m, f, dev, stream, rank):
     out["ctc_b256_t500_us_per_frame"] = ms * 1e3 / T
     out["ctc_b256_t500_ms_per_utterance_batch"] = ms
 
+    # the same utterance batch in ONE persistent launch
+    fr2 = torch.empty((Bc, T), dtype=torch.int32, device=dev)
+    em2 = torch.empty((Bc, T), dtype=torch.int32, device=dev)
+    el2 = torch.empty(Bc, dtype=torch.int32, device=dev)
+
+    def ctc_persistent():
+        m.ctc_greedy_decode(x, st, pv, lam=0.3, frames_out=fr2, emit_out=em2, emit_len=el2, stream=stream)
+    ms_p = _graph_time(ctc_persistent, stream, dev, reps=5, reset=lambda: (st.zero_(), pv.fill_(-1)))
+    out["ctc_b256_t500_persistent_us_per_frame"] = ms_p * 1e3 / T
+    out["ctc_b256_t500_persistent_ms_per_utterance_batch"] = ms_p
+    out["ctc_b256_t500_logits_gbs_persistent"] = x.numel() * 4 / (ms_p * 1e-3) / 1e9
+
     def plain_all():  # plain greedy CTC frame step (argmax only, no LM): torch library op
         for t in range(T):
             frames[t].copy_(torch.argmax(x[:, t], dim=1))

@@ -170,6 +170,36 @@ int ngpulm_fused_greedy_step(const ngpulm_model* model, int32_t mode, const floa
                              const uint8_t* active, float lambda, int32_t blank_id,
                              int32_t* tokens_out, ngpulm_stream stream);
 
+/* Whole-utterance greedy CTC decoding with shallow fusion in ONE launch
+ * (the CTC rule of PAPER.md:138-139). The result is
+ * identical to T calls of ngpulm_fused_greedy_step(NGPULM_CTC) for
+ * t = 0..T-1 with active[b] = (t < lengths[b]): the LM row of a state is
+ * computed on chip only when an emission changes the state and is reused
+ * across the frames in between.
+ *   logits:     dev float32; frame t of row b starts at
+ *               logits + b*row_stride + t*frame_stride and has V+1 columns
+ *               (column layout as for the fused step, R19). A [B,T,V+1]
+ *               contiguous tensor has row_stride = T*(V+1), frame_stride = V+1.
+ *   lengths:    dev [B] int32 (frames of each row, clamped to [0,T]) or NULL (= T).
+ *   states:     dev [B] int32 in/out: LM state before frame 0 / after the last frame.
+ *   prev:       dev [B] int32 in/out: column selected at the frame before
+ *               frame 0 (-1 = none), and at the row's last frame (R17).
+ *   frames_out: dev [B,T] int32 (row stride T) or NULL: the column selected at
+ *               each frame, -1 at t >= lengths[b] (and for invalid states).
+ *   emit_out:   dev [B,T] int32 (row stride T) or NULL: the emitted columns of
+ *               row b (selections that are neither blank nor prev), in order,
+ *               in emit_out[b*T .. b*T + emit_len[b]).
+ *   emit_len:   dev [B] int32 or NULL: number of emissions of each row.
+ * Needs V % 4 == 0, V <= 1024 and a finite lambda (EUSAGE otherwise); row_stride/frame_stride
+ * must be multiples of 1 float (any alignment). Asynchronous, no allocation,
+ * CUDA-graph capturable. An invalid start state sets the bad-row word and the
+ * row decides nothing (frames -1, no emissions, state and prev unchanged). */
+int ngpulm_ctc_greedy_decode(const ngpulm_model* model, const float* logits, int64_t row_stride,
+                             int64_t frame_stride, int32_t B, int32_t T, const int32_t* lengths,
+                             int32_t* states, int32_t* prev, float lambda, int32_t blank_id,
+                             int32_t* frames_out, int32_t* emit_out, int32_t* emit_len,
+                             ngpulm_stream stream);
+
 /* Synchronizes `stream`, reads and clears the sticky bad-row word:
  * *first_bad_row = smallest row index that carried an invalid state since the
  * last check, or -1. */

@@ -55,6 +55,8 @@ def lib():
         L.oracle_finals.argtypes = [P, i32p, C.c_int64, f32p, P]
         L.oracle_fused_step.argtypes = [P, C.c_int, f32p, C.c_int64, C.c_int64, i32p, P, P,
                                         C.c_float, C.c_int32, i32p, C.c_int]
+        L.oracle_ctc_decode.argtypes = [P, f32p, C.c_int64, C.c_int64, C.c_int64, C.c_int32, P, i32p, i32p,
+                                        C.c_float, C.c_int32, i32p, i32p, i32p, C.c_int]
         _lib = L
     return _lib
 
@@ -128,3 +130,21 @@ class Oracle:
         lib().oracle_fused_step(self.h, mode, x, x.shape[1], n, st, _ptr(pv), _ptr(act),
                                 float(lam), int(blank), tok, nthreads)
         return tok, st, pv
+
+    def ctc_decode(self, logits, states, prev=None, lam: float = 0.3, blank_id: int | None = None,
+                   lengths=None, nthreads: int = 0):
+        """Whole-utterance greedy CTC with fusion over logits [n, T, V+1].
+        Returns (frames [n,T], emitted [n,T], emit_len [n], states, prev)."""
+        x = np.ascontiguousarray(logits, dtype=np.float32)
+        n, T = x.shape[0], x.shape[1]
+        st = np.array(states, dtype=np.int32, copy=True).reshape(n)
+        pv = (np.full(n, -1, dtype=np.int32) if prev is None
+              else np.array(prev, dtype=np.int32, copy=True).reshape(n))
+        ln = None if lengths is None else np.ascontiguousarray(lengths, dtype=np.int32)
+        frames = np.empty((n, T), dtype=np.int32)
+        emitted = np.full((n, T), -1, dtype=np.int32)
+        elen = np.empty(n, dtype=np.int32)
+        blank = self.V if blank_id is None else blank_id
+        lib().oracle_ctc_decode(self.h, x, T * x.shape[2], x.shape[2], n, T, _ptr(ln), st, pv,
+                                float(lam), int(blank), frames, emitted, elen, nthreads)
+        return frames, emitted, elen, st, pv

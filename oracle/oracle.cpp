@@ -403,4 +403,31 @@ void oracle_fused_step(void* h, int mode, const float* logits, int64_t row_strid
   });
 }
 
+// Greedy CTC decoding of whole utterances (SPEC.md:307-316 ctc_greedy_fused;
+// PAPER.md:138-139): for t = 0..T-1, frame t of row i (logits + i*row_stride +
+// t*frame_stride) gets one fused CTC step while t < lengths[i] (NULL: T).
+// frames [n,T]: the column selected at each frame (-1 past the length);
+// emitted [n,T]: the selections that are neither blank nor prev, in order;
+// emit_len [n]. states / prev in/out.
+void oracle_ctc_decode(void* h, const float* logits, int64_t row_stride, int64_t frame_stride, int64_t n,
+                       int32_t T, const int32_t* lengths, int32_t* states, int32_t* prev, float lambda,
+                       int32_t blank_id, int32_t* frames, int32_t* emitted, int32_t* emit_len, int nthreads) {
+  auto* o = (Oracle*)h;
+  parallel_rows(n, nthreads, [&](int64_t i) {
+    const int32_t len = lengths ? std::min(T, std::max(0, lengths[i])) : T;
+    int32_t ne = 0;
+    for (int32_t t = 0; t < T; ++t) {
+      int32_t tok = -1;
+      if (t < len) {
+        const int32_t p0 = prev[i];
+        o->fused_step(0, logits + i * row_stride + (int64_t)t * frame_stride, blank_id, lambda, &states[i],
+                      &prev[i], &tok);
+        if (tok != blank_id && tok != p0) emitted[i * T + ne++] = tok;  // "blank ... and repeated tokens" collapse
+      }
+      frames[i * T + t] = tok;
+    }
+    emit_len[i] = ne;
+  });
+}
+
 }  // extern "C"

@@ -61,6 +61,8 @@ SIGNATURES = {
     "ngpulm_advance": (C.c_int, [_P, _P, _I32, _P, _P, _P, _P]),
     "ngpulm_final": (C.c_int, [_P, _P, _I32, _P, _P]),
     "ngpulm_fused_greedy_step": (C.c_int, [_P, _I32, _P, _I64, _I32, _P, _P, _P, _F, _I32, _P, _P]),
+    "ngpulm_ctc_greedy_decode": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _F, _I32, _P, _P, _P,
+                                            _P]),
     "ngpulm_check": (C.c_int, [_P, _P, C.POINTER(_I64)]),
     "ngpulm_advance_host": (C.c_int, [_P, _P, _I32, _P, _P, _P, _P]),
     "ngpulm_touched_bytes": (C.c_int, [_P, _P, _I32, C.POINTER(_I64)]),
@@ -234,6 +236,36 @@ class NgpuLM:
             float(lam), blank, _dev_ptr(tokens_out, torch.int32, "tokens_out", B), _stream(stream)))
         return tokens_out
 
+    def ctc_greedy_decode(self, logits, states, prev, lam: float = 0.3, blank_id: int | None = None,
+                          lengths=None, frames_out=None, emit_out=None, emit_len=None, want_frames=True,
+                          stream=None):
+        """ngpulm_ctc_greedy_decode over a [B, T, V+1] CUDA f32 tensor (any strides
+        with contiguous columns). states/prev [B] int32 are updated in place.
+        Returns (frames [B,T] or None, emitted [B,T], emit_len [B])."""
+        import torch
+        if logits.dtype != torch.float32 or not logits.is_cuda or logits.dim() != 3:
+            raise TypeError("logits: expected a [B, T, V+1] CUDA float32 tensor")
+        if logits.stride(2) != 1 or logits.shape[2] != self.V + 1:
+            raise ValueError("logits: need V+1 contiguous columns")
+        B, T = logits.shape[0], logits.shape[1]
+        dev = logits.device
+        if frames_out is None and want_frames:
+            frames_out = torch.empty((B, T), dtype=torch.int32, device=dev)
+        if emit_out is None:
+            emit_out = torch.empty((B, T), dtype=torch.int32, device=dev)
+        if emit_len is None:
+            emit_len = torch.empty(B, dtype=torch.int32, device=dev)
+        blank = self.V if blank_id is None else blank_id
+        _check(lib().ngpulm_ctc_greedy_decode(
+            self._h, logits.data_ptr(), logits.stride(0), logits.stride(1), B, T,
+            _dev_ptr(lengths, torch.int32, "lengths", B) if lengths is not None else None,
+            _dev_ptr(states, torch.int32, "states", B), _dev_ptr(prev, torch.int32, "prev", B),
+            float(lam), blank,
+            _dev_ptr(frames_out, torch.int32, "frames_out", B * T) if frames_out is not None else None,
+            _dev_ptr(emit_out, torch.int32, "emit_out", B * T),
+            _dev_ptr(emit_len, torch.int32, "emit_len", B), _stream(stream)))
+        return frames_out, emit_out, emit_len
+
     def check(self, stream=None) -> int:
         out = C.c_int64()
         _check(lib().ngpulm_check(self._h, _stream(stream), C.byref(out)))
@@ -268,6 +300,7 @@ ngpulm_advance = NgpuLM.advance
 ngpulm_final = NgpuLM.final
 ngpulm_fused_greedy_step = NgpuLM.fused_greedy_step
 ngpulm_check = NgpuLM.check
+ngpulm_ctc_greedy_decode = NgpuLM.ctc_greedy_decode
 ngpulm_replicate = NgpuLM.replicate
 ngpulm_set_chain_mode = NgpuLM.set_chain_mode
 ngpulm_set_advance_kernel = NgpuLM.set_advance_kernel

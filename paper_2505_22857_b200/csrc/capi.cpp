@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cmath>
 #include <algorithm>
 #include <cstring>
 #include <memory>
@@ -293,6 +294,25 @@ int ngpulm_fused_greedy_step(const ngpulm_model* m, int32_t mode, const float* l
   int e = ngpulm::launch_fused(m->dm, mode, logits, row_stride, B, states, prev, active, lambda, blank_id,
                                tokens_out, stream);
   if (e) return cuda_err((cudaError_t)e, "fused step launch");
+  return NGPULM_OK;
+}
+
+int ngpulm_ctc_greedy_decode(const ngpulm_model* m, const float* logits, int64_t row_stride, int64_t frame_stride,
+                             int32_t B, int32_t T, const int32_t* lengths, int32_t* states, int32_t* prev,
+                             float lambda, int32_t blank_id, int32_t* frames_out, int32_t* emit_out,
+                             int32_t* emit_len, ngpulm_stream stream) {
+  if (int r = check_hot(m, B)) return r;
+  if (T < 0) return err(NGPULM_EUSAGE, "T < 0");
+  if (blank_id < 0 || blank_id > m->h.V) return err(NGPULM_EUSAGE, "blank_id outside [0, V]");
+  if (m->h.V % 4 != 0 || m->h.V > 1024) return err(NGPULM_EUSAGE, "ctc decode needs V % 4 == 0 and V <= 1024");
+  if (!std::isfinite(lambda)) return err(NGPULM_EUSAGE, "lambda must be finite");
+  if (B == 0) return NGPULM_OK;
+  if (!states || !prev || (T > 0 && !logits)) return err(NGPULM_EUSAGE, "NULL device buffer");
+  if (T > 1 && frame_stride < (int64_t)m->h.V + 1 && row_stride < (int64_t)m->h.V + 1)
+    return err(NGPULM_EUSAGE, "frames overlap: frame_stride and row_stride < V+1");
+  int e = ngpulm::launch_ctc_decode(m->dm, logits, row_stride, frame_stride, B, T, lengths, states, prev, lambda,
+                                    blank_id, frames_out, emit_out, emit_len, stream);
+  if (e) return cuda_err((cudaError_t)e, "ctc decode launch");
   return NGPULM_OK;
 }
 

@@ -44,3 +44,31 @@ def small_lms(lm_dir):
 @pytest.fixture(scope="session")
 def fig1_paths():
     return os.path.join(GOLDEN, "fig1.arpa"), os.path.join(GOLDEN, "fig1.vocab")
+
+
+# ---------------------------------------------------------------- GPU fixtures (session: built once)
+GPU_SMALL = ["uni16", "bi16", "tiny3", "tri64", "five48", "ten24"]
+
+
+@pytest.fixture(scope="session")
+def pairs(small_lms, fig1_paths):
+    """(library model on cuda:0, oracle, files) for every small LM and Fig. 1."""
+    import paper_2505_22857_b200 as ng
+    from oracle import Oracle
+    out = {}
+    for n in GPU_SMALL:
+        f = small_lms[n]
+        out[n] = (ng.load_arpa(f.arpa, vocab_size=f.vocab_size, device=0), Oracle(f.arpa, vocab_size=f.vocab_size), f)
+    arpa, vocab = fig1_paths
+    out["fig1"] = (ng.load_arpa(arpa, vocab, device=0), Oracle(arpa, vocab), None)
+    return out
+
+
+@pytest.fixture(scope="session")
+def lm6(lm_dir):
+    """BASELINE configs[1]: token 6-gram, V=1024 BPE-like, ~1M n-grams."""
+    import paper_2505_22857_b200 as ng
+    import synth
+    from oracle import Oracle
+    f = synth.make_lm(lm_dir, 1024, 6, tokens=430000, seed=1, heldout=2000, tag="cfg1_6gram")
+    return ng.load_arpa(f.arpa, vocab_size=1024, device=0), Oracle(f.arpa, vocab_size=1024), f

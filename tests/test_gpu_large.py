@@ -1,0 +1,107 @@
+"""GPU parity at BASELINE.json's full LM sizes (configs[3] and configs[4]), in the
+launch configurations the bench and the decoders use, against the oracle on
+sampled rows plus properties that hold for every row:
+
+* configs[3]: token 8-gram LM (~4.9M n-grams, V=1024), RNN-T fused greedy steps
+  over B=512 rows (label-looping shape: per-step logits, state carried), and
+  advance at B=512;
+* configs[4]: token 10-gram LM (~20M n-grams, V=1024, ~1.9 GB resident with the
+  chain table), advance at B=4096, the B=4096 batch sharded 4 ways (the per-GPU
+  share at 4 GPUs) == unsharded, and a replica == the original.
+
+Bar: next-state ids and argmax tokens bit-exact, scores bit-exact against the
+oracle's Algorithm-1-order float32 value; per-row normalization
+sum_v exp(score) + exp(final) = 1 (Witten-Bell LMs are normalized).
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import RNNT, Oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+import paper_2505_22857_b200 as ng  # noqa: E402
+
+from test_gpu_parity import dev, gpu_advance, same_bits, trajectory_states, using  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def lm8(lm_dir):
+    f = synth.make_lm(lm_dir, 1024, 8, tokens=1_600_000, seed=5, heldout=2000, tag="cfg3_8gram")
+    return ng.load_arpa(f.arpa, vocab_size=1024, device=0), Oracle(f.arpa, vocab_size=1024), f
+
+
+@pytest.fixture(scope="module")
+def lm10(lm_dir):
+    f = synth.make_lm(lm_dir, 1024, 10, tokens=5_200_000, seed=7, heldout=2000, tag="cfg4_10gram")
+    return ng.load_arpa(f.arpa, vocab_size=1024, device=0), Oracle(f.arpa, vocab_size=1024), f
+
+
+def normalized(s, fin, tol=1e-4):
+    tot = np.exp(s.astype(np.float64)).sum(1) + np.exp(fin.astype(np.float64))
+    return np.max(np.abs(tot - 1)) < tol
+
+
+def test_config3_sizes(lm8):
+    m, o, f = lm8
+    n = sum(int(line.split("=")[1]) for line in open(f.arpa).read().split("\n\n")[0].splitlines()[1:])
+    assert 4_500_000 < n < 6_000_000 and m.order == 8
+
+
+@pytest.mark.parametrize("kernel", [ng.ADVANCE_AUTO, ng.ADVANCE_WARP, ng.ADVANCE_CTA])
+def test_config3_rnnt_fused_steps_b512(lm8, kernel):
+    """16 label-looping-shaped steps (B=512, per-step logits, state carried from
+    step to step, ~50 % blank rows), every row and step bit-exact vs the oracle."""
+    m, o, f = lm8
+    B, steps = 512, 16
+    states, _ = trajectory_states(m, f, B, seed=21)
+    xs = synth.rnnt_logits(B, steps, m.V, seed=22)
+    st_d = torch.from_numpy(states.copy()).to(dev())
+    so = states.copy()
+    with using(m, kernel=kernel):
+        for k in range(steps):
+            tok = m.fused_greedy_step(RNNT, torch.from_numpy(xs[k]).to(dev()), st_d, lam=0.3)
+            to, so, _ = o.fused_step(RNNT, xs[k], so, lam=0.3)
+            assert np.array_equal(tok.cpu().numpy(), to), f"step {k}: tokens differ"
+    assert np.array_equal(st_d.cpu().numpy(), so)
+
+
+def test_config3_advance_b512(lm8):
+    m, o, f = lm8
+    states, _ = trajectory_states(m, f, 512, seed=23)
+    s, n, fin = gpu_advance(m, states)
+    rows = np.random.default_rng(24).choice(512, 32, replace=False)
+    s32, s64, n_o, _ = o.rows(states[rows])
+    assert np.array_equal(n[rows], n_o) and same_bits(s[rows], s32)
+    assert np.max(np.abs(s[rows] - s64)) < 1e-5
+    assert normalized(s, fin)
+
+
+def test_config4_sizes(lm10):
+    m, o, f = lm10
+    n = sum(int(line.split("=")[1]) for line in open(f.arpa).read().split("\n\n")[0].splitlines()[1:])
+    assert 18_000_000 < n < 23_000_000 and m.order == 10
+
+
+def test_config4_advance_b4096_sharded_and_replica(lm10):
+    """configs[4]: B=4096 over a replicated 10-gram trie. One launch at B=4096, the
+    same rows as 4 shards of 1024 (each GPU's share at 4 GPUs) and on a replica:
+    bit-identical; sampled rows vs the oracle; normalization on every row."""
+    m, o, f = lm10
+    B = 4096
+    states, _ = trajectory_states(m, f, B, seed=31)
+    s, n, fin = gpu_advance(m, states)
+    rows = np.random.default_rng(32).choice(B, 32, replace=False)
+    s32, s64, n_o, _ = o.rows(states[rows])
+    assert np.array_equal(n[rows], n_o) and same_bits(s[rows], s32)
+    assert np.max(np.abs(s[rows] - s64)) < 2e-5   # f32 bound at 10 levels
+    assert normalized(s, fin)
+    parts = [gpu_advance(m, states[i:i + 1024]) for i in range(0, B, 1024)]
+    assert same_bits(np.concatenate([p[0] for p in parts]), s)
+    assert np.array_equal(np.concatenate([p[1] for p in parts]), n)
+    r = m.replicate(0)
+    s2, n2, f2 = gpu_advance(r, states)
+    assert same_bits(s2, s) and np.array_equal(n2, n) and same_bits(f2, fin)
+    assert m.check() == -1

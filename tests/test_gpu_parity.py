@@ -28,17 +28,6 @@ def same_bits(a, b):
     return np.array_equal(np.asarray(a, np.float32).view(np.int32), np.asarray(b, np.float32).view(np.int32))
 
 
-@pytest.fixture(scope="module")
-def pairs(small_lms, fig1_paths):
-    out = {}
-    for n in SMALL:
-        f = small_lms[n]
-        out[n] = (ng.load_arpa(f.arpa, vocab_size=f.vocab_size, device=0), Oracle(f.arpa, vocab_size=f.vocab_size), f)
-    arpa, vocab = fig1_paths
-    out["fig1"] = (ng.load_arpa(arpa, vocab, device=0), Oracle(arpa, vocab), None)
-    return out
-
-
 KERNELS = [ng.ADVANCE_AUTO, ng.ADVANCE_WARP, ng.ADVANCE_CTA]
 
 
@@ -122,13 +111,6 @@ def test_invalid_state_and_empty_batch(pairs):
     fin = m.final(torch.tensor([1, -7], dtype=torch.int32, device=dev()))
     torch.cuda.synchronize()
     assert np.isnan(fin[1].item()) and m.check() == 1
-
-
-@pytest.fixture(scope="module")
-def lm6(lm_dir):
-    """BASELINE configs[1]: token 6-gram, V=1024 BPE-like, ~1M n-grams."""
-    f = synth.make_lm(lm_dir, 1024, 6, tokens=430000, seed=1, heldout=2000, tag="cfg1_6gram")
-    return ng.load_arpa(f.arpa, vocab_size=1024, device=0), Oracle(f.arpa, vocab_size=1024), f
 
 
 def trajectory_states(m, f, n, seed):

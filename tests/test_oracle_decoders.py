@@ -150,3 +150,48 @@ def test_fusion_weight_tie_break_lowest_column(fig1):
     for mode in (RNNT, AED, CTC):
         tok, st, _ = fig1.fused_step(mode, row, np.array([0]), prev=np.array([-1]), lam=0.7)
         assert tok[0] == 1 and st[0] == 2
+
+
+def test_oracle_ctc_decode_lambda0_is_greedy_collapse_ragged(tri):
+    """Whole-utterance oracle decode at lambda = 0 with ragged lengths = numpy's
+    per-frame argmax collapsed (itertools.groupby, blanks dropped) on each row's prefix."""
+    o, f = tri
+    sents = synth.read_sentences(f.heldout)
+    B, T = 7, 37
+    x = synth.ctc_logits(sents, B=B, T=T, V=o.V, seed=8)
+    lengths = np.array([0, 1, 5, 37, 20, 36, 2], np.int32)
+    frames, emitted, elen, st, pv = o.ctc_decode(x, np.zeros(B, np.int32), lam=0.0, lengths=lengths)
+    for b in range(B):
+        path = np.argmax(x[b, : lengths[b]], axis=1)
+        collapsed = [int(k) for k, _ in itertools.groupby(path) if k != o.V]
+        assert list(emitted[b, : elen[b]]) == collapsed
+        assert (frames[b, : lengths[b]] == path).all() and (frames[b, lengths[b]:] == -1).all()
+        assert pv[b] == (-1 if lengths[b] == 0 or path[-1] == o.V else path[-1])
+
+
+def test_oracle_ctc_decode_is_the_frame_loop(tri):
+    """The whole-utterance decode equals T single fused steps with active = t < len."""
+    o, f = tri
+    sents = synth.read_sentences(f.heldout)
+    B, T = 6, 30
+    x = synth.ctc_logits(sents, B=B, T=T, V=o.V, seed=9)
+    lengths = np.array([30, 0, 7, 29, 15, 30], np.int32)
+    start = synth.uniform_states(o.num_states, B, seed=5)
+    prev0 = np.array([-1, 3, -1, 5, -1, -1], np.int32)
+    frames, emitted, elen, st, pv = o.ctc_decode(x, start, prev=prev0, lam=2.0, lengths=lengths)
+    s, p = start.copy(), prev0.copy()
+    for t in range(T):
+        act = (t < lengths).astype(np.uint8)
+        p_old = p.copy()
+        tok, s, p = o.fused_step(CTC, x[:, t], s, prev=p, active=act, lam=2.0)
+        assert (frames[:, t] == tok).all()
+    assert (st == s).all() and (pv == p).all()
+    # emissions: selections that are neither blank nor the previous selection
+    for b in range(B):
+        sel = list(frames[b, : lengths[b]])
+        em, last = [], prev0[b]
+        for c in sel:
+            if c != o.V and c != last:
+                em.append(c)
+            last = -1 if c == o.V else c
+        assert list(emitted[b, : elen[b]]) == em
