@@ -436,6 +436,21 @@ def bench_fused(m, f, dev, stream, rank):
 
         ms = _graph_time(loop, stream, dev, reps=5, reset=lambda: st.copy_(st0))
         out[f"{name}_b{Bt}_us_per_step"] = ms * 1e3 / nsteps
+        if mode == ng.RNNT:  # the same steps with the HAT internal-LM term (f3)
+            ilm = torch.randn((NB, Bt, V), device=dev) - 4.0
+
+            def loop_ilm():
+                for k in range(nsteps):
+                    m.fused_greedy_step_ilm(mode, xs[k % NB], st, ilm[k % NB], 0.2, lam=0.3, tokens_out=tok,
+                                            stream=stream)
+            ms = _graph_time(loop_ilm, stream, dev, reps=5, reset=lambda: st.copy_(st0))
+            out[f"{name}_ilm_b{Bt}_us_per_step"] = ms * 1e3 / nsteps
+        if mode == ng.AED:  # beam-search expansion: top-4 fused candidates per hypothesis row (f3)
+            def loop_topk():
+                for k in range(nsteps):
+                    m.fused_topk(xs[k % NB], st, 4, lam=0.3, stream=stream)
+            ms = _graph_time(loop_topk, stream, dev, reps=5, reset=lambda: None)
+            out[f"aed_topk4_b{Bt}_us_per_call"] = ms * 1e3 / nsteps
     return out
 
 

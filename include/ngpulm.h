@@ -46,6 +46,7 @@ typedef struct CUstream_st* ngpulm_stream; /* == cudaStream_t */
 enum { NGPULM_OK = 0, NGPULM_EDOMAIN = 1, NGPULM_EUSAGE = 2, NGPULM_ECUDA = 3, NGPULM_EIO = 4 };
 enum { NGPULM_CTC = 0, NGPULM_RNNT = 1, NGPULM_AED = 2 };
 enum { NGPULM_MAX_ORDER = 32 };
+enum { NGPULM_MAX_TOPK = 256 };
 enum { NGPULM_CHAIN_TABLE = 0, NGPULM_CHAIN_WALK = 1 };
 enum { NGPULM_ADVANCE_AUTO = 0, NGPULM_ADVANCE_WARP = 1, NGPULM_ADVANCE_CTA = 2 };
 
@@ -169,6 +170,41 @@ int ngpulm_fused_greedy_step(const ngpulm_model* model, int32_t mode, const floa
                              int64_t row_stride, int32_t B, int32_t* states, int32_t* prev,
                              const uint8_t* active, float lambda, int32_t blank_id,
                              int32_t* tokens_out, ngpulm_stream stream);
+
+/* ngpulm_fused_greedy_step with internal-LM subtraction ("-ILM+LM" for HAT
+ * transducers, Table 3; SPEC.md:298-306 fuse_scores): every
+ * LM-rescored column (CTC: not blank, not prev; RNN-T stage 2: non-blank;
+ * AED: token columns — the eos column takes no ILM term) gets
+ *     fmaf(-lambda_ilm, ilm[b*ilm_stride + v], fmaf(lambda, lm, asr))
+ * (two single roundings in this order, R21; lambda_ilm = 0 gives
+ * exactly the plain fused step's decisions). ilm: dev float32, row b at
+ * ilm + b*ilm_stride, indexed by LM token v in [0, V) (not by column). All
+ * other arguments and rules as ngpulm_fused_greedy_step. */
+int ngpulm_fused_greedy_step_ilm(const ngpulm_model* model, int32_t mode, const float* logits,
+                                 int64_t row_stride, int32_t B, int32_t* states, int32_t* prev,
+                                 const uint8_t* active, float lambda, int32_t blank_id, const float* ilm,
+                                 int64_t ilm_stride, float lambda_ilm, int32_t* tokens_out,
+                                 ngpulm_stream stream);
+
+/* The k best fused expansions of each row, for AED beam search with NGPU-LM
+ * shallow fusion. Fused value of a
+ * token column: fmaf(lambda, lm, asr) [then fmaf(-lambda_ilm, ilm[v], .) when
+ * ilm != NULL]; of the eos column `eos_id`: fmaf(lambda, final(state), asr).
+ *   logits:      dev float32, row b at logits + b*row_stride, V+1 columns (R19).
+ *   states:      dev [B] int32 (read only).
+ *   ilm:         dev float32 or NULL, row b at ilm + b*ilm_stride, V token entries.
+ *   topk_scores: dev [B,k] float32: the k largest fused values, descending
+ *                (ties: lower column first, R14; NaN never selected; slots
+ *                past the selectable columns: -inf with column -1).
+ *   topk_cols:   dev [B,k] int32: their columns.
+ *   topk_next:   dev [B,k] int32 or NULL: the LM state after each candidate
+ *                (the state itself for eos, -1 for an empty slot).
+ * 1 <= k <= NGPULM_MAX_TOPK; needs V % 4 == 0 and V <= 1024 (EUSAGE
+ * otherwise). Invalid states: NaN scores, columns -1, bad-row word set. */
+int ngpulm_fused_topk(const ngpulm_model* model, const float* logits, int64_t row_stride, int32_t B,
+                      const int32_t* states, const float* ilm, int64_t ilm_stride, float lambda,
+                      float lambda_ilm, int32_t eos_id, int32_t k, float* topk_scores,
+                      int32_t* topk_cols, int32_t* topk_next, ngpulm_stream stream);
 
 /* Whole-utterance greedy CTC decoding with shallow fusion in ONE launch
  * (the CTC rule of PAPER.md:138-139). The result is

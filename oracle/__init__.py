@@ -55,6 +55,10 @@ def lib():
         L.oracle_finals.argtypes = [P, i32p, C.c_int64, f32p, P]
         L.oracle_fused_step.argtypes = [P, C.c_int, f32p, C.c_int64, C.c_int64, i32p, P, P,
                                         C.c_float, C.c_int32, i32p, C.c_int]
+        L.oracle_fused_step_ilm.argtypes = [P, C.c_int, f32p, C.c_int64, C.c_int64, i32p, P, P, C.c_float,
+                                            C.c_int32, f32p, C.c_int64, C.c_float, i32p, C.c_int]
+        L.oracle_topk.argtypes = [P, f32p, C.c_int64, C.c_int64, i32p, P, C.c_int64, C.c_float, C.c_float,
+                                  C.c_int32, C.c_int32, f32p, i32p, i32p, C.c_int]
         L.oracle_ctc_decode.argtypes = [P, f32p, C.c_int64, C.c_int64, C.c_int64, C.c_int32, P, i32p, i32p,
                                         C.c_float, C.c_int32, i32p, i32p, i32p, C.c_int]
         _lib = L
@@ -148,3 +152,33 @@ class Oracle:
         lib().oracle_ctc_decode(self.h, x, T * x.shape[2], x.shape[2], n, T, _ptr(ln), st, pv,
                                 float(lam), int(blank), frames, emitted, elen, nthreads)
         return frames, emitted, elen, st, pv
+
+    def fused_step_ilm(self, mode: int, logits, states, ilm, lam_ilm: float, prev=None, active=None,
+                       lam: float = 0.3, blank_id: int | None = None, nthreads: int = 0):
+        """fused_step with the ILM term (R21). ilm [n, V]. Returns (tokens, states, prev)."""
+        x = np.ascontiguousarray(logits, dtype=np.float32)
+        a = np.ascontiguousarray(ilm, dtype=np.float32)
+        n = x.shape[0]
+        st = np.array(states, dtype=np.int32, copy=True)
+        pv = None if prev is None else np.array(prev, dtype=np.int32, copy=True)
+        act = None if active is None else np.ascontiguousarray(active, dtype=np.uint8)
+        tok = np.empty(n, dtype=np.int32)
+        blank = self.V if blank_id is None else blank_id
+        lib().oracle_fused_step_ilm(self.h, mode, x, x.shape[1], n, st, _ptr(pv), _ptr(act), float(lam),
+                                    int(blank), a, a.shape[1], float(lam_ilm), tok, nthreads)
+        return tok, st, pv
+
+    def topk(self, logits, states, k: int, lam: float = 0.3, eos_id: int | None = None, ilm=None,
+             lam_ilm: float = 0.0, nthreads: int = 0):
+        """k best AED expansions per row -> (scores [n,k], cols [n,k], next [n,k])."""
+        x = np.ascontiguousarray(logits, dtype=np.float32)
+        n = x.shape[0]
+        st = np.ascontiguousarray(states, dtype=np.int32)
+        a = None if ilm is None else np.ascontiguousarray(ilm, dtype=np.float32)
+        sc = np.empty((n, k), dtype=np.float32)
+        cols = np.empty((n, k), dtype=np.int32)
+        nx = np.empty((n, k), dtype=np.int32)
+        eos = self.V if eos_id is None else eos_id
+        lib().oracle_topk(self.h, x, x.shape[1], n, st, _ptr(a), 0 if a is None else a.shape[1], float(lam),
+                          float(lam_ilm), int(eos), int(k), sc, cols, nx, nthreads)
+        return sc, cols, nx

@@ -164,8 +164,16 @@ struct Oracle {
   // selection at t-1 (-1 = none).
   int32_t tok_of(int32_t col, int32_t sp) const { return col < sp ? col : col - 1; }
 
+  // [R21] internal-LM subtraction ("-ILM+LM"; SPEC.md:301
+  // fuse_scores: out = asr + lambda*lm - lambda_ilm*aux): on the LM-rescored
+  // columns, fmaf(-lambda_ilm, ilm[v], fmaf(lambda, lm[v], asr[c])).
+  float rescore(float lambda, float lmv, float asr, const float* ilm, float lam_ilm, int32_t v) const {
+    const float y = std::fmaf(lambda, lmv, asr);
+    return ilm ? std::fmaf(-lam_ilm, ilm[v], y) : y;
+  }
+
   void fused_step(int mode, const float* asr, int32_t sp, float lambda, int32_t* st,
-                  int32_t* prev, int32_t* token_out) const {
+                  int32_t* prev, int32_t* token_out, const float* ilm = nullptr, float lam_ilm = 0.f) const {
     const int32_t ncols = V + 1, s = *st;
     std::vector<float> lm(V);
     for (int32_t v = 0; v < V; ++v) lm[v] = score32(s, v);
@@ -183,7 +191,7 @@ struct Oracle {
       int32_t c1 = argmax(val, -1);
       if (c1 == sp) { *token_out = sp; return; }  // "If blank is predicted, we retain it"
       for (int32_t c = 0; c < ncols; ++c)
-        if (c != sp) val[c] = std::fmaf(lambda, lm[tok_of(c, sp)], asr[c]);
+        if (c != sp) val[c] = rescore(lambda, lm[tok_of(c, sp)], asr[c], ilm, lam_ilm, tok_of(c, sp));
       int32_t c2 = argmax(val, sp);  // "greedy selection among non-blank symbols"
       *token_out = c2;
       *st = next(s, tok_of(c2, sp));
@@ -192,7 +200,7 @@ struct Oracle {
     if (mode == 0) {  // CTC three groups
       const int32_t p = *prev;
       for (int32_t c = 0; c < ncols; ++c)
-        val[c] = (c == sp || c == p) ? asr[c] : std::fmaf(lambda, lm[tok_of(c, sp)], asr[c]);
+        val[c] = (c == sp || c == p) ? asr[c] : rescore(lambda, lm[tok_of(c, sp)], asr[c], ilm, lam_ilm, tok_of(c, sp));
       int32_t c = argmax(val, -1);
       *token_out = c;
       if (c == sp) { *prev = -1; return; }
@@ -204,10 +212,36 @@ struct Oracle {
     // AED: eos column scored with the final weight
     for (int32_t c = 0; c < ncols; ++c)
       val[c] = (c == sp) ? std::fmaf(lambda, final32(s), asr[c])
-                         : std::fmaf(lambda, lm[tok_of(c, sp)], asr[c]);
+                         : rescore(lambda, lm[tok_of(c, sp)], asr[c], ilm, lam_ilm, tok_of(c, sp));
     int32_t c = argmax(val, -1);
     *token_out = c;
     if (c != sp) *st = next(s, tok_of(c, sp));
+  }
+
+  // The k best AED expansions (beam search with fusion): all
+  // V+1 fused values by the AED rule, ordered by value descending then
+  // column ascending; NaN values are never candidates (R14, R15).
+  void topk(const float* asr, int32_t sp, float lambda, int32_t s, const float* ilm, float lam_ilm, int32_t k,
+            float* sc, int32_t* cols, int32_t* nxt) const {
+    const int32_t ncols = V + 1;
+    std::vector<std::pair<float, int32_t>> cand;
+    for (int32_t c = 0; c < ncols; ++c) {
+      const float v = (c == sp) ? std::fmaf(lambda, final32(s), asr[c])
+                                : rescore(lambda, score32(s, tok_of(c, sp)), asr[c], ilm, lam_ilm, tok_of(c, sp));
+      if (!std::isnan(v)) cand.emplace_back(v, c);
+    }
+    std::sort(cand.begin(), cand.end(), [](const std::pair<float, int32_t>& a, const std::pair<float, int32_t>& b) {
+      return a.first > b.first || (a.first == b.first && a.second < b.second);
+    });
+    for (int32_t i = 0; i < k; ++i) {
+      if (i < (int32_t)cand.size()) {
+        sc[i] = cand[i].first;
+        cols[i] = cand[i].second;
+        nxt[i] = cand[i].second == sp ? s : next(s, tok_of(cand[i].second, sp));
+      } else {
+        sc[i] = -INFINITY; cols[i] = -1; nxt[i] = -1;
+      }
+    }
   }
 };
 
@@ -400,6 +434,30 @@ void oracle_fused_step(void* h, int mode, const float* logits, int64_t row_strid
     int32_t dummy = -1;
     o->fused_step(mode, logits + i * row_stride, blank_id, lambda, &states[i],
                   prev ? &prev[i] : &dummy, &tokens_out[i]);
+  });
+}
+
+// fused step with the ILM term (R21); ilm row i at ilm + i*ilm_stride, V entries
+void oracle_fused_step_ilm(void* h, int mode, const float* logits, int64_t row_stride, int64_t n,
+                           int32_t* states, int32_t* prev, const uint8_t* active, float lambda, int32_t blank_id,
+                           const float* ilm, int64_t ilm_stride, float lam_ilm, int32_t* tokens_out, int nthreads) {
+  auto* o = (Oracle*)h;
+  parallel_rows(n, nthreads, [&](int64_t i) {
+    if (active && !active[i]) { tokens_out[i] = -1; return; }
+    int32_t dummy = -1;
+    o->fused_step(mode, logits + i * row_stride, blank_id, lambda, &states[i], prev ? &prev[i] : &dummy,
+                  &tokens_out[i], ilm + i * ilm_stride, lam_ilm);
+  });
+}
+
+// k best AED expansions per row (ilm may be NULL)
+void oracle_topk(void* h, const float* logits, int64_t row_stride, int64_t n, const int32_t* states,
+                 const float* ilm, int64_t ilm_stride, float lambda, float lam_ilm, int32_t eos_id, int32_t k,
+                 float* sc, int32_t* cols, int32_t* nxt, int nthreads) {
+  auto* o = (Oracle*)h;
+  parallel_rows(n, nthreads, [&](int64_t i) {
+    o->topk(logits + i * row_stride, eos_id, lambda, states[i], ilm ? ilm + i * ilm_stride : nullptr, lam_ilm, k,
+            sc + i * k, cols + i * k, nxt + i * k);
   });
 }
 

@@ -23,6 +23,7 @@ CTC, RNNT, AED = 0, 1, 2
 CHAIN_TABLE, CHAIN_WALK = 0, 1
 ADVANCE_AUTO, ADVANCE_WARP, ADVANCE_CTA = 0, 1, 2
 MAX_ORDER = 32
+MAX_TOPK = 256
 
 
 class NgpulmError(RuntimeError):
@@ -61,6 +62,9 @@ SIGNATURES = {
     "ngpulm_advance": (C.c_int, [_P, _P, _I32, _P, _P, _P, _P]),
     "ngpulm_final": (C.c_int, [_P, _P, _I32, _P, _P]),
     "ngpulm_fused_greedy_step": (C.c_int, [_P, _I32, _P, _I64, _I32, _P, _P, _P, _F, _I32, _P, _P]),
+    "ngpulm_fused_greedy_step_ilm": (C.c_int, [_P, _I32, _P, _I64, _I32, _P, _P, _P, _F, _I32, _P, _I64, _F, _P,
+                                                _P]),
+    "ngpulm_fused_topk": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _I64, _F, _F, _I32, _I32, _P, _P, _P, _P]),
     "ngpulm_ctc_greedy_decode": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _F, _I32, _P, _P, _P,
                                             _P]),
     "ngpulm_check": (C.c_int, [_P, _P, C.POINTER(_I64)]),
@@ -236,6 +240,49 @@ class NgpuLM:
             float(lam), blank, _dev_ptr(tokens_out, torch.int32, "tokens_out", B), _stream(stream)))
         return tokens_out
 
+    def fused_greedy_step_ilm(self, mode: int, logits, states, ilm, lam_ilm: float, prev=None, active=None,
+                              lam: float = 0.3, blank_id: int | None = None, tokens_out=None, stream=None):
+        """ngpulm_fused_greedy_step_ilm: the fused step minus lam_ilm * ilm[b, v] on the
+        LM-rescored columns. ilm: [B, V] CUDA f32 (rows contiguous)."""
+        import torch
+        B = states.numel()
+        if logits.dtype != torch.float32 or not logits.is_cuda or logits.dim() != 2 or logits.stride(1) != 1:
+            raise TypeError("logits: expected a [B, V+1] CUDA float32 tensor with contiguous rows")
+        if ilm.dtype != torch.float32 or not ilm.is_cuda or ilm.dim() != 2 or ilm.stride(1) != 1:
+            raise TypeError("ilm: expected a [B, V] CUDA float32 tensor with contiguous rows")
+        if tokens_out is None:
+            tokens_out = torch.empty(B, dtype=torch.int32, device=states.device)
+        blank = self.V if blank_id is None else blank_id
+        _check(lib().ngpulm_fused_greedy_step_ilm(
+            self._h, mode, logits.data_ptr(), logits.stride(0), B,
+            _dev_ptr(states, torch.int32, "states", B),
+            _dev_ptr(prev, torch.int32, "prev", B) if prev is not None else None,
+            _dev_ptr(active, torch.uint8, "active", B) if active is not None else None,
+            float(lam), blank, ilm.data_ptr(), ilm.stride(0), float(lam_ilm),
+            _dev_ptr(tokens_out, torch.int32, "tokens_out", B), _stream(stream)))
+        return tokens_out
+
+    def fused_topk(self, logits, states, k: int, lam: float = 0.3, eos_id: int | None = None, ilm=None,
+                   lam_ilm: float = 0.0, want_next: bool = True, stream=None):
+        """ngpulm_fused_topk -> (scores [B,k] f32, cols [B,k] i32, next [B,k] i32 or None)."""
+        import torch
+        B = states.numel()
+        if logits.dtype != torch.float32 or not logits.is_cuda or logits.dim() != 2 or logits.stride(1) != 1:
+            raise TypeError("logits: expected a [B, V+1] CUDA float32 tensor with contiguous rows")
+        dev = logits.device
+        sc = torch.empty((B, k), dtype=torch.float32, device=dev)
+        cols = torch.empty((B, k), dtype=torch.int32, device=dev)
+        nx = torch.empty((B, k), dtype=torch.int32, device=dev) if want_next else None
+        eos = self.V if eos_id is None else eos_id
+        if ilm is not None and (ilm.dtype != torch.float32 or not ilm.is_cuda or ilm.stride(-1) != 1):
+            raise TypeError("ilm: expected a [B, V] CUDA float32 tensor with contiguous rows")
+        _check(lib().ngpulm_fused_topk(
+            self._h, logits.data_ptr(), logits.stride(0), B, _dev_ptr(states, torch.int32, "states", B),
+            ilm.data_ptr() if ilm is not None else None, ilm.stride(0) if ilm is not None else 0,
+            float(lam), float(lam_ilm), eos, k, sc.data_ptr(), cols.data_ptr(),
+            nx.data_ptr() if nx is not None else None, _stream(stream)))
+        return sc, cols, nx
+
     def ctc_greedy_decode(self, logits, states, prev, lam: float = 0.3, blank_id: int | None = None,
                           lengths=None, frames_out=None, emit_out=None, emit_len=None, want_frames=True,
                           stream=None):
@@ -301,6 +348,8 @@ ngpulm_final = NgpuLM.final
 ngpulm_fused_greedy_step = NgpuLM.fused_greedy_step
 ngpulm_check = NgpuLM.check
 ngpulm_ctc_greedy_decode = NgpuLM.ctc_greedy_decode
+ngpulm_fused_greedy_step_ilm = NgpuLM.fused_greedy_step_ilm
+ngpulm_fused_topk = NgpuLM.fused_topk
 ngpulm_replicate = NgpuLM.replicate
 ngpulm_set_chain_mode = NgpuLM.set_chain_mode
 ngpulm_set_advance_kernel = NgpuLM.set_advance_kernel

@@ -291,9 +291,45 @@ int ngpulm_fused_greedy_step(const ngpulm_model* m, int32_t mode, const float* l
   if (!logits || !states || !tokens_out || (mode == NGPULM_CTC && !prev))
     return err(NGPULM_EUSAGE, "NULL device buffer");
   if (B > 1 && row_stride < (int64_t)m->h.V + 1) return err(NGPULM_EUSAGE, "row_stride < V+1");
-  int e = ngpulm::launch_fused(m->dm, mode, logits, row_stride, B, states, prev, active, lambda, blank_id,
-                               tokens_out, stream);
+  int e = ngpulm::launch_fused(m->dm, mode, logits, row_stride, B, states, prev, active, lambda, blank_id, nullptr,
+                               0, 0.f, tokens_out, stream);
   if (e) return cuda_err((cudaError_t)e, "fused step launch");
+  return NGPULM_OK;
+}
+
+int ngpulm_fused_greedy_step_ilm(const ngpulm_model* m, int32_t mode, const float* logits, int64_t row_stride,
+                                 int32_t B, int32_t* states, int32_t* prev, const uint8_t* active, float lambda,
+                                 int32_t blank_id, const float* ilm, int64_t ilm_stride, float lambda_ilm,
+                                 int32_t* tokens_out, ngpulm_stream stream) {
+  if (int r = check_hot(m, B)) return r;
+  if (mode != NGPULM_CTC && mode != NGPULM_RNNT && mode != NGPULM_AED) return err(NGPULM_EUSAGE, "bad mode");
+  if (blank_id < 0 || blank_id > m->h.V) return err(NGPULM_EUSAGE, "blank_id outside [0, V]");
+  if (B == 0) return NGPULM_OK;
+  if (!logits || !states || !tokens_out || !ilm || (mode == NGPULM_CTC && !prev))
+    return err(NGPULM_EUSAGE, "NULL device buffer");
+  if (B > 1 && row_stride < (int64_t)m->h.V + 1) return err(NGPULM_EUSAGE, "row_stride < V+1");
+  if (B > 1 && ilm_stride < (int64_t)m->h.V) return err(NGPULM_EUSAGE, "ilm_stride < V");
+  int e = ngpulm::launch_fused(m->dm, mode, logits, row_stride, B, states, prev, active, lambda, blank_id, ilm,
+                               ilm_stride, lambda_ilm, tokens_out, stream);
+  if (e) return cuda_err((cudaError_t)e, "fused step launch");
+  return NGPULM_OK;
+}
+
+int ngpulm_fused_topk(const ngpulm_model* m, const float* logits, int64_t row_stride, int32_t B,
+                      const int32_t* states, const float* ilm, int64_t ilm_stride, float lambda, float lambda_ilm,
+                      int32_t eos_id, int32_t k, float* topk_scores, int32_t* topk_cols, int32_t* topk_next,
+                      ngpulm_stream stream) {
+  if (int r = check_hot(m, B)) return r;
+  if (eos_id < 0 || eos_id > m->h.V) return err(NGPULM_EUSAGE, "eos_id outside [0, V]");
+  if (k < 1 || k > NGPULM_MAX_TOPK) return err(NGPULM_EUSAGE, "k outside [1, NGPULM_MAX_TOPK]");
+  if (m->h.V % 4 != 0 || m->h.V > 1024) return err(NGPULM_EUSAGE, "top-k needs V % 4 == 0 and V <= 1024");
+  if (B == 0) return NGPULM_OK;
+  if (!logits || !states || !topk_scores || !topk_cols) return err(NGPULM_EUSAGE, "NULL device buffer");
+  if (B > 1 && row_stride < (int64_t)m->h.V + 1) return err(NGPULM_EUSAGE, "row_stride < V+1");
+  if (ilm && B > 1 && ilm_stride < (int64_t)m->h.V) return err(NGPULM_EUSAGE, "ilm_stride < V");
+  int e = ngpulm::launch_topk(m->dm, logits, row_stride, B, states, ilm, ilm_stride, lambda, lambda_ilm, eos_id, k,
+                              topk_scores, topk_cols, topk_next, stream);
+  if (e) return cuda_err((cudaError_t)e, "top-k launch");
   return NGPULM_OK;
 }
 

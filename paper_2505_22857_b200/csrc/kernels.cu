@@ -873,6 +873,15 @@ __global__ void final_kernel(DevModel m, const int32_t* __restrict__ states, int
 }
 
 // ---------------------------------------------------------------- fused greedy step
+// Optional internal-LM subtraction (HAT "-ILM+LM"):
+// the LM-rescored columns get fmaf(-lam, ilm[token], fmaf(lambda, lm, asr))
+// (R21). ilm row b: p + b * stride, indexed by LM token (V entries).
+struct AuxRow {
+  const float* p;  // nullptr: no ILM term
+  int64_t stride;
+  float lam;
+};
+
 // (value, column) order: larger value first, then lower column (R14).
 __device__ __forceinline__ bool better(float v2, int32_t c2, float v, int32_t c) {
   return v2 > v || (v2 == v && c2 < c);
@@ -900,7 +909,7 @@ template <int kMode, bool kTable>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     fused_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int32_t* __restrict__ states,
                  int32_t* __restrict__ prev, const uint8_t* __restrict__ active, float lambda, int32_t sp,
-                 int32_t* __restrict__ tokens_out) {
+                 AuxRow aux, int32_t* __restrict__ tokens_out) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int32_t V = m.V, ncols = V + 1, b = blockIdx.x;
   const int t = threadIdx.x;
@@ -953,7 +962,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     } else if (kMode == NGPULM_CTC && col == pc) {
       val = a;                                                        // repeated token: not rescored
     } else {
-      val = __fmaf_rn(lambda, s.row_s[col < sp ? col : col - 1], a);  // asr + lambda * lm, one rounding
+      const int32_t tok = col < sp ? col : col - 1;
+      val = __fmaf_rn(lambda, s.row_s[tok], a);  // asr + lambda * lm, one rounding
+      if (aux.p) val = __fmaf_rn(-aux.lam, __ldg(aux.p + (size_t)b * aux.stride + tok), val);  // - lambda_ilm * ilm (R21)
     }
     if (better(val, col, bv, bc)) { bv = val; bc = col; }
   }
@@ -1029,11 +1040,11 @@ __device__ __forceinline__ void edge_logits(const float* lrow, int32_t ncols, co
   if (c >= 0) const_cast<float*>(L.buf)[L.h + c] = __ldg(&lrow[c]);
 }
 
-template <int kMode, bool kTable, bool kPacked>
+template <int kMode, bool kTable, bool kPacked, bool kAux>
 __global__ void __launch_bounds__(256, 1)
     fused_warp_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int32_t B,
                       int32_t* __restrict__ states, int32_t* __restrict__ prev, const uint8_t* __restrict__ active,
-                      float lambda, int32_t sp, int32_t* __restrict__ tokens_out) {
+                      float lambda, int32_t sp, AuxRow aux, int32_t* __restrict__ tokens_out) {
   constexpr int kW = 8;
   extern __shared__ __align__(16) unsigned char smem[];
   const int32_t V = m.V, ncols = V + 1;
@@ -1066,6 +1077,16 @@ __global__ void __launch_bounds__(256, 1)
   pdl_wait();
   STAMP(2);
   const float* lrow = logits + (size_t)row * row_stride;
+  float ilm[kAux ? kMaxColsPerLane : 1];
+  if (kAux) {  // the row's ILM scores, column layout (lane i: columns i, i+32, ...), loads in flight early
+    const float* arow = aux.p + (size_t)row * aux.stride;
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j) {
+      const int32_t col = lane + 32 * j;
+      ilm[j] = 0.f;
+      if (col < ncols && col != sp) ilm[j] = __ldg(arow + (col - (col > sp)));
+    }
+  }
   const bool on = !active || __ldg(&active[row]);  // used only after the state and record loads are issued
   const int32_t pc = (kMode == NGPULM_CTC) ? __ldg(&prev[row]) : -2;
   WLevel lv;
@@ -1141,6 +1162,7 @@ __global__ void __launch_bounds__(256, 1)
       const float x = xs[j];
       if (kMode == NGPULM_RNNT && (x > rv || (rc == INT_MAX && x == rv))) { rv = x; rc = col; }  // stage 1
       float val = __fmaf_rn(lambda, col == sp ? sp_val : lm[j], x);  // asr + lambda * lm, one rounding
+      if (kAux && col != sp) val = __fmaf_rn(-aux.lam, ilm[j], val);  // - lambda_ilm * ilm (R21)
       if (kMode == NGPULM_CTC && (col == sp || col == pc)) val = x;  // blank raw, repeated token not rescored
       if (kMode == NGPULM_RNNT && col == sp) val = __int_as_float(0x7fc00000);  // stage 2: non-blank only
       if (val > bv || (bc == INT_MAX && val == bv)) { bv = val; bc = col; }
@@ -1167,6 +1189,157 @@ __global__ void __launch_bounds__(256, 1)
   }
   STAMP(8);
   if (w == 0) STAMPS_OUT(row);
+}
+
+// Total order of floats as unsigned keys (larger float -> larger key).
+__device__ __forceinline__ uint32_t fkey(float v) {
+  const uint32_t u = __float_as_uint(v);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// ---------------------------------------------------------------- fused top-k
+// The k best expansions of each row for AED beam search with NGPU-LM fusion
+// ("greedy and beam search"): fused values over all V+1
+// columns by the AED rule (token columns fmaf(lambda, lm, asr) [- lambda_ilm
+// * ilm], eos column fmaf(lambda, final(state), asr[eos])), sorted by value
+// descending, lowest column first on ties, NaN never selected. Row build and
+// logits staging as in fused_warp_kernel; k rounds of a two-pass warp
+// argmax over the values held in registers.
+template <bool kTable, bool kPacked>
+__global__ void __launch_bounds__(256, 1)
+    topk_warp_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int32_t B,
+                     const int32_t* __restrict__ states, float lambda, int32_t sp, AuxRow aux, int32_t k,
+                     float* __restrict__ out_scores, int32_t* __restrict__ out_cols, int32_t* __restrict__ out_next) {
+  constexpr int kW = 8;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int32_t V = m.V, ncols = V + 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, R = blockDim.x >> 5;
+  unsigned char* base = smem + (size_t)w * fslice_bytes(V, m.order);
+  const WSlice s = wcarve(base, V, m.order, 0);
+  uint64_t* lbar = s.abar;
+  float* lbuf = reinterpret_cast<float*>(base + wslice_bytes(V, m.order, 0));
+  const int32_t row = (int32_t)blockIdx.x * R + w;
+  pdl_trigger();
+  if (row >= B) return;
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(s.bar)) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(lbar)) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)), "r"((uint32_t)V * 4u)
+                 : "memory");
+    bulk_g2s(s.row_n, m.arc_to, (uint32_t)V * 4u, s.bar);
+  }
+  float4 rw[8];
+  {
+    const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (lane + 32 * j < V / 4) rw[j] = __ldg(w4 + lane + 32 * j);
+  }
+  pdl_wait();
+  const float* lrow = logits + (size_t)row * row_stride;
+  float ilm[kMaxColsPerLane];
+#pragma unroll
+  for (int j = 0; j < kMaxColsPerLane; ++j) {
+    const int32_t col = lane + 32 * j;
+    ilm[j] = 0.f;
+    if (aux.p && col < ncols && col != sp) ilm[j] = __ldg(aux.p + (size_t)row * aux.stride + (col - (col > sp)));
+  }
+  WLevel lv;
+  int32_t nslots;
+  LogitsRow L{lbuf, 0, 0, 0};
+  bool started = false;
+  auto begin_logits = [&]() {
+    L = start_logits(lrow, ncols, lbuf, lbar);
+    started = true;
+  };
+  const Row r = warp_row<kTable>(m, states + row, s, lv, nslots, begin_logits);
+  float* osc = out_scores + (size_t)row * k;
+  int32_t* ocol = out_cols + (size_t)row * k;
+  int32_t* onx = out_next ? out_next + (size_t)row * k : nullptr;
+  if (r.bad) {
+    if (lane == 0) atomicMin(m.bad_row, (unsigned long long)row);
+    for (int32_t i = lane; i < k; i += 32) {
+      osc[i] = __int_as_float(0x7fc00000);
+      ocol[i] = -1;
+      if (onx) onx[i] = -1;
+    }
+    mbar_wait(s.bar, 0);
+    if (started) mbar_wait(lbar, 0);
+    return;
+  }
+  Window<kW, kPacked> a;
+  load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
+  edge_logits(lrow, ncols, L);
+  {
+    float4* s4 = reinterpret_cast<float4*>(s.row_s);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (lane + 32 * j < V / 4) {
+        float4 y = rw[j];
+        y.x = __fadd_rn(r.acc_root, y.x);
+        y.y = __fadd_rn(r.acc_root, y.y);
+        y.z = __fadd_rn(r.acc_root, y.z);
+        y.w = __fadd_rn(r.acc_root, y.w);
+        s4[lane + 32 * j] = y;
+      }
+  }
+  mbar_wait(s.bar, 0);
+  __syncwarp();
+  for (int32_t k0 = 0; k0 < nslots;) {
+    write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
+    k0 += kW;
+    if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
+  }
+  mbar_wait(lbar, 0);
+  __syncwarp();
+  float val[kMaxColsPerLane];
+#pragma unroll
+  for (int j = 0; j < kMaxColsPerLane; ++j) {
+    const int32_t col = lane + 32 * j;
+    float x = __int_as_float(0x7fc00000);
+    float v = x;
+    if (col < ncols) {
+      x = L.buf[L.h + col];
+      if (col == sp) {
+        v = __fmaf_rn(lambda, r.fin, x);  // eos <-> final weight
+      } else {
+        v = __fmaf_rn(lambda, s.row_s[col - (col > sp)], x);
+        if (aux.p) v = __fmaf_rn(-aux.lam, ilm[j], v);
+      }
+    }
+    val[j] = v;
+  }
+  for (int32_t i = 0; i < k; ++i) {
+    float mx[kMaxColsPerLane];
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j) mx[j] = val[j];
+#pragma unroll
+    for (int d = 1; d < kMaxColsPerLane; d *= 2)
+#pragma unroll
+      for (int j = 0; j + d < kMaxColsPerLane; j += 2 * d) mx[j] = fmaxf(mx[j], mx[j + d]);
+    const float lmax = mx[0] == mx[0] ? mx[0] : -INFINITY;
+    const bool any = __any_sync(kFull, mx[0] == mx[0]);
+    if (!any) {  // fewer than k selectable (non-NaN) columns
+      if (lane == 0) { osc[i] = -INFINITY; ocol[i] = -1; if (onx) onx[i] = -1; }
+      continue;
+    }
+    const uint32_t kmax = __reduce_max_sync(kFull, fkey(lmax));
+    const float M = __uint_as_float((kmax & 0x80000000u) ? (kmax ^ 0x80000000u) : ~kmax);
+    int32_t cm = INT_MAX;
+#pragma unroll
+    for (int j = kMaxColsPerLane - 1; j >= 0; --j)
+      if (val[j] == M) cm = lane + 32 * j;
+    const int32_t bc = (int32_t)__reduce_min_sync(kFull, (uint32_t)cm);
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j)
+      if (lane + 32 * j == bc) val[j] = __int_as_float(0x7fc00000);  // taken
+    if (lane == 0) {
+      osc[i] = M;
+      ocol[i] = bc;
+      if (onx) onx[i] = bc == sp ? r.state : s.row_n[bc - (bc > sp)];
+    }
+  }
 }
 
 // ---------------------------------------------------------------- persistent CTC decode
@@ -1270,12 +1443,6 @@ __device__ __forceinline__ Row build_row_warp(const DevModel& m, const WSlice& s
   __syncwarp();
   stamp(8);
   return r;
-}
-
-// Total order of floats as unsigned keys (larger float -> larger key).
-__device__ __forceinline__ uint32_t fkey(float v) {
-  const uint32_t u = __float_as_uint(v);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
 constexpr int kDecodeMaxRows = 4;  // rows per CTA (2 warps each): 256 threads, up to 255 registers
@@ -1564,17 +1731,19 @@ int launch_final(const DevModel& m, const int32_t* states, int32_t B, float* out
 
 template <int kMode>
 int launch_fused_mode(const DevModel& m, const float* logits, int64_t row_stride, int32_t B, int32_t* states,
-                      int32_t* prev, const uint8_t* active, float lambda, int32_t blank, int32_t* tokens_out,
-                      cudaStream_t st) {
+                      int32_t* prev, const uint8_t* active, float lambda, int32_t blank, AuxRow aux,
+                      int32_t* tokens_out, cudaStream_t st) {
   if (m.V % 4 == 0 && m.V <= 1024 && m.adv_kind != NGPULM_ADVANCE_CTA) {
     int R = (B + 147) / 148;
     R = R < 1 ? 1 : (R > 8 ? 8 : R);
     const size_t wsm = (size_t)R * fslice_bytes(m.V, m.order);
     const dim3 wg((B + R - 1) / R), wb(32 * R);
     const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
-#define NGPULM_FUSED_LAUNCH(T, P)                                                                              \
-  return launch(fused_warp_kernel<kMode, T, P>, wg, wb, wsm, st, m, logits, row_stride, B, states, prev, active, \
-                lambda, blank, tokens_out)
+#define NGPULM_FUSED_LAUNCH(T, P)                                                                                 \
+  return aux.p ? launch(fused_warp_kernel<kMode, T, P, true>, wg, wb, wsm, st, m, logits, row_stride, B, states,    \
+                        prev, active, lambda, blank, aux, tokens_out)                                               \
+               : launch(fused_warp_kernel<kMode, T, P, false>, wg, wb, wsm, st, m, logits, row_stride, B, states,   \
+                        prev, active, lambda, blank, aux, tokens_out)
     if (table) { if (pk) NGPULM_FUSED_LAUNCH(true, true); NGPULM_FUSED_LAUNCH(true, false); }
     if (pk) NGPULM_FUSED_LAUNCH(false, true);
     NGPULM_FUSED_LAUNCH(false, false);
@@ -1584,9 +1753,9 @@ int launch_fused_mode(const DevModel& m, const float* logits, int64_t row_stride
   const dim3 gd(B), bd(kThreads);
   if (m.chain != nullptr)
     return launch(fused_kernel<kMode, true>, gd, bd, sm, st, m, logits, row_stride, states, prev, active, lambda,
-                  blank, tokens_out);
+                  blank, aux, tokens_out);
   return launch(fused_kernel<kMode, false>, gd, bd, sm, st, m, logits, row_stride, states, prev, active, lambda,
-                blank, tokens_out);
+                blank, aux, tokens_out);
 }
 
 int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride, int64_t frame_stride, int32_t B,
@@ -1613,19 +1782,40 @@ int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride
 
 int launch_fused(const DevModel& m, int32_t mode, const float* logits, int64_t row_stride, int32_t B,
                  int32_t* states, int32_t* prev, const uint8_t* active, float lambda, int32_t blank,
-                 int32_t* tokens_out, void* stream) {
+                 const float* aux, int64_t aux_stride, float lambda_ilm, int32_t* tokens_out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  const AuxRow ax{aux, aux_stride, lambda_ilm};
   switch (mode) {
     case NGPULM_CTC:
-      return launch_fused_mode<NGPULM_CTC>(m, logits, row_stride, B, states, prev, active, lambda, blank,
+      return launch_fused_mode<NGPULM_CTC>(m, logits, row_stride, B, states, prev, active, lambda, blank, ax,
                                            tokens_out, st);
     case NGPULM_RNNT:
-      return launch_fused_mode<NGPULM_RNNT>(m, logits, row_stride, B, states, prev, active, lambda, blank,
+      return launch_fused_mode<NGPULM_RNNT>(m, logits, row_stride, B, states, prev, active, lambda, blank, ax,
                                             tokens_out, st);
     default:
-      return launch_fused_mode<NGPULM_AED>(m, logits, row_stride, B, states, prev, active, lambda, blank,
+      return launch_fused_mode<NGPULM_AED>(m, logits, row_stride, B, states, prev, active, lambda, blank, ax,
                                            tokens_out, st);
   }
+}
+
+int launch_topk(const DevModel& m, const float* logits, int64_t row_stride, int32_t B, const int32_t* states,
+                const float* aux, int64_t aux_stride, float lambda, float lambda_ilm, int32_t eos, int32_t k,
+                float* out_scores, int32_t* out_cols, int32_t* out_next, void* stream) {
+  if (m.V % 4 != 0 || m.V > 1024) return (int)cudaErrorNotSupported;
+  int R = (B + 147) / 148;
+  R = R < 1 ? 1 : (R > 8 ? 8 : R);
+  const size_t wsm = (size_t)R * fslice_bytes(m.V, m.order);
+  const dim3 wg((B + R - 1) / R), wb(32 * R);
+  const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
+  const AuxRow ax{aux, aux_stride, lambda_ilm};
+  cudaStream_t st = (cudaStream_t)stream;
+#define NGPULM_TOPK_LAUNCH(T, P)                                                                                   \
+  return launch(topk_warp_kernel<T, P>, wg, wb, wsm, st, m, logits, row_stride, B, states, lambda, eos, ax, k, \
+                out_scores, out_cols, out_next)
+  if (table) { if (pk) NGPULM_TOPK_LAUNCH(true, true); NGPULM_TOPK_LAUNCH(true, false); }
+  if (pk) NGPULM_TOPK_LAUNCH(false, true);
+  NGPULM_TOPK_LAUNCH(false, false);
+#undef NGPULM_TOPK_LAUNCH
 }
 
 }  // namespace ngpulm

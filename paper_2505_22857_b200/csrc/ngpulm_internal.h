@@ -86,7 +86,11 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
 int launch_final(const DevModel& m, const int32_t* states, int32_t B, float* out, void* stream);
 int launch_fused(const DevModel& m, int32_t mode, const float* logits, int64_t row_stride,
                  int32_t B, int32_t* states, int32_t* prev, const uint8_t* active, float lambda,
-                 int32_t blank, int32_t* tokens_out, void* stream);
+                 int32_t blank, const float* aux, int64_t aux_stride, float lambda_ilm,
+                 int32_t* tokens_out, void* stream);
+int launch_topk(const DevModel& m, const float* logits, int64_t row_stride, int32_t B, const int32_t* states,
+                const float* aux, int64_t aux_stride, float lambda, float lambda_ilm, int32_t eos, int32_t k,
+                float* out_scores, int32_t* out_cols, int32_t* out_next, void* stream);
 int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride, int64_t frame_stride, int32_t B,
                       int32_t T, const int32_t* lengths, int32_t* states, int32_t* prev, float lambda, int32_t blank,
                       int32_t* frames_out, int32_t* emit_out, int32_t* emit_len, void* stream);

@@ -1,0 +1,108 @@
+"""GPU parity of the SURVEY.md §8(f) f3 extensions against the oracle:
+ngpulm_fused_greedy_step_ilm (internal-LM subtraction, R21) and ngpulm_fused_topk
+(the k best AED expansions for beam search with NGPU-LM fusion). Bar: tokens,
+states, columns and next states bit-exact; top-k scores bit-exact (same float
+operations in the same order as the oracle)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import AED, CTC, RNNT
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2505_22857_b200 as ng  # noqa: E402
+
+from test_gpu_parity import dev, same_bits, trajectory_states, using  # noqa: E402
+
+
+def T(a, dt=None):
+    return torch.from_numpy(np.ascontiguousarray(a if dt is None else a.astype(dt))).to(dev())
+
+
+@pytest.mark.parametrize("kernel", [ng.ADVANCE_AUTO, ng.ADVANCE_WARP, ng.ADVANCE_CTA])
+@pytest.mark.parametrize("lam_ilm", [0.0, 0.6])
+@pytest.mark.parametrize("mode", [CTC, RNNT, AED])
+@pytest.mark.parametrize("name", ["tri64", "ten24"])
+def test_fused_step_ilm_matches_oracle(pairs, name, mode, lam_ilm, kernel):
+    m, o, _ = pairs[name]
+    B = 257
+    rng = np.random.default_rng(41)
+    x = synth.rnnt_logits(B, 1, o.V, seed=42)[0]
+    st = synth.uniform_states(o.num_states, B, seed=43)
+    ilm = rng.normal(-4, 2, size=(B, o.V)).astype(np.float32)
+    prev = rng.integers(-1, o.V, size=B).astype(np.int32) if mode == CTC else None
+    active = (rng.random(B) > 0.1).astype(np.uint8)
+    st_d = T(st)
+    pv_d = T(prev) if prev is not None else None
+    with using(m, kernel=kernel):
+        tok = m.fused_greedy_step_ilm(mode, T(x), st_d, T(ilm), lam_ilm, prev=pv_d, active=T(active), lam=1.1)
+    torch.cuda.synchronize()
+    to, so, po = o.fused_step_ilm(mode, x, st, ilm, lam_ilm, prev=prev, active=active, lam=1.1)
+    assert np.array_equal(tok.cpu().numpy(), to) and np.array_equal(st_d.cpu().numpy(), so)
+    if mode == CTC:
+        assert np.array_equal(pv_d.cpu().numpy(), po)
+
+
+@pytest.mark.parametrize("chain", [ng.CHAIN_TABLE, ng.CHAIN_WALK])
+@pytest.mark.parametrize("kernel", [ng.ADVANCE_AUTO, ng.ADVANCE_WARP])
+@pytest.mark.parametrize("k", [1, 4, 33])
+@pytest.mark.parametrize("lam", [0.0, 0.3, 3.0])
+@pytest.mark.parametrize("name", ["tiny3", "five48", "ten24"])
+def test_topk_matches_oracle(pairs, name, lam, k, kernel, chain):
+    m, o, _ = pairs[name]
+    B = 150
+    x = synth.rnnt_logits(B, 1, o.V, seed=44)[0]
+    x[::7, 5] = x[::7, 2]                         # exact ties
+    st = synth.uniform_states(o.num_states, B, seed=45)
+    with using(m, chain, kernel):
+        sc, cols, nx = m.fused_topk(T(x), T(st), k, lam=lam)
+    torch.cuda.synchronize()
+    so, co, no = o.topk(x, st, k, lam=lam)
+    assert np.array_equal(cols.cpu().numpy(), co)
+    assert same_bits(sc.cpu().numpy(), so)
+    assert np.array_equal(nx.cpu().numpy(), no)
+
+
+@pytest.mark.parametrize("eos", [0, 11])
+def test_topk_with_ilm_and_eos_inside(pairs, eos):
+    m, o, _ = pairs["tri64"]
+    B, k = 100, 8
+    x = synth.rnnt_logits(B, 1, o.V, seed=46, blank=eos)[0]
+    st = synth.uniform_states(o.num_states, B, seed=47)
+    ilm = np.random.default_rng(48).normal(-4, 2, size=(B, o.V)).astype(np.float32)
+    sc, cols, nx = m.fused_topk(T(x), T(st), k, lam=0.9, eos_id=eos, ilm=T(ilm), lam_ilm=0.4)
+    torch.cuda.synchronize()
+    so, co, no = o.topk(x, st, k, lam=0.9, eos_id=eos, ilm=ilm, lam_ilm=0.4)
+    assert np.array_equal(cols.cpu().numpy(), co) and same_bits(sc.cpu().numpy(), so)
+    assert np.array_equal(nx.cpu().numpy(), no)
+
+
+def test_topk_beam_shape_6gram(lm6):
+    """AED beam-search shape on the configs[1] LM: beam 4 x 128 utterances = 512
+    hypothesis rows, k = 4 (beam = 4), trajectory states."""
+    m, o, f = lm6
+    B, k = 512, 4
+    st, _ = trajectory_states(m, f, B, seed=49)
+    x = synth.aed_logits(B, 1, m.V, seed=50)[0]
+    sc, cols, nx = m.fused_topk(T(x), T(st), k, lam=0.3)
+    torch.cuda.synchronize()
+    rows = np.arange(0, B, 8)
+    so, co, no = o.topk(x[rows], st[rows], k, lam=0.3)
+    assert np.array_equal(cols.cpu().numpy()[rows], co) and same_bits(sc.cpu().numpy()[rows], so)
+    assert np.array_equal(nx.cpu().numpy()[rows], no)
+
+
+def test_topk_invalid_state_and_bad_k(pairs):
+    m, o, _ = pairs["tri64"]
+    x = synth.rnnt_logits(3, 1, o.V, seed=1)[0]
+    st = np.array([1, o.num_states + 5, 2], np.int32)
+    sc, cols, nx = m.fused_topk(T(x), T(st), 3, lam=0.5)
+    torch.cuda.synchronize()
+    assert (cols.cpu().numpy()[1] == -1).all() and np.isnan(sc.cpu().numpy()[1]).all()
+    assert m.check() == 1
+    with pytest.raises(ng.NgpulmError):
+        m.fused_topk(T(x), T(st), 0)
+    with pytest.raises(ng.NgpulmError):
+        m.fused_topk(T(x), T(st), ng.MAX_TOPK + 1)

@@ -195,3 +195,93 @@ def test_oracle_ctc_decode_is_the_frame_loop(tri):
                 em.append(c)
             last = -1 if c == o.V else c
         assert list(emitted[b, : elen[b]]) == em
+
+
+# ---------------------------------------------------------------- ILM subtraction (R21) and top-k (f3)
+def _margin_ok(vals, tol=1e-3):
+    """rows whose best value beats the runner-up by more than tol (decision not rounding-sensitive)"""
+    s = np.sort(vals, axis=1)
+    return (s[:, -1] - s[:, -2]) > tol
+
+
+@pytest.mark.parametrize("mode", [CTC, RNNT, AED])
+def test_ilm_zero_weight_is_plain_fusion(tri, mode):
+    o, f = tri
+    B = 64
+    x = synth.rnnt_logits(B, 1, o.V, seed=31)[0]
+    st = synth.uniform_states(o.num_states, B, seed=32)
+    ilm = np.random.default_rng(33).normal(-5, 2, size=(B, o.V)).astype(np.float32)
+    pv = np.full(B, -1, np.int32) if mode == CTC else None
+    a = o.fused_step(mode, x, st, prev=pv, lam=0.8)
+    b = o.fused_step_ilm(mode, x, st, ilm, 0.0, prev=pv, lam=0.8)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_ilm_term_against_float64_definition(tri):
+    """AED decisions = argmax of asr + lam*lm - lam_ilm*ilm computed in float64 from
+    the textbook score64 rows and final64, wherever the margin is clear."""
+    o, f = tri
+    B = 400
+    x = synth.rnnt_logits(B, 1, o.V, seed=34)[0]
+    st = synth.uniform_states(o.num_states, B, seed=35)
+    ilm = np.random.default_rng(36).normal(-4, 2, size=(B, o.V)).astype(np.float32)
+    lam, lam_ilm = 1.5, 0.7
+    _, s64, _, _ = o.rows(st)
+    _, f64 = o.finals(st)
+    ref = np.empty((B, o.V + 1))
+    ref[:, : o.V] = x[:, : o.V].astype(np.float64) + lam * s64 - lam_ilm * ilm.astype(np.float64)
+    ref[:, o.V] = x[:, o.V] + lam * f64
+    tok, _, _ = o.fused_step_ilm(AED, x, st, ilm, lam_ilm, lam=lam)
+    ok = _margin_ok(ref)
+    assert ok.sum() > 0.9 * B
+    assert np.array_equal(tok[ok], np.argmax(ref, axis=1)[ok])
+    # the ILM term changes decisions at this weight (the pin means something)
+    tok0, _, _ = o.fused_step(AED, x, st, lam=lam)
+    assert (tok0 != tok).any()
+
+
+def test_ilm_cancels_lm(tri):
+    """ilm = the LM row and lam_ilm = lam: the terms cancel, so the
+    decisions are the raw argmax wherever the margin is clear."""
+    o, f = tri
+    B = 300
+    x = synth.rnnt_logits(B, 1, o.V, seed=37)[0]
+    st = synth.uniform_states(o.num_states, B, seed=38)
+    s32, _, _, _ = o.rows(st, want64=False)
+    tok, _, _ = o.fused_step_ilm(RNNT, x, st, s32, 2.0, lam=2.0)
+    raw = x.astype(np.float64)
+    ok = _margin_ok(raw[:, : o.V], 1e-4) & (np.argmax(raw, axis=1) != o.V)
+    assert np.array_equal(tok[ok], np.argmax(raw[:, : o.V], axis=1)[ok])
+
+
+def test_topk_special_cases(tri):
+    o, f = tri
+    B, k = 50, 9
+    x = synth.rnnt_logits(B, 1, o.V, seed=39)[0]
+    x[::5, 7] = x[::5, 3]                    # exact ties: the lower column first
+    st = synth.uniform_states(o.num_states, B, seed=40)
+    # lambda = 0: numpy's stable descending sort of the logits
+    sc, cols, nx = o.topk(x, st, k, lam=0.0)
+    order = np.argsort(-x, axis=1, kind="stable")[:, :k]
+    assert np.array_equal(cols, order)
+    assert np.array_equal(sc, np.take_along_axis(x, order, 1))
+    # candidates' next states: the LM row's next ids (eos keeps the state)
+    _, _, n_o, _ = o.rows(st, want64=False)
+    for b in range(B):
+        for c, s in zip(cols[b], nx[b]):
+            assert s == (st[b] if c == o.V else n_o[b, c])
+    # k = 1 is the AED fused greedy decision
+    sc1, cols1, _ = o.topk(x, st, 1, lam=1.3)
+    tok, _, _ = o.fused_step(AED, x, st, lam=1.3)
+    assert np.array_equal(cols1[:, 0], tok)
+    # values: the float64 definition within the f32 bound; descending order
+    sc, cols, _ = o.topk(x, st, k, lam=1.3)
+    _, s64, _, _ = o.rows(st)
+    _, f64 = o.finals(st)
+    full = np.concatenate([s64, f64[:, None]], 1)
+    ref = np.take_along_axis(x.astype(np.float64), cols, 1) + 1.3 * np.take_along_axis(full, cols, 1)
+    assert np.max(np.abs(sc - ref)) < 1e-4
+    assert (np.diff(sc, axis=1) <= 0).all()
+    # more candidates than columns: the tail is empty
+    sc, cols, nx = o.topk(x[:2], st[:2], o.V + 4, lam=0.5)
+    assert (cols[:, o.V + 1:] == -1).all() and np.isneginf(sc[:, o.V + 1:]).all()
