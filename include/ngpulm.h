@@ -91,6 +91,25 @@ typedef struct {
 int ngpulm_load_arpa(const char* arpa_path, const char* vocab_path, int32_t vocab_size,
                      int32_t cuda_device, ngpulm_model** out);
 
+/* NGLM binary model files (format SPEC.md:209: "NGLM" magic,
+ * u32 version = 1, u32 order, u32 vocab_size, u32 num_states, u64 num_arcs,
+ * u32 root_state, u32 bos_state, then arc_tokens u32[A], arc_weights f32[A],
+ * arc_to_states u32[A], start_arcs u64[S], end_arcs u64[S], boff_weights
+ * f32[S], boff_to_states u32[S], final_weights f32[S], and a trailing CRC-32
+ * (IEEE) of all preceding bytes; little-endian).
+ * ngpulm_save writes the model's host arrays (synchronous; EIO on a write
+ * failure). ngpulm_load_binary reads such a file and builds/uploads the model
+ * exactly as ngpulm_load_arpa would from the ARPA it came from (arrays
+ * bit-identical, hence bit-identical query results), without parsing text.
+ * Errors: EIO (cannot read), EDOMAIN with a message naming the failure: "bad
+ * magic", "unsupported version", "truncated header"/"truncated payload",
+ * "checksum mismatch", or an inconsistent array. info.num_unk_filled is
+ * recomputed from the root arcs for order >= 2 (else -1); info.num_dropped
+ * is -1 (not stored). The vocabulary strings are not stored: token ids are
+ * the file's ids. */
+int ngpulm_save(const ngpulm_model* model, const char* path);
+int ngpulm_load_binary(const char* path, int32_t cuda_device, ngpulm_model** out);
+
 /* Copy an existing model's arrays to another device without re-parsing
  * (one replica per GPU for multi-GPU sharding). */
 int ngpulm_replicate(const ngpulm_model* src, int32_t cuda_device, ngpulm_model** out);

@@ -52,6 +52,8 @@ _P, _I32, _I64, _F = C.c_void_p, C.c_int32, C.c_int64, C.c_float
 SIGNATURES = {
     "ngpulm_load_arpa": (C.c_int, [C.c_char_p, C.c_char_p, _I32, _I32, C.POINTER(_P)]),
     "ngpulm_replicate": (C.c_int, [_P, _I32, C.POINTER(_P)]),
+    "ngpulm_save": (C.c_int, [_P, C.c_char_p]),
+    "ngpulm_load_binary": (C.c_int, [C.c_char_p, _I32, C.POINTER(_P)]),
     "ngpulm_free": (None, [_P]),
     "ngpulm_set_chain_mode": (C.c_int, [_P, _I32]),
     "ngpulm_set_advance_kernel": (C.c_int, [_P, _I32]),
@@ -148,6 +150,10 @@ class NgpuLM:
         ADVANCE_WARP (one warp per row, three arc arrays) or ADVANCE_CTA (one CTA per row)."""
         _check(lib().ngpulm_set_advance_kernel(self._h, kind))
         self.info.advance_kernel = kind
+
+    def save(self, path: str) -> None:
+        """ngpulm_save: NGLM binary file (SPEC.md:209 format)."""
+        _check(lib().ngpulm_save(self._h, path.encode()))
 
     def replicate(self, device: int) -> "NgpuLM":
         out = C.c_void_p()
@@ -341,6 +347,16 @@ def load_arpa(arpa_path: str, vocab_path: str | None = None, vocab_size: int = 0
     return NgpuLM(out.value)
 
 
+def load_binary(path: str, device: int | None = None) -> NgpuLM:
+    """ngpulm_load_binary. device=None -> torch's current device; -1 -> host-only model."""
+    if device is None:
+        import torch
+        device = torch.cuda.current_device()
+    out = C.c_void_p()
+    _check(lib().ngpulm_load_binary(path.encode(), device, C.byref(out)))
+    return NgpuLM(out.value)
+
+
 # C-ABI names, for callers that mirror include/ngpulm.h
 ngpulm_load_arpa = load_arpa
 ngpulm_advance = NgpuLM.advance
@@ -350,6 +366,8 @@ ngpulm_check = NgpuLM.check
 ngpulm_ctc_greedy_decode = NgpuLM.ctc_greedy_decode
 ngpulm_fused_greedy_step_ilm = NgpuLM.fused_greedy_step_ilm
 ngpulm_fused_topk = NgpuLM.fused_topk
+ngpulm_save = NgpuLM.save
+ngpulm_load_binary = load_binary
 ngpulm_replicate = NgpuLM.replicate
 ngpulm_set_chain_mode = NgpuLM.set_chain_mode
 ngpulm_set_advance_kernel = NgpuLM.set_advance_kernel

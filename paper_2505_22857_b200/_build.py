@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libngpulm.so")
-SOURCES = ["kernels.cu", "capi.cpp", "build.cpp"]
+SOURCES = ["kernels.cu", "capi.cpp", "build.cpp", "nglm.cpp"]
 HEADERS = ["ngpulm_internal.h", os.path.join("..", "..", "include", "ngpulm.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -475,4 +475,38 @@ void build_chain_table(const HostModel& m, const std::vector<int32_t>& arc_begin
   }
 }
 
+// The context trie's prefix edges (state_of) from the flat arrays alone, for
+// models loaded from NGLM files: state ids are ordered by context length
+// (R6), so walking states in id order, an arc (s, v) whose target has no
+// length yet reaches the state of context(s)+v — its child (a target of
+// length <= |context(s)| was reached before). <s> is the root's child V.
+bool rebuild_child_map(HostModel& m, std::string& err) {
+  const int32_t S = m.num_states, V = m.V;
+  std::vector<int32_t> len((size_t)S, -1);
+  m.child_keys.clear();
+  m.child_vals.clear();
+  m.child_mask = 0;
+  len[0] = 0;
+  if (m.bos_state != 0) {
+    len[(size_t)m.bos_state] = 1;
+    child_insert(m, ckey(0, V), m.bos_state);
+  }
+  for (int32_t s = 0; s < S; ++s) {
+    if (len[(size_t)s] < 0) { err = "state " + std::to_string(s) + " is not reachable by a prefix arc"; return false; }
+    for (int32_t a = m.arc_off[s]; a < m.arc_off[s + 1]; ++a) {
+      const int32_t t = m.arc_to[a];
+      if (t != 0 && len[(size_t)t] < 0) {
+        len[(size_t)t] = len[(size_t)s] + 1;
+        child_insert(m, ckey(s, m.arc_tok[a]), t);
+      }
+    }
+  }
+  if (m.order >= 2) {  // root arcs that fall back to the root: tokens without a unigram (R2)
+    int64_t M = 0;
+    for (int32_t v = 0; v < V; ++v) M += m.arc_to[v] == 0;
+    m.num_unk_filled = M;
+  }
+  return true;
+}
+
 }  // namespace ngpulm

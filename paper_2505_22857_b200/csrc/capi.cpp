@@ -166,6 +166,31 @@ int ngpulm_load_arpa(const char* arpa_path, const char* vocab_path, int32_t voca
   return NGPULM_OK;
 }
 
+int ngpulm_save(const ngpulm_model* m, const char* path) {
+  if (!m || !path) return err(NGPULM_EUSAGE, "NULL argument");
+  std::string e;
+  int r = ngpulm::save_binary(m->h, path, e);
+  return r == NGPULM_OK ? r : err(r, e);
+}
+
+int ngpulm_load_binary(const char* path, int32_t cuda_device, ngpulm_model** out) {
+  if (!path || !out) return err(NGPULM_EUSAGE, "NULL argument");
+  *out = nullptr;
+  std::unique_ptr<ngpulm_model> m(new (std::nothrow) ngpulm_model());
+  if (!m) return err(NGPULM_EUSAGE, "out of host memory");
+  std::string e;
+  int r = ngpulm::load_binary(path, m->h, e);
+  if (r != NGPULM_OK) return err(r, e);
+  if (cuda_device >= 0) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || cuda_device >= n) return err(NGPULM_EUSAGE, "no such CUDA device");
+    r = upload(m.get(), cuda_device);
+    if (r != NGPULM_OK) return r;
+  }
+  *out = m.release();
+  return NGPULM_OK;
+}
+
 int ngpulm_replicate(const ngpulm_model* src, int32_t cuda_device, ngpulm_model** out) {
   if (!src || !out || cuda_device < 0) return err(NGPULM_EUSAGE, "bad argument");
   *out = nullptr;

@@ -38,6 +38,12 @@ struct HostModel {
 int build_from_arpa(const char* arpa_path, const char* vocab_path, int32_t vocab_size,
                     HostModel& out, std::string& err);
 
+// NGLM binary files (nglm.cpp) and the prefix-edge map
+// rebuilt from the flat arrays (build.cpp).
+int save_binary(const HostModel& m, const char* path, std::string& err);
+int load_binary(const char* path, HostModel& m, std::string& err);
+bool rebuild_child_map(HostModel& m, std::string& err);
+
 // Device arc layout: state s's arcs start at
 // arc_begin[s], a multiple of 4 (one 16-byte quad); the gap before the next
 // state repeats the state's last arc, so a whole quad can be written into a

@@ -285,3 +285,19 @@ def test_fused_invalid_state(pairs):
     x = synth.rnnt_logits(3, 1, o.V, seed=1)[0]
     tg, sg, pg = gpu_step(m, CTC, x, [1, o.num_states, 2], [-1, -1, -1], None, 0.5)
     assert tg[1] == -1 and sg[1] == o.num_states and m.check() == 1
+
+
+def test_binary_model_same_results(lm6, tmp_path):
+    """A model reloaded from its NGLM file answers bit-identically."""
+    m, o, f = lm6
+    p = str(tmp_path / "lm6.nglm")
+    m.save(p)
+    r = ng.load_binary(p, device=0)
+    states, _ = trajectory_states(m, f, 1024, seed=61)
+    a, b = gpu_advance(m, states), gpu_advance(r, states)
+    assert same_bits(a[0], b[0]) and np.array_equal(a[1], b[1]) and same_bits(a[2], b[2])
+    x = synth.rnnt_logits(256, 1, m.V, seed=62)[0]
+    for mode in (CTC, RNNT, AED):
+        g = [gpu_step(mm, mode, x, states[:256], np.full(256, -1, np.int32) if mode == CTC else None, None, 0.4)
+             for mm in (m, r)]
+        assert all(np.array_equal(g[0][i], g[1][i]) for i in range(2))
