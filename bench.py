@@ -451,6 +451,26 @@ def bench_fused(m, f, dev, stream, rank):
                     m.fused_topk(xs[k % NB], st, 4, lam=0.3, stream=stream)
             ms = _graph_time(loop_topk, stream, dev, reps=5, reset=lambda: None)
             out[f"aed_topk4_b{Bt}_us_per_call"] = ms * 1e3 / nsteps
+    # --- label-looping transducer decode (f2): B=512 utterances of 100 frames, synthetic joint
+    from paper_2505_22857_b200.decode import TransducerGreedyDecoder
+    Bl = 512
+    lengths = torch.full((Bl,), 100, dtype=torch.int32, device=dev)
+    dec = None
+
+    def joint(frame, u, last, outl):
+        synth.joint_gpu(5 + rank, frame, u, last, outl, temperature=8.0, blank=V, blank_bias=0.75, stream=dec.stream)
+    dec = TransducerGreedyDecoder(m, joint, Bl, 100, lam=0.3)
+    dec(lengths)  # capture + warm-up
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = dec(lengths)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    out["rnnt_label_loop_b512_t100_ms"] = ms
+    out["rnnt_label_loop_iterations"] = res.iterations
+    out["rnnt_label_loop_us_per_iteration"] = ms * 1e3 / max(1, res.iterations)
+    out["rnnt_label_loop_labels"] = int(res.emit_len.sum().item())
     return out
 
 

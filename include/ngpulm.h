@@ -205,6 +205,33 @@ int ngpulm_fused_greedy_step_ilm(const ngpulm_model* model, int32_t mode, const 
                                  int64_t ilm_stride, float lambda_ilm, int32_t* tokens_out,
                                  ngpulm_stream stream);
 
+/* One iteration of batched label-looping greedy transducer decoding with
+ * fusion. Each row
+ * carries a loop state (frame_idx, sym_count, emit_len, last_token); the
+ * caller's joint network produces row b's logits for (frame_idx[b],
+ * u = emit_len[b], last_token[b]) before each call. A row is active while
+ * frame_idx[b] < lengths[b]; for an active row the call makes the RNN-T
+ * two-stage decision of ngpulm_fused_greedy_step (with the ILM term when ilm
+ * != NULL, as ngpulm_fused_greedy_step_ilm), then:
+ *   blank        -> frame_idx += 1, sym_count = 0;
+ *   a label (col)-> emit_out[b*max_len + emit_len[b]] = col (if emit_len[b] <
+ *                   max_len), emit_len += 1, last_token = its LM token,
+ *                   states[b] = next state, sym_count += 1, and when sym_count
+ *                   reaches max_symbols: frame_idx += 1, sym_count = 0.
+ * tokens_out[b] = the selected column (-1 for inactive rows). Iterating until
+ * no row is active reproduces, row by row, the frame-by-frame greedy loop
+ * with at most max_symbols labels per frame. An invalid state sets the
+ * bad-row word and ends the row (frame_idx = lengths[b]); an all-NaN logits
+ * row counts as blank. All buffers dev int32 [B] except emit_out [B, max_len]
+ * and logits (row stride row_stride, V+1 columns, R19); last_token may be
+ * NULL. Needs V % 4 == 0 and V <= 1024. Graph-capturable. */
+int ngpulm_transducer_loop_step(const ngpulm_model* model, const float* logits, int64_t row_stride,
+                                int32_t B, int32_t* states, int32_t* frame_idx, int32_t* sym_count,
+                                const int32_t* lengths, int32_t max_symbols, float lambda,
+                                int32_t blank_id, const float* ilm, int64_t ilm_stride, float lambda_ilm,
+                                int32_t* tokens_out, int32_t* emit_out, int32_t* emit_len,
+                                int32_t* last_token, int32_t max_len, ngpulm_stream stream);
+
 /* The k best fused expansions of each row, for AED beam search with NGPU-LM
  * shallow fusion. Fused value of a
  * token column: fmaf(lambda, lm, asr) [then fmaf(-lambda_ilm, ilm[v], .) when

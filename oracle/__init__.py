@@ -59,6 +59,8 @@ def lib():
                                             C.c_int32, f32p, C.c_int64, C.c_float, i32p, C.c_int]
         L.oracle_topk.argtypes = [P, f32p, C.c_int64, C.c_int64, i32p, P, C.c_int64, C.c_float, C.c_float,
                                   C.c_int32, C.c_int32, f32p, i32p, i32p, C.c_int]
+        L.oracle_transducer_decode.argtypes = [P, C.c_uint64, C.c_float, C.c_float, i32p, C.c_int64, i32p, C.c_float,
+                                               C.c_int32, C.c_int32, C.c_int32, P, C.c_float, i32p, i32p, C.c_int]
         L.oracle_ctc_decode.argtypes = [P, f32p, C.c_int64, C.c_int64, C.c_int64, C.c_int32, P, i32p, i32p,
                                         C.c_float, C.c_int32, i32p, i32p, i32p, C.c_int]
         _lib = L
@@ -182,3 +184,23 @@ class Oracle:
         lib().oracle_topk(self.h, x, x.shape[1], n, st, _ptr(a), 0 if a is None else a.shape[1], float(lam),
                           float(lam_ilm), int(eos), int(k), sc, cols, nx, nthreads)
         return sc, cols, nx
+
+    def transducer_decode(self, seed: int, lengths, states, lam: float = 0.3, blank_id: int | None = None,
+                          max_symbols: int = 10, max_len: int = 0, temperature: float = 8.0, ilm=None,
+                          lam_ilm: float = 0.0, blank_bias: float = 0.0, nthreads: int = 0):
+        """SPEC.md:317-325 greedy transducer loop over the synthetic joint (synth/joint.cu twin).
+        ilm: optional [n, V] per-utterance ILM row (constant over steps). Returns (emitted [n, max_len],
+        emit_len [n], states)."""
+        ln = np.ascontiguousarray(lengths, dtype=np.int32)
+        n = ln.size
+        st = np.array(states, dtype=np.int32, copy=True).reshape(n)
+        max_len = max_len or int(ln.max(initial=0)) * max_symbols
+        em = np.full((n, max(1, max_len)), -1, dtype=np.int32)
+        el = np.empty(n, dtype=np.int32)
+        a = None if ilm is None else np.ascontiguousarray(ilm, dtype=np.float32)
+        blank = self.V if blank_id is None else blank_id
+        lib().oracle_transducer_decode(self.h, seed & ((1 << 64) - 1), float(temperature), float(blank_bias), ln, n,
+                                       st, float(lam),
+                                       int(blank), int(max_symbols), int(max_len), _ptr(a), float(lam_ilm),
+                                       em, el, nthreads)
+        return em[:, :max_len], el, st

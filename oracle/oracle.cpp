@@ -461,6 +461,59 @@ void oracle_topk(void* h, const float* logits, int64_t row_stride, int64_t n, co
   });
 }
 
+// The synthetic joint (test input, not the method; the oracle's own copy of
+// the counter-based generator of synth/joint.cu).
+static uint64_t smix(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static void joint_row(uint64_t seed, int32_t t, int32_t u, int32_t last, int32_t ncols, int32_t blank, float bias,
+                      float temp, float* out) {
+  uint64_t h = seed;
+  h = smix(h ^ (uint64_t)(int64_t)t);
+  h = smix(h ^ (uint64_t)(int64_t)u);
+  h = smix(h ^ (uint64_t)(int64_t)(last + 1));
+  for (int32_t v = 0; v < ncols; ++v) {
+    float x = (float)(smix(h ^ (uint64_t)v) >> 40) * 5.9604644775390625e-08f;
+    if (v == blank) x = x + bias;
+    out[v] = x * temp;
+  }
+}
+
+// Greedy transducer decoding with fusion (SPEC.md:317-325
+// transducer_greedy_fused): per utterance, frame loop t <
+// lengths[i]; on each frame up to max_sym labels: the joint row for (t, u,
+// last) -> the two-stage fused step; blank -> next frame; else emit (u += 1,
+// last = the label's LM token, LM state advanced). emitted [n, max_len]
+// (columns; emissions past max_len are counted, not stored), emit_len [n],
+// states in/out.
+void oracle_transducer_decode(void* h, uint64_t seed, float temp, float blank_bias, const int32_t* lengths, int64_t n,
+                              int32_t* states, float lambda, int32_t blank_id, int32_t max_sym, int32_t max_len,
+                              const float* ilm_rows, float lam_ilm, int32_t* emitted, int32_t* emit_len,
+                              int nthreads) {
+  auto* o = (Oracle*)h;
+  const int32_t ncols = o->V + 1;
+  parallel_rows(n, nthreads, [&](int64_t i) {
+    std::vector<float> row(ncols);
+    int32_t u = 0, last = -1;
+    for (int32_t t = 0; t < lengths[i]; ++t) {
+      for (int32_t k = 0; k < max_sym; ++k) {
+        joint_row(seed, t, u, last, ncols, blank_id, blank_bias, temp, row.data());
+        int32_t tok = -1, dummy = -1;
+        o->fused_step(1, row.data(), blank_id, lambda, &states[i], &dummy, &tok,
+                      ilm_rows ? ilm_rows + (size_t)i * o->V : nullptr, lam_ilm);
+        if (tok == blank_id) break;  // "If blank is predicted, we retain it": next frame
+        if (u < max_len) emitted[i * max_len + u] = tok;
+        ++u;
+        last = o->tok_of(tok, blank_id);
+      }
+    }
+    emit_len[i] = u;
+  });
+}
+
 // Greedy CTC decoding of whole utterances (SPEC.md:307-316 ctc_greedy_fused;
 // PAPER.md:138-139): for t = 0..T-1, frame t of row i (logits + i*row_stride +
 // t*frame_stride) gets one fused CTC step while t < lengths[i] (NULL: T).

@@ -66,6 +66,8 @@ SIGNATURES = {
     "ngpulm_fused_greedy_step": (C.c_int, [_P, _I32, _P, _I64, _I32, _P, _P, _P, _F, _I32, _P, _P]),
     "ngpulm_fused_greedy_step_ilm": (C.c_int, [_P, _I32, _P, _I64, _I32, _P, _P, _P, _F, _I32, _P, _I64, _F, _P,
                                                 _P]),
+    "ngpulm_transducer_loop_step": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _P, _P, _I32, _F, _I32, _P, _I64, _F,
+                                               _P, _P, _P, _P, _I32, _P]),
     "ngpulm_fused_topk": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _I64, _F, _F, _I32, _I32, _P, _P, _P, _P]),
     "ngpulm_ctc_greedy_decode": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _F, _I32, _P, _P, _P,
                                             _P]),
@@ -268,6 +270,32 @@ class NgpuLM:
             _dev_ptr(tokens_out, torch.int32, "tokens_out", B), _stream(stream)))
         return tokens_out
 
+    def transducer_loop_step(self, logits, states, frame_idx, sym_count, lengths, emit_out, emit_len,
+                             last_token=None, lam: float = 0.3, blank_id: int | None = None,
+                             max_symbols: int = 10, ilm=None, lam_ilm: float = 0.0, tokens_out=None,
+                             stream=None):
+        """ngpulm_transducer_loop_step: one label-looping iteration over B rows (all int32 [B]
+        CUDA tensors updated in place; emit_out [B, max_len])."""
+        import torch
+        B = states.numel()
+        if logits.dtype != torch.float32 or not logits.is_cuda or logits.dim() != 2 or logits.stride(1) != 1:
+            raise TypeError("logits: expected a [B, V+1] CUDA float32 tensor with contiguous rows")
+        if tokens_out is None:
+            tokens_out = torch.empty(B, dtype=torch.int32, device=states.device)
+        max_len = emit_out.shape[1] if emit_out.dim() == 2 else 0
+        blank = self.V if blank_id is None else blank_id
+        _check(lib().ngpulm_transducer_loop_step(
+            self._h, logits.data_ptr(), logits.stride(0), B, _dev_ptr(states, torch.int32, "states", B),
+            _dev_ptr(frame_idx, torch.int32, "frame_idx", B), _dev_ptr(sym_count, torch.int32, "sym_count", B),
+            _dev_ptr(lengths, torch.int32, "lengths", B), int(max_symbols), float(lam), blank,
+            ilm.data_ptr() if ilm is not None else None, ilm.stride(0) if ilm is not None else 0,
+            float(lam_ilm), _dev_ptr(tokens_out, torch.int32, "tokens_out", B),
+            _dev_ptr(emit_out, torch.int32, "emit_out", B * max_len) if max_len else None,
+            _dev_ptr(emit_len, torch.int32, "emit_len", B),
+            _dev_ptr(last_token, torch.int32, "last_token", B) if last_token is not None else None,
+            max_len, _stream(stream)))
+        return tokens_out
+
     def fused_topk(self, logits, states, k: int, lam: float = 0.3, eos_id: int | None = None, ilm=None,
                    lam_ilm: float = 0.0, want_next: bool = True, stream=None):
         """ngpulm_fused_topk -> (scores [B,k] f32, cols [B,k] i32, next [B,k] i32 or None)."""
@@ -367,6 +395,7 @@ ngpulm_ctc_greedy_decode = NgpuLM.ctc_greedy_decode
 ngpulm_fused_greedy_step_ilm = NgpuLM.fused_greedy_step_ilm
 ngpulm_fused_topk = NgpuLM.fused_topk
 ngpulm_save = NgpuLM.save
+ngpulm_transducer_loop_step = NgpuLM.transducer_loop_step
 ngpulm_load_binary = load_binary
 ngpulm_replicate = NgpuLM.replicate
 ngpulm_set_chain_mode = NgpuLM.set_chain_mode

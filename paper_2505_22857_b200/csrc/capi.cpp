@@ -340,6 +340,28 @@ int ngpulm_fused_greedy_step_ilm(const ngpulm_model* m, int32_t mode, const floa
   return NGPULM_OK;
 }
 
+int ngpulm_transducer_loop_step(const ngpulm_model* m, const float* logits, int64_t row_stride, int32_t B,
+                                int32_t* states, int32_t* frame_idx, int32_t* sym_count, const int32_t* lengths,
+                                int32_t max_symbols, float lambda, int32_t blank_id, const float* ilm,
+                                int64_t ilm_stride, float lambda_ilm, int32_t* tokens_out, int32_t* emit_out,
+                                int32_t* emit_len, int32_t* last_token, int32_t max_len, ngpulm_stream stream) {
+  if (int r = check_hot(m, B)) return r;
+  if (blank_id < 0 || blank_id > m->h.V) return err(NGPULM_EUSAGE, "blank_id outside [0, V]");
+  if (max_symbols < 1 || max_len < 0) return err(NGPULM_EUSAGE, "max_symbols < 1 or max_len < 0");
+  if (m->h.V % 4 != 0 || m->h.V > 1024) return err(NGPULM_EUSAGE, "loop step needs V % 4 == 0 and V <= 1024");
+  if (B == 0) return NGPULM_OK;
+  if (!logits || !states || !frame_idx || !sym_count || !lengths || !tokens_out || !emit_len ||
+      (max_len > 0 && !emit_out))
+    return err(NGPULM_EUSAGE, "NULL device buffer");
+  if (B > 1 && row_stride < (int64_t)m->h.V + 1) return err(NGPULM_EUSAGE, "row_stride < V+1");
+  if (ilm && B > 1 && ilm_stride < (int64_t)m->h.V) return err(NGPULM_EUSAGE, "ilm_stride < V");
+  int e = ngpulm::launch_transducer_loop(m->dm, logits, row_stride, B, states, frame_idx, sym_count, lengths,
+                                         max_symbols, lambda, blank_id, ilm, ilm_stride, lambda_ilm, tokens_out,
+                                         emit_out, emit_len, last_token, max_len, stream);
+  if (e) return cuda_err((cudaError_t)e, "transducer loop step launch");
+  return NGPULM_OK;
+}
+
 int ngpulm_fused_topk(const ngpulm_model* m, const float* logits, int64_t row_stride, int32_t B,
                       const int32_t* states, const float* ilm, int64_t ilm_stride, float lambda, float lambda_ilm,
                       int32_t eos_id, int32_t k, float* topk_scores, int32_t* topk_cols, int32_t* topk_next,

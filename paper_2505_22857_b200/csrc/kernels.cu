@@ -1040,12 +1040,30 @@ __device__ __forceinline__ void edge_logits(const float* lrow, int32_t ncols, co
   if (c >= 0) const_cast<float*>(L.buf)[L.h + c] = __ldg(&lrow[c]);
 }
 
+// Transducer label-looping bookkeeping (
+// SPEC.md:317-325): with kMode == kLoop the fused step makes the RNN-T
+// two-stage decision for the rows whose frame index is inside their length,
+// then moves each row's loop state: blank -> next frame; a label -> emitted,
+// LM advance, one more symbol on this frame, and after max_sym symbols the
+// frame advances anyway.
+constexpr int kLoop = 3;
+struct Loop {
+  int32_t* frame;        // [B] current frame of the row
+  int32_t* sym;          // [B] symbols emitted on the current frame
+  const int32_t* len;    // [B] frames of the row
+  int32_t* emit;         // [B, max_len] emitted columns
+  int32_t* emit_len;     // [B] emissions so far (may exceed max_len: truncated)
+  int32_t* last;         // [B] last emitted LM token (-1 none), or nullptr
+  int32_t max_sym, max_len;
+};
+
 template <int kMode, bool kTable, bool kPacked, bool kAux>
 __global__ void __launch_bounds__(256, 1)
     fused_warp_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int32_t B,
                       int32_t* __restrict__ states, int32_t* __restrict__ prev, const uint8_t* __restrict__ active,
-                      float lambda, int32_t sp, AuxRow aux, int32_t* __restrict__ tokens_out) {
+                      float lambda, int32_t sp, AuxRow aux, Loop lp, int32_t* __restrict__ tokens_out) {
   constexpr int kW = 8;
+  constexpr bool kTwo = kMode == NGPULM_RNNT || kMode == kLoop;  // two-stage transducer selection
   extern __shared__ __align__(16) unsigned char smem[];
   const int32_t V = m.V, ncols = V + 1;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, R = blockDim.x >> 5;
@@ -1087,7 +1105,8 @@ __global__ void __launch_bounds__(256, 1)
       if (col < ncols && col != sp) ilm[j] = __ldg(arow + (col - (col > sp)));
     }
   }
-  const bool on = !active || __ldg(&active[row]);  // used only after the state and record loads are issued
+  // used only after the state and record loads are issued
+  const bool on = kMode == kLoop ? __ldg(&lp.frame[row]) < __ldg(&lp.len[row]) : (!active || __ldg(&active[row]));
   const int32_t pc = (kMode == NGPULM_CTC) ? __ldg(&prev[row]) : -2;
   WLevel lv;
   int32_t nslots;
@@ -1103,6 +1122,7 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       tokens_out[row] = -1;
       if (on) atomicMin(m.bad_row, (unsigned long long)row);
+      if (kMode == kLoop && on) lp.frame[row] = lp.len[row];  // an invalid state ends the row's loop
     }
     mbar_wait(s.bar, 0);  // no exit with a bulk copy in flight
     if (started) mbar_wait(lbar, 0);
@@ -1160,20 +1180,45 @@ __global__ void __launch_bounds__(256, 1)
     for (int j = 0; j < kMaxColsPerLane; ++j) {
       const int32_t col = lane + 32 * j;
       const float x = xs[j];
-      if (kMode == NGPULM_RNNT && (x > rv || (rc == INT_MAX && x == rv))) { rv = x; rc = col; }  // stage 1
+      if (kTwo && (x > rv || (rc == INT_MAX && x == rv))) { rv = x; rc = col; }  // stage 1
       float val = __fmaf_rn(lambda, col == sp ? sp_val : lm[j], x);  // asr + lambda * lm, one rounding
       if (kAux && col != sp) val = __fmaf_rn(-aux.lam, ilm[j], val);  // - lambda_ilm * ilm (R21)
       if (kMode == NGPULM_CTC && (col == sp || col == pc)) val = x;  // blank raw, repeated token not rescored
-      if (kMode == NGPULM_RNNT && col == sp) val = __int_as_float(0x7fc00000);  // stage 2: non-blank only
+      if (kTwo && col == sp) val = __int_as_float(0x7fc00000);  // stage 2: non-blank only
       if (val > bv || (bc == INT_MAX && val == bv)) { bv = val; bc = col; }
     }
   }
   warp_argmax(bv, bc);
-  if (kMode == NGPULM_RNNT) {
+  if (kTwo) {
     warp_argmax(rv, rc);
     if (rc == sp) bc = sp;  // stage 1 keeps blank: no LM advance
   }
   STAMP(7);
+  if (kMode == kLoop) {
+    if (lane == 0) {
+      const bool ok = bc >= 0 && bc < ncols;
+      tokens_out[row] = ok ? bc : -1;
+      int32_t fr = lp.frame[row], sy = lp.sym[row];
+      if (!ok || bc == sp) {  // blank (or an all-NaN row): next frame
+        ++fr;
+        sy = 0;
+      } else {  // a label: emit it, advance the LM, stay on the frame (up to max_sym symbols)
+        const int32_t tok = bc < sp ? bc : bc - 1;
+        const int32_t e = lp.emit_len[row];
+        if (e < lp.max_len) lp.emit[(size_t)row * lp.max_len + e] = bc;
+        lp.emit_len[row] = e + 1;
+        if (lp.last) lp.last[row] = tok;
+        states[row] = s.row_n[tok];
+        if (++sy >= lp.max_sym) {
+          ++fr;
+          sy = 0;
+        }
+      }
+      lp.frame[row] = fr;
+      lp.sym[row] = sy;
+    }
+    return;
+  }
   if (lane == 0) {
     if (bc < 0 || bc >= ncols) {
       tokens_out[row] = -1;  // all-NaN row (unspecified)
@@ -1741,9 +1786,9 @@ int launch_fused_mode(const DevModel& m, const float* logits, int64_t row_stride
     const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
 #define NGPULM_FUSED_LAUNCH(T, P)                                                                                 \
   return aux.p ? launch(fused_warp_kernel<kMode, T, P, true>, wg, wb, wsm, st, m, logits, row_stride, B, states,    \
-                        prev, active, lambda, blank, aux, tokens_out)                                               \
+                        prev, active, lambda, blank, aux, Loop{}, tokens_out)                                       \
                : launch(fused_warp_kernel<kMode, T, P, false>, wg, wb, wsm, st, m, logits, row_stride, B, states,   \
-                        prev, active, lambda, blank, aux, tokens_out)
+                        prev, active, lambda, blank, aux, Loop{}, tokens_out)
     if (table) { if (pk) NGPULM_FUSED_LAUNCH(true, true); NGPULM_FUSED_LAUNCH(true, false); }
     if (pk) NGPULM_FUSED_LAUNCH(false, true);
     NGPULM_FUSED_LAUNCH(false, false);
@@ -1796,6 +1841,31 @@ int launch_fused(const DevModel& m, int32_t mode, const float* logits, int64_t r
       return launch_fused_mode<NGPULM_AED>(m, logits, row_stride, B, states, prev, active, lambda, blank, ax,
                                            tokens_out, st);
   }
+}
+
+int launch_transducer_loop(const DevModel& m, const float* logits, int64_t row_stride, int32_t B, int32_t* states,
+                           int32_t* frame, int32_t* sym, const int32_t* lengths, int32_t max_sym, float lambda,
+                           int32_t blank, const float* aux, int64_t aux_stride, float lambda_ilm,
+                           int32_t* tokens_out, int32_t* emit, int32_t* emit_len, int32_t* last, int32_t max_len,
+                           void* stream) {
+  if (m.V % 4 != 0 || m.V > 1024) return (int)cudaErrorNotSupported;
+  int R = (B + 147) / 148;
+  R = R < 1 ? 1 : (R > 8 ? 8 : R);
+  const size_t wsm = (size_t)R * fslice_bytes(m.V, m.order);
+  const dim3 wg((B + R - 1) / R), wb(32 * R);
+  const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
+  const AuxRow ax{aux, aux_stride, lambda_ilm};
+  const Loop lp{frame, sym, lengths, emit, emit_len, last, max_sym, max_len};
+  cudaStream_t st = (cudaStream_t)stream;
+#define NGPULM_LOOP_LAUNCH(T, P)                                                                                     \
+  return aux ? launch(fused_warp_kernel<kLoop, T, P, true>, wg, wb, wsm, st, m, logits, row_stride, B, states,       \
+                      (int32_t*)nullptr, (const uint8_t*)nullptr, lambda, blank, ax, lp, tokens_out)                 \
+             : launch(fused_warp_kernel<kLoop, T, P, false>, wg, wb, wsm, st, m, logits, row_stride, B, states,      \
+                      (int32_t*)nullptr, (const uint8_t*)nullptr, lambda, blank, ax, lp, tokens_out)
+  if (table) { if (pk) NGPULM_LOOP_LAUNCH(true, true); NGPULM_LOOP_LAUNCH(true, false); }
+  if (pk) NGPULM_LOOP_LAUNCH(false, true);
+  NGPULM_LOOP_LAUNCH(false, false);
+#undef NGPULM_LOOP_LAUNCH
 }
 
 int launch_topk(const DevModel& m, const float* logits, int64_t row_stride, int32_t B, const int32_t* states,

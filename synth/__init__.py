@@ -27,6 +27,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LMGEN_SRC = os.path.join(HERE, "lmgen.cpp")
 LMGEN_BIN = os.path.join(HERE, "lmgen")
+JOINT_SRC = os.path.join(HERE, "joint.cu")
+JOINT_LIB = os.path.join(HERE, "libsynthjoint.so")
 
 
 def build_lmgen(force: bool = False) -> str:
@@ -241,3 +243,50 @@ def synthetic_scorer_row(seed: int, t: int, u: int, last: int, ncols: int,
     for v in range(ncols):
         vals[v] = (splitmix64(h ^ v) >> 11) * (1.0 / 9007199254740992.0)
     return _log_softmax64(vals * temperature).astype(np.float32)
+
+
+# ---------------------------------------------------------------- synthetic transducer joint (f2 driver input)
+def synthetic_joint_raw(seed: int, t: int, u: int, last: int, ncols: int, temperature: float = 8.0,
+                        blank: int = -1, blank_bias: float = 0.0) -> np.ndarray:
+    """CPU twin of synth/joint.cu: h = fold of (t, u, last+1) by splitmix64 (SPEC.md:348);
+    x[v] = float32((splitmix64(h ^ v) >> 40) * 2^-24), x[blank] += blank_bias (float32),
+    out = x * temperature; unnormalized scores."""
+    h = seed & _M64
+    for x in (t, u, last + 1):
+        h = splitmix64(h ^ (x & _M64))
+    r = np.array([splitmix64(h ^ v) >> 40 for v in range(ncols)], dtype=np.float64)
+    x = r.astype(np.float32) * np.float32(5.9604644775390625e-08)
+    if 0 <= blank < ncols:
+        x[blank] = np.float32(x[blank] + np.float32(blank_bias))
+    return x * np.float32(temperature)
+
+
+def build_joint(force: bool = False) -> str:
+    if force or not os.path.exists(JOINT_LIB) or os.path.getmtime(JOINT_LIB) < os.path.getmtime(JOINT_SRC):
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                               "-shared", "-Xcompiler", "-fPIC", "-o", JOINT_LIB, JOINT_SRC])
+    return JOINT_LIB
+
+
+_joint = None
+
+
+def joint_gpu(seed: int, frame, u, last, out, temperature: float = 8.0, blank: int = -1, blank_bias: float = 0.0,
+              stream=None):
+    """Fill out [B, ncols] (CUDA f32, contiguous rows) with the synthetic joint rows for
+    (frame[b], u[b], last[b]) (CUDA int32 [B]); graph-capturable."""
+    import ctypes as C
+    import torch
+    global _joint
+    if _joint is None:
+        L = C.CDLL(build_joint())
+        L.synth_joint.restype = C.c_int
+        L.synth_joint.argtypes = [C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                  C.c_float, C.c_float, C.c_void_p, C.c_int64, C.c_void_p]
+        _joint = L
+    st = (stream or torch.cuda.current_stream()).cuda_stream
+    rc = _joint.synth_joint(seed & _M64, out.shape[0], frame.data_ptr(), u.data_ptr(), last.data_ptr(),
+                            out.shape[1], int(blank), float(blank_bias), float(temperature), out.data_ptr(),
+                            out.stride(0), st)
+    if rc != 0:
+        raise RuntimeError(f"synth_joint: CUDA error {rc}")

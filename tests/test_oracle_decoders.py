@@ -285,3 +285,68 @@ def test_topk_special_cases(tri):
     # more candidates than columns: the tail is empty
     sc, cols, nx = o.topk(x[:2], st[:2], o.V + 4, lam=0.5)
     assert (cols[:, o.V + 1:] == -1).all() and np.isneginf(sc[:, o.V + 1:]).all()
+
+
+# ---------------------------------------------------------------- greedy transducer loop (f2)
+def _plain_transducer(seed, T, V, max_sym, temp=8.0, bias=0.0):
+    """Plain greedy transducer over the synthetic joint (numpy twin), no LM:
+    frame loop, <= max_sym labels per frame, raw argmax (first max) per row."""
+    out, u, last = [], 0, -1
+    for t in range(T):
+        for _ in range(max_sym):
+            row = synth.synthetic_joint_raw(seed, t, u, last, V + 1, temp, V, bias)
+            c = int(np.argmax(row))
+            if c == V:
+                break
+            out.append(c)
+            u += 1
+            last = c
+    return out
+
+
+def test_transducer_decode_lambda0_is_plain_greedy(tri):
+    """lambda = 0 -> the plain greedy transducer loop (here a numpy
+    simulator over the CPU twin of the synthetic joint)."""
+    o, f = tri
+    lengths = np.array([0, 1, 5, 12, 7], np.int32)
+    for max_sym, bias in ((1, 0.0), (3, 0.5), (10, 0.75)):
+        em, el, st = o.transducer_decode(1234, lengths, np.zeros(5, np.int32), lam=0.0, max_symbols=max_sym,
+                                         temperature=2.0, blank_bias=bias)
+        for b, T in enumerate(lengths):
+            ref = _plain_transducer(1234, int(T), o.V, max_sym, temp=2.0, bias=bias)
+            assert list(em[b, : el[b]]) == ref
+            # LM state = the emitted tokens replayed from the root (SPEC.md: LM-state consistency)
+            assert st[b] == o.state_of(False, [int(x) for x in ref])
+
+
+def test_transducer_decode_fused_float64_simulator(tri):
+    """lambda = 2: the decoded labels follow a float64 two-stage simulator (score64
+    rows, SPEC.md:325 'brute-force two-stage simulator run in 64-bit') for as long
+    as every stage-2 decision has a clear margin."""
+    o, f = tri
+    seed, T, lam, max_sym, temp = 77, 20, 2.0, 4, 2.0
+    em, el, st = o.transducer_decode(seed, np.array([T], np.int32), np.zeros(1, np.int32), lam=lam,
+                                     max_symbols=max_sym, temperature=temp, blank_bias=0.25)
+    got = list(em[0, : el[0]])
+    ref, u, last, s, checked = [], 0, -1, 0, 0
+    for t in range(T):
+        for _ in range(max_sym):
+            row = synth.synthetic_joint_raw(seed, t, u, last, o.V + 1, temp, o.V, 0.25).astype(np.float64)
+            if int(np.argmax(row)) == o.V:
+                break
+            _, s64, nx, _ = o.rows(np.array([s], np.int32))
+            fused = row[: o.V] + lam * s64[0]
+            srt = np.sort(fused)
+            if srt[-1] - srt[-2] < 1e-3:
+                break
+            c = int(np.argmax(fused))
+            ref.append(c)
+            checked += 1
+            s, u, last = int(nx[0, c]), u + 1, c
+        else:
+            continue
+        if checked and (srt[-1] - srt[-2] < 1e-3):
+            break
+    assert checked > 5 and got[: len(ref)] == ref
+    # the LM matters at this weight
+    assert got != _plain_transducer(seed, T, o.V, max_sym, temp, 0.25)
