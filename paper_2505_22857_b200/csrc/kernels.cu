@@ -433,6 +433,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #ifndef NGPULM_STORE_HINT
 #define NGPULM_STORE_HINT 1
 #endif
+#ifndef NGPULM_CTA_ROOT
+#define NGPULM_CTA_ROOT 1  // the 16-slot path (148 < B <= 1184): measured 3.74 -> 3.64 us at B = 1024
+#endif
+#ifndef NGPULM_WIDE_MAX_B
+#define NGPULM_WIDE_MAX_B (8 * 148)  // up to 8 rows per SM: 16-slot windows (measured)
+#endif
 
 __host__ __device__ constexpr size_t wrow_bytes(int32_t V) { return align16((size_t)V * 4 + 4); }  // + trash word
 // staged arcs: kStageQuads packed arc quads (32 bytes each)
@@ -710,16 +716,28 @@ __global__ void __launch_bounds__(256, 1)
   // step 0, on immutable model data, so before the wait: the root weights
   // once per CTA, and the root targets straight into every row's next-state
   // slots (the root has an arc for every token, [0, V)).
+  // kCtaRoot (register root): the root targets reach the CTA once (one bulk
+  // copy into the otherwise unused root-weight buffer) and every row copies
+  // them shared -> shared, so the 4 KB root level is read from L2 once per CTA
+  // instead of once per row (1024 rows reading the same 32 lines at once
+  // queue on their L2 slices).
+  constexpr bool kCtaRoot = kRegRoot && kW == 16 && !kStage && NGPULM_CTA_ROOT;
   if (lane == 0 && row < B) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(s.bar)) : "memory");
     if (kStage) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(s.abar)) : "memory");
-    if (w == 0 && !kRegRoot) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    if (w == 0 && (!kRegRoot || kCtaRoot))
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)), "r"(bytes) : "memory");
-    bulk_g2s(s.row_n, m.arc_to, bytes, s.bar);
-    if (w == 0 && !kRegRoot) {
+    if (!kCtaRoot) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)), "r"(bytes)
+                   : "memory");
+      bulk_g2s(s.row_n, m.arc_to, bytes, s.bar);
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(s.bar)) : "memory");  // unused phase
+    }
+    if (w == 0 && (!kRegRoot || kCtaRoot)) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-      bulk_g2s(const_cast<float*>(root_w), m.arc_w, bytes, bar);
+      bulk_g2s(const_cast<float*>(root_w), kCtaRoot ? static_cast<const void*>(m.arc_to) : m.arc_w, bytes, bar);
     }
   }
   float4 rw[kRegRoot ? 8 : 1];
@@ -729,7 +747,15 @@ __global__ void __launch_bounds__(256, 1)
     for (int j = 0; j < 8; ++j)
       if (lane + 32 * j < V / 4) rw[j] = __ldg(w4 + lane + 32 * j);
   }
-  if (!kRegRoot) __syncthreads();  // the CTA barrier's init visible to every warp
+  if (!kRegRoot || kCtaRoot) __syncthreads();  // the CTA barrier's init visible to every warp
+  if (kCtaRoot && row < B) {  // model data only: before the wait
+    mbar_wait(bar, 0);
+    const int4* src = reinterpret_cast<const int4*>(root_w);
+    int4* dst = reinterpret_cast<int4*>(s.row_n);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (lane + 32 * j < V / 4) dst[lane + 32 * j] = src[lane + 32 * j];
+  }
   pdl_wait();
   STAMP(2);
   if (row >= B) return;  // warp 0 always has a row and waits for the CTA's bulk copy
@@ -1009,35 +1035,62 @@ __host__ __device__ constexpr size_t fslice_bytes(int32_t V, int32_t order) {
   return wslice_bytes(V, order, 0) + align16((size_t)(V + 1) * 4 + 16);
 }
 
-struct LogitsRow {  // where column c of the row sits in shared memory: buf[h + c]
-  const float* buf;
-  int32_t h, head, tail;  // head/tail: columns [0, head) and [tail, ncols) not in the bulk copy
-};
-
-__device__ __forceinline__ LogitsRow start_logits(const float* lrow, int32_t ncols, float* buf, uint64_t* lbar) {
+// Issue frame row `lrow` (ncols floats) into `buf` (column c lands at
+// buf[h + c], h = (lrow & 15) / 4, so the interior copies 16-byte aligned).
+__device__ __forceinline__ void issue_frame(const float* lrow, int32_t ncols, float* buf, uint64_t* bar,
+                                            uint64_t pol) {
+  const int lane = threadIdx.x & 31;
   const uintptr_t src = reinterpret_cast<uintptr_t>(lrow);
   const uintptr_t lo = (src + 15) & ~(uintptr_t)15, hi = (src + (uintptr_t)ncols * 4) & ~(uintptr_t)15;
-  LogitsRow L;
-  L.buf = buf;
-  L.h = (int32_t)((src & 15) / 4);
+  const int32_t h = (int32_t)((src & 15) / 4);
   const bool bulk = hi > lo;
-  L.head = bulk ? (int32_t)((lo - src) / 4) : ncols;
-  L.tail = bulk ? (int32_t)((hi - src) / 4) : ncols;
-  if ((threadIdx.x & 31) == 0) {
-    const uint32_t bytes = bulk ? (uint32_t)(hi - lo) : 0u;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(lbar)), "r"(bytes) : "memory");
-    if (bulk) bulk_g2s(buf + L.h + L.head, reinterpret_cast<const void*>(lo), bytes, lbar);
+  const int32_t head = bulk ? (int32_t)((lo - src) / 4) : ncols, tail = bulk ? (int32_t)((hi - src) / 4) : ncols;
+  int32_t c = -1;
+  if (lane < head && lane < ncols) c = lane;
+  else if (lane >= 8 && lane - 8 < ncols - tail) c = tail + lane - 8;
+  if (c >= 0) {  // edge column: 4-byte async copy; the mbarrier's pending count covers it until it lands
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(buf + h + c)), "l"(lrow + c) : "memory");
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
   }
-  return L;
+  __syncwarp();
+  if (lane == 0) {
+    const uint32_t bytes = bulk ? (uint32_t)(hi - lo) : 0u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    if (bulk)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+              smem_u32(buf + h + head)),
+          "l"(lo), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+          : "memory");
+  }
 }
 
-// the columns outside the bulk copy: lanes 0..5 (<= 3 on each side)
-__device__ __forceinline__ void edge_logits(const float* lrow, int32_t ncols, const LogitsRow& L) {
+// Total order of floats as unsigned keys (larger float -> larger key).
+__device__ __forceinline__ uint32_t fkey(float v) {
+  const uint32_t u = __float_as_uint(v);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// Argmax over a row held in registers, lane i holding columns i + 32 j (R14):
+// the largest value (NaN never taken), then the lowest column holding it, by
+// two warp reductions. Returns INT_MAX when every value is NaN.
+__device__ __forceinline__ int32_t warp_argmax_cols(const float (&v)[kMaxColsPerLane]) {
   const int lane = threadIdx.x & 31;
-  int32_t c = -1;
-  if (lane < L.head) c = lane;
-  else if (lane >= 8 && lane - 8 < ncols - L.tail) c = L.tail + lane - 8;
-  if (c >= 0) const_cast<float*>(L.buf)[L.h + c] = __ldg(&lrow[c]);
+  float mx[kMaxColsPerLane];
+#pragma unroll
+  for (int j = 0; j < kMaxColsPerLane; ++j) mx[j] = v[j];
+#pragma unroll
+  for (int d = 1; d < kMaxColsPerLane; d *= 2)
+#pragma unroll
+    for (int j = 0; j + d < kMaxColsPerLane; j += 2 * d) mx[j] = fmaxf(mx[j], mx[j + d]);
+  const float lmax = mx[0] == mx[0] ? mx[0] : -INFINITY;
+  const uint32_t kmax = __reduce_max_sync(kFull, fkey(lmax));
+  const float M = __uint_as_float((kmax & 0x80000000u) ? (kmax ^ 0x80000000u) : ~kmax);
+  int32_t cm = INT_MAX;
+#pragma unroll
+  for (int j = kMaxColsPerLane - 1; j >= 0; --j)
+    if (v[j] == M) cm = lane + 32 * j;
+  return (int32_t)__reduce_min_sync(kFull, (uint32_t)cm);
 }
 
 // Transducer label-looping bookkeeping (
@@ -1110,13 +1163,15 @@ __global__ void __launch_bounds__(256, 1)
   const int32_t pc = (kMode == NGPULM_CTC) ? __ldg(&prev[row]) : -2;
   WLevel lv;
   int32_t nslots;
-  LogitsRow L{lbuf, 0, 0, 0};
   bool started = false;
-  auto begin_logits = [&]() {  // the logits' bulk copy, issued once the chain record is in flight
-    L = start_logits(lrow, ncols, lbuf, lbar);
+  auto begin_logits = [&]() {  // the logits' copy, issued once the chain record is in flight
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));  // read once
+    issue_frame(lrow, ncols, lbuf, lbar, pol);
     started = true;
   };
   const Row r = warp_row<kTable>(m, states + row, s, lv, nslots, begin_logits);
+  const float* lb = lbuf + (reinterpret_cast<uintptr_t>(lrow) & 15) / 4;  // column c at lb[c]
   STAMP(11);
   if (!on || r.bad) {  // inactive rows are untouched (their state is not even checked)
     if (lane == 0) {
@@ -1132,7 +1187,6 @@ __global__ void __launch_bounds__(256, 1)
   // logits — and is simply not used when blank wins)
   Window<kW, kPacked> a;
   load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
-  edge_logits(lrow, ncols, L);  // queued behind the gathers, needed last
   STAMP(3);
   {  // root scores: acc_root + root weight, while the gathers fly
     float4* s4 = reinterpret_cast<float4*>(s.row_s);
@@ -1161,37 +1215,39 @@ __global__ void __launch_bounds__(256, 1)
   __syncwarp();
   STAMP(12);
   // fused values and the row's argmax (R13, R14, R19):
-  // lane i takes columns i, i+32, ... (at most 33 at V <= 1024), all loads
-  // first. Within a lane the columns ascend, so a strict > keeps the lowest
-  // column on ties; the bc == INT_MAX clause takes a first -inf (R14), and a
-  // NaN is never taken (as in better()).
-  float bv = -INFINITY, rv = -INFINITY;
-  int32_t bc = INT_MAX, rc = INT_MAX;
+  // lane i takes columns i, i+32, ... (at most 33 at V <= 1024); two-pass warp
+  // argmax (warp_argmax_cols). Transducers: stage 1 = the raw argmax over all
+  // columns; blank is kept, else stage 2 = the fused argmax
+  // over the non-blank columns.
+  int32_t bc;
   {
-    float xs[kMaxColsPerLane], lm[kMaxColsPerLane];
+    float xs[kMaxColsPerLane];
 #pragma unroll
     for (int j = 0; j < kMaxColsPerLane; ++j) {
       const int32_t col = lane + 32 * j;
-      xs[j] = col < ncols ? L.buf[L.h + col] : __int_as_float(0x7fc00000);  // NaN: never taken
-      lm[j] = col < ncols ? s.row_s[col - (col > sp)] : 0.f;                   // col == sp: unused
+      xs[j] = __int_as_float(0x7fc00000);  // past the last column: NaN, never taken
+      if (col < ncols) xs[j] = lb[col];
     }
-    const float sp_val = (kMode == NGPULM_AED) ? r.fin : 0.f;  // eos <-> final (lambda * final + asr)
+    int32_t rc = 0;
+    if (kTwo) rc = warp_argmax_cols(xs);
+    if (kTwo && rc == sp) {
+      bc = sp;  // stage 1 keeps blank: no LM advance
+    } else {
+      const float sp_val = (kMode == NGPULM_AED) ? r.fin : 0.f;  // eos <-> final (lambda * final + asr)
+      float val[kMaxColsPerLane];
 #pragma unroll
-    for (int j = 0; j < kMaxColsPerLane; ++j) {
-      const int32_t col = lane + 32 * j;
-      const float x = xs[j];
-      if (kTwo && (x > rv || (rc == INT_MAX && x == rv))) { rv = x; rc = col; }  // stage 1
-      float val = __fmaf_rn(lambda, col == sp ? sp_val : lm[j], x);  // asr + lambda * lm, one rounding
-      if (kAux && col != sp) val = __fmaf_rn(-aux.lam, ilm[j], val);  // - lambda_ilm * ilm (R21)
-      if (kMode == NGPULM_CTC && (col == sp || col == pc)) val = x;  // blank raw, repeated token not rescored
-      if (kTwo && col == sp) val = __int_as_float(0x7fc00000);  // stage 2: non-blank only
-      if (val > bv || (bc == INT_MAX && val == bv)) { bv = val; bc = col; }
+      for (int j = 0; j < kMaxColsPerLane; ++j) {
+        const int32_t col = lane + 32 * j;
+        const float x = xs[j];
+        const float lmv = col < ncols && col != sp ? s.row_s[col - (col > sp)] : sp_val;
+        float v = __fmaf_rn(lambda, lmv, x);  // asr + lambda * lm, one rounding
+        if (kAux && col != sp) v = __fmaf_rn(-aux.lam, ilm[j], v);  // - lambda_ilm * ilm (R21)
+        if (kMode == NGPULM_CTC && (col == sp || col == pc)) v = x;  // blank raw, repeated token not rescored
+        if (kTwo && col == sp) v = __int_as_float(0x7fc00000);        // stage 2: non-blank only
+        val[j] = v;
+      }
+      bc = warp_argmax_cols(val);
     }
-  }
-  warp_argmax(bv, bc);
-  if (kTwo) {
-    warp_argmax(rv, rc);
-    if (rc == sp) bc = sp;  // stage 1 keeps blank: no LM advance
   }
   STAMP(7);
   if (kMode == kLoop) {
@@ -1234,12 +1290,6 @@ __global__ void __launch_bounds__(256, 1)
   }
   STAMP(8);
   if (w == 0) STAMPS_OUT(row);
-}
-
-// Total order of floats as unsigned keys (larger float -> larger key).
-__device__ __forceinline__ uint32_t fkey(float v) {
-  const uint32_t u = __float_as_uint(v);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
 // ---------------------------------------------------------------- fused top-k
@@ -1292,13 +1342,15 @@ __global__ void __launch_bounds__(256, 1)
   }
   WLevel lv;
   int32_t nslots;
-  LogitsRow L{lbuf, 0, 0, 0};
   bool started = false;
   auto begin_logits = [&]() {
-    L = start_logits(lrow, ncols, lbuf, lbar);
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    issue_frame(lrow, ncols, lbuf, lbar, pol);
     started = true;
   };
   const Row r = warp_row<kTable>(m, states + row, s, lv, nslots, begin_logits);
+  const float* lb = lbuf + (reinterpret_cast<uintptr_t>(lrow) & 15) / 4;  // column c at lb[c]
   float* osc = out_scores + (size_t)row * k;
   int32_t* ocol = out_cols + (size_t)row * k;
   int32_t* onx = out_next ? out_next + (size_t)row * k : nullptr;
@@ -1315,7 +1367,6 @@ __global__ void __launch_bounds__(256, 1)
   }
   Window<kW, kPacked> a;
   load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
-  edge_logits(lrow, ncols, L);
   {
     float4* s4 = reinterpret_cast<float4*>(s.row_s);
 #pragma unroll
@@ -1345,7 +1396,7 @@ __global__ void __launch_bounds__(256, 1)
     float x = __int_as_float(0x7fc00000);
     float v = x;
     if (col < ncols) {
-      x = L.buf[L.h + col];
+      x = lb[col];
       if (col == sp) {
         v = __fmaf_rn(lambda, r.fin, x);  // eos <-> final weight
       } else {
@@ -1356,29 +1407,19 @@ __global__ void __launch_bounds__(256, 1)
     val[j] = v;
   }
   for (int32_t i = 0; i < k; ++i) {
-    float mx[kMaxColsPerLane];
-#pragma unroll
-    for (int j = 0; j < kMaxColsPerLane; ++j) mx[j] = val[j];
-#pragma unroll
-    for (int d = 1; d < kMaxColsPerLane; d *= 2)
-#pragma unroll
-      for (int j = 0; j + d < kMaxColsPerLane; j += 2 * d) mx[j] = fmaxf(mx[j], mx[j + d]);
-    const float lmax = mx[0] == mx[0] ? mx[0] : -INFINITY;
-    const bool any = __any_sync(kFull, mx[0] == mx[0]);
-    if (!any) {  // fewer than k selectable (non-NaN) columns
+    const int32_t bc = warp_argmax_cols(val);
+    if (bc == INT_MAX) {  // fewer than k selectable (non-NaN) columns
       if (lane == 0) { osc[i] = -INFINITY; ocol[i] = -1; if (onx) onx[i] = -1; }
       continue;
     }
-    const uint32_t kmax = __reduce_max_sync(kFull, fkey(lmax));
-    const float M = __uint_as_float((kmax & 0x80000000u) ? (kmax ^ 0x80000000u) : ~kmax);
-    int32_t cm = INT_MAX;
-#pragma unroll
-    for (int j = kMaxColsPerLane - 1; j >= 0; --j)
-      if (val[j] == M) cm = lane + 32 * j;
-    const int32_t bc = (int32_t)__reduce_min_sync(kFull, (uint32_t)cm);
+    float mine = 0.f;
 #pragma unroll
     for (int j = 0; j < kMaxColsPerLane; ++j)
-      if (lane + 32 * j == bc) val[j] = __int_as_float(0x7fc00000);  // taken
+      if (lane + 32 * j == bc) {
+        mine = val[j];
+        val[j] = __int_as_float(0x7fc00000);  // taken
+      }
+    const float M = __shfl_sync(kFull, mine, bc & 31);
     if (lane == 0) {
       osc[i] = M;
       ocol[i] = bc;
@@ -1411,36 +1452,6 @@ __host__ __device__ constexpr size_t dslice_bytes(int32_t V, int32_t order, int 
 // CTA: root weights [V] | root targets [V] | mbarrier | R slices
 __host__ __device__ constexpr size_t dcta_smem(int32_t V, int32_t order, int R, int depth) {
   return 2 * align16((size_t)V * 4) + 16 + (size_t)R * dslice_bytes(V, order, depth);
-}
-
-// Issue frame row `lrow` (ncols floats) into `buf` (column c lands at
-// buf[h + c], h = (lrow & 15) / 4, so the interior copies 16-byte aligned).
-__device__ __forceinline__ void issue_frame(const float* lrow, int32_t ncols, float* buf, uint64_t* bar,
-                                            uint64_t pol) {
-  const int lane = threadIdx.x & 31;
-  const uintptr_t src = reinterpret_cast<uintptr_t>(lrow);
-  const uintptr_t lo = (src + 15) & ~(uintptr_t)15, hi = (src + (uintptr_t)ncols * 4) & ~(uintptr_t)15;
-  const int32_t h = (int32_t)((src & 15) / 4);
-  const bool bulk = hi > lo;
-  const int32_t head = bulk ? (int32_t)((lo - src) / 4) : ncols, tail = bulk ? (int32_t)((hi - src) / 4) : ncols;
-  int32_t c = -1;
-  if (lane < head && lane < ncols) c = lane;
-  else if (lane >= 8 && lane - 8 < ncols - tail) c = tail + lane - 8;
-  if (c >= 0) {  // edge column: 4-byte async copy; the mbarrier's pending count covers it until it lands
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(buf + h + c)), "l"(lrow + c) : "memory");
-    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-  }
-  __syncwarp();
-  if (lane == 0) {
-    const uint32_t bytes = bulk ? (uint32_t)(hi - lo) : 0u;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-    if (bulk)
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-              smem_u32(buf + h + head)),
-          "l"(lo), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-          : "memory");
-  }
 }
 
 // The row of state `st` into s.row_s / s.row_n (Algorithm 1, as in
@@ -1734,7 +1745,7 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
     // up to 8 rows per SM: 16-slot windows (almost every row in one window),
     // packed arcs bulk-copied into a staging area; more rows per SM: 8-slot
     // windows of direct gathers (registers and shared memory for occupancy)
-    const bool wide = B <= 8 * 148, pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO;
+    const bool wide = B <= NGPULM_WIDE_MAX_B, pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO;
     const bool small_v = m.V <= 1024, stage = B >= 2 && B <= NGPULM_STAGE_MAX_B && pk && small_v && table;
     const int sq = stage ? kStageQuads : 0;
     int R = (B + 147) / 148;
