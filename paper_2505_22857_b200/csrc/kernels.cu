@@ -1019,15 +1019,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 // arc loads queued behind them — except the <= 3 columns on each side of the
 // copy's 16-byte-aligned interior, which two lanes load directly. The fused
 // values are reduced with warp shuffles.
-__device__ __forceinline__ void warp_argmax(float& v, int32_t& c) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const float v2 = __shfl_xor_sync(kFull, v, o);
-    const int32_t c2 = __shfl_xor_sync(kFull, c, o);
-    if (better(v2, c2, v, c)) { v = v2; c = c2; }
-  }
-}
-
 constexpr int kMaxColsPerLane = 33;  // (1024 + 1 + 31) / 32
 
 // per warp: row_s | row_n | levels | 2 mbarriers | logits (V+1 floats + 16-byte slack)

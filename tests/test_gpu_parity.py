@@ -301,3 +301,18 @@ def test_binary_model_same_results(lm6, tmp_path):
         g = [gpu_step(mm, mode, x, states[:256], np.full(256, -1, np.int32) if mode == CTC else None, None, 0.4)
              for mm in (m, r)]
         assert all(np.array_equal(g[0][i], g[1][i]) for i in range(2))
+
+
+@pytest.mark.parametrize("B", [149, 600, 1036])
+@pytest.mark.parametrize("name", ["uni16", "bi16", "tiny3", "tri64", "five48", "ten24"])
+def test_mid_size_batches_full_rows(pairs, name, B):
+    """Batches between one row per SM and 7 per SM (the 16-slot warp kernel with the
+    CTA-shared root level) against the oracle: full rows of every batch row."""
+    m, o, _ = pairs[name]
+    assert m.info.num_states > 0
+    states = synth.uniform_states(o.num_states, B, seed=B)
+    s, n, f = gpu_advance(m, states)
+    uniq, inv = np.unique(states, return_inverse=True)
+    s32, _, n_o, _ = o.rows(uniq, want64=False)
+    f32, _ = o.finals(uniq)
+    assert np.array_equal(n, n_o[inv]) and same_bits(s, s32[inv]) and same_bits(f, f32[inv])
