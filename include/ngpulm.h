@@ -19,7 +19,9 @@
  *  - Return codes: NGPULM_OK, or
  *      NGPULM_EDOMAIN  invalid ARPA / vocabulary content (message names the line),
  *      NGPULM_EUSAGE   bad arguments (NULL, negative sizes, bad mode/blank id,
- *                      wrong current device, V beyond the kernels' limit),
+ *                      wrong current device, V beyond the kernels' limit:
+ *                      info.max_vocab for advance/final — vocabulary-tiled
+ *                      rows — and info.max_fused_vocab for the fused step),
  *      NGPULM_ECUDA    a CUDA runtime error (message carries cudaGetErrorString),
  *      NGPULM_EIO      a file could not be read.
  *    ngpulm_last_error() returns a thread-local message for the last non-OK return.
@@ -61,10 +63,11 @@ typedef struct {
   int64_t num_unk_filled; /* M: vocabulary tokens without a unigram (R2) */
   int64_t num_dropped;    /* n-grams with <unk> beyond the unigram, dropped (R5) */
   int64_t device_bytes;   /* bytes of the resident model on the device */
-  int32_t max_vocab;      /* largest V the kernels accept */
+  int32_t max_vocab;      /* largest V advance/final accept (rows beyond shared memory are tiled) */
   int32_t chain_mode;     /* NGPULM_CHAIN_TABLE or NGPULM_CHAIN_WALK */
   int32_t advance_kernel; /* NGPULM_ADVANCE_* as set (AUTO by default) */
   int32_t packed_arcs;    /* 1: the device also holds arcs packed as (target << bits) | token */
+  int32_t max_fused_vocab;/* largest V of the fused step (its row must fit in shared memory) */
 } ngpulm_info;
 
 /* Read-only view of the model's host copy of the flat arrays.

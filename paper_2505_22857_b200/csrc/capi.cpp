@@ -132,8 +132,7 @@ int check_hot(const ngpulm_model* m, int32_t B) {
   if (!m) return err(NGPULM_EUSAGE, "model is NULL");
   if (m->device < 0) return err(NGPULM_EUSAGE, "host-only model (loaded with cuda_device = -1)");
   if (B < 0) return err(NGPULM_EUSAGE, "B < 0");
-  if (m->h.V > ngpulm::max_vocab_supported())
-    return err(NGPULM_EUSAGE, "vocabulary larger than the kernels' shared-memory row");
+  if (m->h.V > ngpulm::max_vocab_supported()) return err(NGPULM_EUSAGE, "vocabulary larger than supported");
   int cur = -1;
   cudaGetDevice(&cur);
   if (cur != m->device) return err(NGPULM_EUSAGE, "current CUDA device differs from the model's device");
@@ -243,6 +242,7 @@ int ngpulm_get_info(const ngpulm_model* m, ngpulm_info* out) {
   out->num_dropped = m->h.num_dropped;
   out->device_bytes = (int64_t)m->blob_bytes;
   out->max_vocab = ngpulm::max_vocab_supported();
+  out->max_fused_vocab = ngpulm::max_fused_vocab();
   out->chain_mode = m->chain_mode;
   out->advance_kernel = m->dm.adv_kind;
   out->packed_arcs = m->dm.arc_q != nullptr;
@@ -312,6 +312,7 @@ int ngpulm_fused_greedy_step(const ngpulm_model* m, int32_t mode, const float* l
   if (int r = check_hot(m, B)) return r;
   if (mode != NGPULM_CTC && mode != NGPULM_RNNT && mode != NGPULM_AED) return err(NGPULM_EUSAGE, "bad mode");
   if (blank_id < 0 || blank_id > m->h.V) return err(NGPULM_EUSAGE, "blank_id outside [0, V]");
+  if (m->h.V > ngpulm::max_fused_vocab()) return err(NGPULM_EUSAGE, "fused step: the row must fit in shared memory");
   if (B == 0) return NGPULM_OK;
   if (!logits || !states || !tokens_out || (mode == NGPULM_CTC && !prev))
     return err(NGPULM_EUSAGE, "NULL device buffer");
@@ -329,6 +330,7 @@ int ngpulm_fused_greedy_step_ilm(const ngpulm_model* m, int32_t mode, const floa
   if (int r = check_hot(m, B)) return r;
   if (mode != NGPULM_CTC && mode != NGPULM_RNNT && mode != NGPULM_AED) return err(NGPULM_EUSAGE, "bad mode");
   if (blank_id < 0 || blank_id > m->h.V) return err(NGPULM_EUSAGE, "blank_id outside [0, V]");
+  if (m->h.V > ngpulm::max_fused_vocab()) return err(NGPULM_EUSAGE, "fused step: the row must fit in shared memory");
   if (B == 0) return NGPULM_OK;
   if (!logits || !states || !tokens_out || !ilm || (mode == NGPULM_CTC && !prev))
     return err(NGPULM_EUSAGE, "NULL device buffer");

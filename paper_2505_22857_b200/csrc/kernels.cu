@@ -164,20 +164,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // it): root level -> row slots by TMA bulk copy (SASS: UBLKCP). The barrier
 // init is made visible to the async proxy with a CTA-scope proxy fence.
 constexpr int kTmaThread = 32;
-__device__ __forceinline__ void prologue(const DevModel& m, const Slice& s, bool tma) {
+// lo / tv: the vocabulary tile [lo, lo + tv) this CTA answers (the whole row
+// when the row fits in shared memory).
+__device__ __forceinline__ void prologue(const DevModel& m, const Slice& s, bool tma, int32_t lo = 0,
+                                         int32_t tv = -1) {
   if (threadIdx.x != kTmaThread) return;
-  const uint32_t b = smem_u32(s.bar), bytes = (uint32_t)m.V * 4u;
+  const uint32_t b = smem_u32(s.bar), bytes = (uint32_t)(tv < 0 ? m.V : tv) * 4u;
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (!tma) return;
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(2u * bytes) : "memory");
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(s.row_s)),
-               "l"(m.arc_w), "r"(bytes), "r"(b)
+               "l"(m.arc_w + lo), "r"(bytes), "r"(b)
                : "memory");
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(s.row_n)),
-               "l"(m.arc_to), "r"(bytes), "r"(b)
+               "l"(m.arc_to + lo), "r"(bytes), "r"(b)
                : "memory");
 }
 
@@ -300,13 +303,17 @@ __device__ __forceinline__ void stage_arcs(const DevModel& m, const Slice& s, in
 
 // Step 3 for one round: levels from the highest index (lowest order) down,
 // one barrier each, threads strided over the level's staged slots.
-__device__ __forceinline__ void write_levels(const Slice& s, int32_t lo, int32_t hi, int Llo, int Lhi) {
+// (tile: tokens [t0, t0 + tv) of the row; others are skipped)
+__device__ __forceinline__ void write_levels(const Slice& s, int32_t lo, int32_t hi, int Llo, int Lhi, int32_t t0,
+                                             uint32_t tv) {
   for (int L = Lhi; L >= Llo; --L) {
     const int32_t j1 = min(hi, s.pre[L + 1]) - lo;
     for (int32_t j = max(lo, s.pre[L]) - lo + (int32_t)threadIdx.x; j < j1; j += kThreads) {
-      const int32_t tok = s.st_tok[j];
-      s.row_s[tok] = s.st_s[j];
-      s.row_n[tok] = s.st_n[j];
+      const uint32_t i = (uint32_t)(s.st_tok[j] - t0);
+      if (i < tv) {
+        s.row_s[i] = s.st_s[j];
+        s.row_n[i] = s.st_n[j];
+      }
     }
     __syncthreads();
   }
@@ -316,8 +323,9 @@ __device__ __forceinline__ void write_levels(const Slice& s, int32_t lo, int32_t
 // first. Rounds of kChunk arcs run from the last (lowest-order) arcs to the
 // first; the first round's loads are issued before the root fix-up so their
 // latencies overlap.
-__device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, const Row& r, bool tma) {
-  const int32_t V = m.V, T = r.total;
+__device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, const Row& r, bool tma, int32_t t0 = 0,
+                                          int32_t tv = -1) {
+  const int32_t V = tv < 0 ? m.V : tv, T = r.total;
   const float acc_root = r.acc_root;
   int32_t lo = T > kChunk ? T - kChunk : 0;
   if (T > 0) stage_arcs(m, s, lo, T);
@@ -335,15 +343,15 @@ __device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, con
     }
   } else {
     for (int32_t v = threadIdx.x; v < V; v += kThreads) {
-      s.row_s[v] = __fadd_rn(acc_root, __ldg(&m.arc_w[v]));
-      s.row_n[v] = __ldg(&m.arc_to[v]);
+      s.row_s[v] = __fadd_rn(acc_root, __ldg(&m.arc_w[t0 + v]));
+      s.row_n[v] = __ldg(&m.arc_to[t0 + v]);
     }
   }
   __syncthreads();
   STAMP(5);
   for (int32_t hi = T; hi > 0;) {
     const int Llo = lo == 0 ? 0 : level_of(s, lo), Lhi = hi == T ? r.nlev - 1 : level_of(s, hi - 1);
-    write_levels(s, lo, hi, Llo, Lhi);
+    write_levels(s, lo, hi, Llo, Lhi, t0, (uint32_t)V);
     hi = lo;
     if (hi == 0) break;
     lo = hi > kChunk ? hi - kChunk : 0;
@@ -354,12 +362,17 @@ __device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, con
 }
 
 // ---------------------------------------------------------------- advance
+// Vocabulary tiling: when a row does not fit in shared
+// memory, CTA (b, y) answers tokens [y * tile, y * tile + tv) of row b —
+// Algorithm 1 restricted to the tile is exact (each token's value depends only
+// on the arcs for that token); every CTA reads the row's full arc list and
+// keeps its tile's tokens.
 template <bool kVec4, bool kTable>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     advance_kernel(DevModel m, const int32_t* __restrict__ states, float* __restrict__ scores,
-                   int32_t* __restrict__ next, float* __restrict__ final_out) {
+                   int32_t* __restrict__ next, float* __restrict__ final_out, int32_t tile) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int32_t V = m.V, b = blockIdx.x;
+  const int32_t b = blockIdx.x, t0 = (int32_t)blockIdx.y * tile, V = min(tile, m.V - t0);
   const int t = threadIdx.x;
   const Slice s = carve(smem, V, m.order);
   STAMP(0);
@@ -371,23 +384,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #else
   const bool use_tma = kVec4;
 #endif
-  prologue(m, s, use_tma);
+  prologue(m, s, use_tma, t0, V);
   pdl_wait();
   STAMP(2);
   const Row r = row_levels<kTable>(m, states + b, s);
   STAMP(3);
-  if (t == 0) {
+  if (t == 0 && t0 == 0) {
     if (r.bad) atomicMin(m.bad_row, (unsigned long long)b);
     if (final_out) final_out[b] = r.bad ? __int_as_float(0x7fc00000) : r.fin;
   }
-  float* srow = scores + (size_t)b * V;
-  int32_t* nrow = next + (size_t)b * V;
+  float* srow = scores + (size_t)b * m.V + t0;
+  int32_t* nrow = next + (size_t)b * m.V + t0;
   if (r.bad) {
     for (int32_t v = t; v < V; v += kThreads) { srow[v] = __int_as_float(0x7fc00000); nrow[v] = -1; }
     if (use_tma) mbar_wait(s.bar, 0);  // no exit with the bulk copy in flight
     return;
   }
-  build_row(m, s, r, use_tma);
+  build_row(m, s, r, use_tma, t0, V);
 
   if (kVec4) {
     // step 4: the finished row leaves by TMA bulk stores (SASS: UBLKCP shared -> global)
@@ -1721,10 +1734,20 @@ extern "C" int ngpulm_debug_phases(unsigned long long* host, int n) {
 }
 #endif
 
-int max_vocab_supported() {
+// The largest row (multiple of 4 tokens) the CTA kernels hold in shared memory.
+int max_row_in_smem(int32_t order) {
   int v = 32768;
-  while (v > 0 && row_smem(v, NGPULM_MAX_ORDER) > 227 * 1024) v -= 4;
+  while (v > 0 && row_smem(v, order) > 227 * 1024) v -= 4;
   return v;
+}
+// advance / final: any V (rows are tiled); fused step, top-k, decode: one row in shared memory.
+int max_vocab_supported() { return 1 << 24; }
+int max_fused_vocab() { return max_row_in_smem(NGPULM_MAX_ORDER); }
+// Tile of the CTA advance kernel: the whole row if it fits, else the largest
+// multiple of 4 that fits (unaligned V: the scalar path, any tile).
+int32_t vocab_tile(int32_t V, int32_t order) {
+  const int32_t cap = max_row_in_smem(order);
+  return V <= cap ? V : cap;
 }
 
 int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* scores, int32_t* next,
@@ -1764,12 +1787,14 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
 #undef NGPULM_WARP_LAUNCH
     }
   }
-  const size_t sm = row_smem(m.V, m.order);
-  const dim3 gd(B), bd(kThreads);
-  if (vec && table) return launch(advance_kernel<true, true>, gd, bd, sm, st, m, states, scores, next, final_out);
-  if (vec) return launch(advance_kernel<true, false>, gd, bd, sm, st, m, states, scores, next, final_out);
-  if (table) return launch(advance_kernel<false, true>, gd, bd, sm, st, m, states, scores, next, final_out);
-  return launch(advance_kernel<false, false>, gd, bd, sm, st, m, states, scores, next, final_out);
+  const int32_t tile = vocab_tile(m.V, m.order);
+  const size_t sm = row_smem(tile, m.order);
+  const dim3 gd(B, (m.V + tile - 1) / tile), bd(kThreads);
+  if (vec && table)
+    return launch(advance_kernel<true, true>, gd, bd, sm, st, m, states, scores, next, final_out, tile);
+  if (vec) return launch(advance_kernel<true, false>, gd, bd, sm, st, m, states, scores, next, final_out, tile);
+  if (table) return launch(advance_kernel<false, true>, gd, bd, sm, st, m, states, scores, next, final_out, tile);
+  return launch(advance_kernel<false, false>, gd, bd, sm, st, m, states, scores, next, final_out, tile);
 }
 
 int launch_final(const DevModel& m, const int32_t* states, int32_t B, float* out, void* stream) {

@@ -106,5 +106,6 @@ int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride
                       int32_t T, const int32_t* lengths, int32_t* states, int32_t* prev, float lambda, int32_t blank,
                       int32_t* frames_out, int32_t* emit_out, int32_t* emit_len, void* stream);
 int max_vocab_supported();
+int max_fused_vocab();
 
 }  // namespace ngpulm

@@ -316,3 +316,39 @@ def test_mid_size_batches_full_rows(pairs, name, B):
     s32, _, n_o, _ = o.rows(uniq, want64=False)
     f32, _ = o.finals(uniq)
     assert np.array_equal(n, n_o[inv]) and same_bits(s, s32[inv]) and same_bits(f, f32[inv])
+
+
+@pytest.fixture(scope="module")
+def lm_bigv(lm_dir):
+    """V = 40000 (beyond one shared-memory row): a word-level-sized vocabulary, 3-gram."""
+    f = synth.make_lm(lm_dir, 40000, 3, tokens=300000, seed=9, heldout=300, tag="bigv_3gram")
+    return ng.load_arpa(f.arpa, vocab_size=40000, device=0), Oracle(f.arpa, vocab_size=40000), f
+
+
+@pytest.mark.parametrize("chain", [ng.CHAIN_TABLE, ng.CHAIN_WALK])
+def test_vocab_tiled_advance(lm_bigv, chain):
+    """rows larger than shared memory are answered tile by tile
+    (one CTA per (row, vocabulary tile)); full rows bit-exact vs the oracle."""
+    m, o, f = lm_bigv
+    assert m.V > m.info.max_fused_vocab and m.info.max_vocab >= m.V
+    states, _ = trajectory_states(m, f, 24, seed=71)
+    states[:3] = [0, m.bos_state, o.num_states - 1]
+    with using(m, chain):
+        s, n, fin = gpu_advance(m, states)
+    s32, s64, n_o, _ = o.rows(states)
+    f32, _ = o.finals(states)
+    assert np.array_equal(n, n_o) and same_bits(s, s32) and same_bits(fin, f32)
+    # the fused step refuses a row that does not fit
+    x = torch.zeros((2, m.V + 1), dtype=torch.float32, device=dev())
+    with pytest.raises(ng.NgpulmError):
+        m.fused_greedy_step(RNNT, x, torch.zeros(2, dtype=torch.int32, device=dev()))
+
+
+def test_vocab_tiled_unaligned_v(lm_dir):
+    """V % 4 != 0 beyond one row: the scalar (no-TMA) path, tiled."""
+    f = synth.make_lm(lm_dir, 30001, 2, tokens=100000, seed=10, heldout=100, tag="bigv_odd")
+    m, o = ng.load_arpa(f.arpa, vocab_size=30001, device=0), Oracle(f.arpa, vocab_size=30001)
+    states = synth.uniform_states(o.num_states, 16, seed=72)
+    s, n, fin = gpu_advance(m, states)
+    s32, _, n_o, _ = o.rows(states, want64=False)
+    assert np.array_equal(n, n_o) and same_bits(s, s32)
