@@ -446,6 +446,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #ifndef NGPULM_STORE_HINT
 #define NGPULM_STORE_HINT 1
 #endif
+#ifndef NGPULM_FUSED_MAX_ROWS
+#define NGPULM_FUSED_MAX_ROWS 8
+#endif
 #ifndef NGPULM_CTA_ROOT
 #define NGPULM_CTA_ROOT 1  // the 16-slot path (148 < B <= 1184): measured 3.74 -> 3.64 us at B = 1024
 #endif
@@ -1807,7 +1810,7 @@ int launch_fused_mode(const DevModel& m, const float* logits, int64_t row_stride
                       int32_t* tokens_out, cudaStream_t st) {
   if (m.V % 4 == 0 && m.V <= 1024 && m.adv_kind != NGPULM_ADVANCE_CTA) {
     int R = (B + 147) / 148;
-    R = R < 1 ? 1 : (R > 8 ? 8 : R);
+    R = R < 1 ? 1 : (R > NGPULM_FUSED_MAX_ROWS ? NGPULM_FUSED_MAX_ROWS : R);
     const size_t wsm = (size_t)R * fslice_bytes(m.V, m.order);
     const dim3 wg((B + R - 1) / R), wb(32 * R);
     const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
