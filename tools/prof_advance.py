@@ -17,7 +17,7 @@ import synth  # noqa: E402
 p = argparse.ArgumentParser()
 p.add_argument("--batch", type=int, default=1024)
 p.add_argument("--iters", type=int, default=20)
-p.add_argument("--mode", default="advance", choices=["advance", "ctc", "rnnt", "aed"])
+p.add_argument("--mode", default="advance", choices=["advance", "ctc", "rnnt", "aed", "decode"])
 a = p.parse_args()
 f = synth.make_lm("/tmp/ngpulm_prof", 1024, 6, tokens=430000, seed=1, heldout=4000, tag="bench_6gram")
 m = ng.load_arpa(f.arpa, vocab_size=1024, device=0)
@@ -30,6 +30,13 @@ if a.mode == "advance":
     fi = torch.empty((4, a.batch), dtype=torch.float32, device="cuda")
     for i in range(a.iters):
         m.advance(st[i % 4], sc[i % 4], nx[i % 4], fi[i % 4])
+elif a.mode == "decode":  # persistent CTC decode, BASELINE configs[2] shape
+    T = 500
+    x = torch.from_numpy(synth.ctc_logits(synth.read_sentences(f.heldout), a.batch, T, 1024, seed=4)).cuda()
+    for i in range(a.iters):
+        s = torch.zeros(a.batch, dtype=torch.int32, device="cuda")
+        pv = torch.full((a.batch,), -1, dtype=torch.int32, device="cuda")
+        m.ctc_greedy_decode(x, s, pv, lam=0.3)
 else:
     mode = {"ctc": ng.CTC, "rnnt": ng.RNNT, "aed": ng.AED}[a.mode]
     x = torch.from_numpy(synth.rnnt_logits(a.batch, 4, 1024, seed=4)).cuda()

@@ -20,3 +20,6 @@ tail -3 gpurun_out/ncu_full_$TAG.log
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused_warp -s 10 -c 1 \
     -o gpurun_out/fused_ctc_$TAG -f python tools/prof_advance.py --batch 256 --mode ctc > gpurun_out/ncu_fused_$TAG.log 2>&1
 tail -3 gpurun_out/ncu_fused_$TAG.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ctc_decode -s 2 -c 1 \
+    -o gpurun_out/decode_$TAG -f python tools/prof_advance.py --batch 256 --mode decode --iters 4 > gpurun_out/ncu_decode_$TAG.log 2>&1
+tail -3 gpurun_out/ncu_decode_$TAG.log
