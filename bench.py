@@ -294,6 +294,7 @@ def run_ours(args):
            "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": 8 * B * V + 4 * B, "steps": Ke}
 
     variants = advance_variants(m, states, scores, nxt, fin, R, stream)
+    variants.update(tiny_lm_variant(f"{args.workdir}_r{rank}", dev, stream))
     fused = {}
     if not args.no_fused:
         fused = bench_fused(m, f, dev, stream, rank)
@@ -378,6 +379,31 @@ def advance_variants(m, states, scores, nxt, fin, R, stream):
 
         out[name] = _graph_time(calls, stream, None, reps=3, reset=lambda: None) * 1e3 / n
     m.set_chain_mode(ng.CHAIN_TABLE)
+    return out
+
+
+def tiny_lm_variant(workdir, dev, stream):
+    """A keyword-biasing-sized LM (a 200-keyword LM; here a 3-gram from
+    600 corpus tokens, V=1024, ~800 states): advance at B=1024 with the model resident
+    in shared memory (AUTO) vs read from global memory (WARP)."""
+    import torch
+    import paper_2505_22857_b200 as ng
+    import synth
+    f = synth.make_lm(workdir + "_tiny", V, 3, tokens=600, seed=11, heldout=200, tag="tiny_bias")
+    m = ng.load_arpa(f.arpa, vocab_size=V, device=dev.index)
+    B, R = 1024, 32
+    st = torch.from_numpy(synth.uniform_states(m.num_states, B * R, seed=12).reshape(R, B)).to(dev)
+    sc = torch.empty((R, B, V), dtype=torch.float32, device=dev)
+    nx = torch.empty((R, B, V), dtype=torch.int32, device=dev)
+    out = {"tiny_lm_states": m.num_states, "tiny_resident": int(m.info.tiny_resident)}
+    for name, kind in (("tiny_lm_b1024_smem_us", ng.ADVANCE_AUTO), ("tiny_lm_b1024_global_us", ng.ADVANCE_WARP)):
+        m.set_advance_kernel(kind)
+
+        def calls():
+            for k in range(4 * R):
+                m.advance(st[k % R], sc[k % R], nx[k % R], want_final=False, stream=stream)
+        out[name] = _graph_time(calls, stream, None, reps=3, reset=lambda: None) * 1e3 / (4 * R)
+    m.set_advance_kernel(ng.ADVANCE_AUTO)
     return out
 
 

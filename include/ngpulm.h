@@ -68,6 +68,8 @@ typedef struct {
   int32_t advance_kernel; /* NGPULM_ADVANCE_* as set (AUTO by default) */
   int32_t packed_arcs;    /* 1: the device also holds arcs packed as (target << bits) | token */
   int32_t max_fused_vocab;/* largest V of the fused step (its row must fit in shared memory) */
+  int32_t tiny_resident;  /* 1: a tiny LM (<= 96 KiB of chain table + packed arcs): NGPULM_ADVANCE_AUTO
+                             answers from a copy in every CTA's shared memory */
 } ngpulm_info;
 
 /* Read-only view of the model's host copy of the flat arrays.
@@ -134,7 +136,8 @@ int ngpulm_set_chain_mode(ngpulm_model* model, int32_t mode);
  * bit-identical results:
  *   NGPULM_ADVANCE_AUTO (default): one warp per row, reading the arcs packed as
  *     (target << ceil(log2 V)) | token beside the weights when every target
- *     fits (info.packed_arcs), else as NGPULM_ADVANCE_WARP;
+ *     fits (info.packed_arcs), else as NGPULM_ADVANCE_WARP; a tiny LM
+ *     (info.tiny_resident) is read from a copy in shared memory;
  *   NGPULM_ADVANCE_WARP: one warp per row over the token/weight/target arrays;
  *   NGPULM_ADVANCE_CTA: one 256-thread CTA per row.
  * The warp kernels need V % 4 == 0 and 16-byte aligned outputs; otherwise

@@ -37,7 +37,8 @@ class Info(C.Structure):
                 ("root_state", C.c_int32), ("bos_state", C.c_int32), ("device", C.c_int32),
                 ("num_arcs", C.c_int64), ("num_unk_filled", C.c_int64), ("num_dropped", C.c_int64),
                 ("device_bytes", C.c_int64), ("max_vocab", C.c_int32), ("chain_mode", C.c_int32),
-                ("advance_kernel", C.c_int32), ("packed_arcs", C.c_int32), ("max_fused_vocab", C.c_int32)]
+                ("advance_kernel", C.c_int32), ("packed_arcs", C.c_int32), ("max_fused_vocab", C.c_int32),
+                ("tiny_resident", C.c_int32)]
 
 
 class HostView(C.Structure):

@@ -125,6 +125,11 @@ int upload(ngpulm_model* m, int device) {
   m->dm.arc_q = pack ? static_cast<const void*>(base + o_q) : nullptr;
   m->dm.pk_bits = pk_bits;
   m->dm.adv_kind = NGPULM_ADVANCE_AUTO;
+  // tiny LM (keyword-biasing size): chain table + packed quads <= 96 KiB stay in shared memory
+  const size_t chain_bytes = chain.size() * 4, arcq_bytes = pack ? A * 8 : 0;
+  const bool tiny = pack && h.V <= 1024 && h.V % 4 == 0 && chain_bytes + arcq_bytes <= ((size_t)96 << 10);
+  m->dm.tiny_chain_bytes = tiny ? (int32_t)chain_bytes : 0;
+  m->dm.tiny_arcq_bytes = tiny ? (int32_t)arcq_bytes : 0;
   return NGPULM_OK;
 }
 
@@ -243,6 +248,7 @@ int ngpulm_get_info(const ngpulm_model* m, ngpulm_info* out) {
   out->device_bytes = (int64_t)m->blob_bytes;
   out->max_vocab = ngpulm::max_vocab_supported();
   out->max_fused_vocab = ngpulm::max_fused_vocab();
+  out->tiny_resident = m->dm.tiny_chain_bytes > 0;
   out->chain_mode = m->chain_mode;
   out->advance_kernel = m->dm.adv_kind;
   out->packed_arcs = m->dm.arc_q != nullptr;

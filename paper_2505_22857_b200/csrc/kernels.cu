@@ -898,6 +898,130 @@ __global__ void __launch_bounds__(256, 1)
   if (w == 0) STAMPS_OUT(row);
 }
 
+// ---------------------------------------------------------------- advance, tiny LM resident in shared memory
+// Tiny LMs (the paper's 200-keyword biasing LM,
+// PAPER.md:295): the whole chain table and the packed arc quads are
+// bulk-copied into every CTA's shared memory before griddepcontrol.wait (model
+// data is immutable, so the copy overlaps the previous kernel), and a row's
+// record and arc quads are then read from shared memory — the two dependent
+// L2 round trips after the state load become ~30-cycle shared loads. Row
+// construction otherwise as advance_warp_kernel (root level from registers,
+// level-ordered writes, bulk stores).
+__host__ __device__ constexpr size_t tiny_model_bytes(int64_t chain_bytes, int64_t arcq_bytes, int32_t V) {
+  return align16((size_t)chain_bytes) + align16((size_t)arcq_bytes) + align16((size_t)V * 4) + 16;
+}
+
+template <int kW>
+__global__ void __launch_bounds__(256, 1)
+    advance_tiny_kernel(DevModel m, const int32_t* __restrict__ states, int32_t B, float* __restrict__ scores,
+                        int32_t* __restrict__ next, float* __restrict__ final_out, int32_t chain_bytes,
+                        int32_t arcq_bytes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int32_t V = m.V;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, R = blockDim.x >> 5;
+  const int4* chain_s = reinterpret_cast<const int4*>(smem);
+  int4* arcq_s = reinterpret_cast<int4*>(smem + align16(chain_bytes));
+  int32_t* root_to = reinterpret_cast<int32_t*>(smem + align16(chain_bytes) + align16(arcq_bytes));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + align16(chain_bytes) + align16(arcq_bytes) + align16(V * 4));
+  const size_t mb = tiny_model_bytes(chain_bytes, arcq_bytes, V);
+  WSlice s = wcarve(smem + mb + (size_t)w * wslice_bytes(V, m.order, 0), V, m.order, 0);
+  s.st_q = arcq_s;  // the quads are read from the CTA's copy (absolute quad index)
+  const int32_t row = (int32_t)blockIdx.x * R + w;
+  const uint32_t bytes = (uint32_t)V * 4u;
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"((uint32_t)(chain_bytes + arcq_bytes) + bytes)
+                 : "memory");
+    bulk_g2s(const_cast<int4*>(chain_s), m.chain, (uint32_t)chain_bytes, bar);
+    bulk_g2s(arcq_s, m.arc_q, (uint32_t)arcq_bytes, bar);
+    bulk_g2s(root_to, m.arc_to, bytes, bar);
+  }
+  float4 rw[8];
+  if (row < B) {
+    const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (lane + 32 * j < V / 4) rw[j] = __ldg(w4 + lane + 32 * j);
+  }
+  __syncthreads();  // the barrier's init visible to every warp
+  if (row < B) {
+    mbar_wait(bar, 0);
+    const int4* src = reinterpret_cast<const int4*>(root_to);
+    int4* dst = reinterpret_cast<int4*>(s.row_n);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (lane + 32 * j < V / 4) dst[lane + 32 * j] = src[lane + 32 * j];
+  }
+  pdl_wait();
+  if (row >= B) return;  // warp 0 of every CTA has a row (and waited for the CTA's copy)
+  // the row's state and its chain-table record (lane l+1 = level l), from shared memory
+  const int32_t st = __shfl_sync(kFull, lane == 0 ? __ldg(states + row) : 0, 0);
+  float* srow = scores + (size_t)row * V;
+  int32_t* nrow = next + (size_t)row * V;
+  const bool bad = st < 0 || st >= m.S;
+  int4 x = make_int4(0, 0, 0, 0);
+  if (!bad && lane < m.chain_slots) x = chain_s[(size_t)st * m.chain_slots + lane];
+  const int32_t nlev = __shfl_sync(kFull, x.x, 0);
+  const float acc_root = __int_as_float(__shfl_sync(kFull, x.y, 0));
+  const float fin = __int_as_float(__shfl_sync(kFull, x.z, 0));
+  if (lane == 0) {
+    if (bad) atomicMin(m.bad_row, (unsigned long long)row);
+    if (final_out) final_out[row] = bad ? __int_as_float(0x7fc00000) : fin;
+  }
+  if (bad) {
+    for (int32_t v = lane; v < V; v += 32) { srow[v] = __int_as_float(0x7fc00000); nrow[v] = -1; }
+    return;
+  }
+  WLevel lv;
+  lv.beg = 0; lv.qbase = 0; lv.info = 0; lv.eslot = INT_MAX; lv.acc = 0.f;
+  if (lane >= 1 && lane <= nlev) {
+    lv.beg = x.x;
+    lv.acc = __int_as_float(x.z);
+    lv.info = x.w;
+    lv.eslot = (lv.info >> 16) + (((lv.info & 0xffff) + 31) >> 5);
+  }
+  lv.qbase = lv.beg >> 2;
+  const int32_t nslots = nlev > 0 ? __shfl_sync(kFull, lv.eslot, 1) : 0;
+  Window<kW, true> a;
+  load_window<kW, true, true>(m, s, lv, nlev, 0, nslots, a);
+  {  // root scores: acc_root + root weight
+    float4* s4 = reinterpret_cast<float4*>(s.row_s);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (lane + 32 * j < V / 4) {
+        float4 y = rw[j];
+        y.x = __fadd_rn(acc_root, y.x);
+        y.y = __fadd_rn(acc_root, y.y);
+        y.z = __fadd_rn(acc_root, y.z);
+        y.w = __fadd_rn(acc_root, y.w);
+        s4[lane + 32 * j] = y;
+      }
+  }
+  __syncwarp();
+  for (int32_t k0 = 0; k0 < nslots;) {
+    write_window<kW, true>(s, a, k0, nslots, m.pk_bits);
+    k0 += kW;
+    if (k0 < nslots) load_window<kW, true, true>(m, s, lv, nlev, k0, nslots, a);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(srow),
+                 "r"(smem_u32(s.row_s)), "r"(bytes), "l"(pol)
+                 : "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(nrow),
+                 "r"(smem_u32(s.row_n)), "r"(bytes), "l"(pol)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
 // ---------------------------------------------------------------- final
 __global__ void final_kernel(DevModel m, const int32_t* __restrict__ states, int32_t B,
                              float* __restrict__ out) {
@@ -1758,6 +1882,22 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
   const bool vec = (m.V % 4 == 0) && ((uintptr_t)scores % 16 == 0) && ((uintptr_t)next % 16 == 0);
   const bool table = m.chain != nullptr;
   cudaStream_t st = (cudaStream_t)stream;
+  if (vec && table && m.tiny_chain_bytes > 0 && m.adv_kind == NGPULM_ADVANCE_AUTO) {
+    // tiny LM: model resident in every CTA's shared memory
+    const size_t mb = tiny_model_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes, m.V);
+    int R = (B + 147) / 148;
+    R = R < 1 ? 1 : (R > 8 ? 8 : R);
+    while (R > 1 && mb + (size_t)R * wslice_bytes(m.V, m.order, 0) > 227 * 1024) --R;
+    const size_t tsm = mb + (size_t)R * wslice_bytes(m.V, m.order, 0);
+    if (tsm <= 227 * 1024) {
+      const dim3 tg((B + R - 1) / R), tb(32 * R);
+      if (B > 8 * 148)
+        return launch(advance_tiny_kernel<8>, tg, tb, tsm, st, m, states, B, scores, next, final_out,
+                      m.tiny_chain_bytes, m.tiny_arcq_bytes);
+      return launch(advance_tiny_kernel<16>, tg, tb, tsm, st, m, states, B, scores, next, final_out,
+                    m.tiny_chain_bytes, m.tiny_arcq_bytes);
+    }
+  }
   if (vec && m.adv_kind != NGPULM_ADVANCE_CTA) {
     // up to 8 rows per SM: 16-slot windows (almost every row in one window),
     // packed arcs bulk-copied into a staging area; more rows per SM: 8-slot

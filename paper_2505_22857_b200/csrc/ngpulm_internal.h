@@ -84,6 +84,9 @@ struct DevModel {
   int32_t pk_bits;
   int32_t adv_kind;             // NGPULM_ADVANCE_*
   unsigned long long* bad_row;  // sticky min bad row (ULLONG_MAX = none)
+  // tiny LMs: bytes of the chain table and of the packed arc quads, both
+  // staged into shared memory by the advance kernel (0: not a tiny LM)
+  int32_t tiny_chain_bytes, tiny_arcq_bytes;
 };
 
 // Kernel launchers (kernels.cu). Return cudaError_t as int.

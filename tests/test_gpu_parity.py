@@ -352,3 +352,20 @@ def test_vocab_tiled_unaligned_v(lm_dir):
     s, n, fin = gpu_advance(m, states)
     s32, _, n_o, _ = o.rows(states, want64=False)
     assert np.array_equal(n, n_o) and same_bits(s, s32)
+
+
+@pytest.mark.parametrize("B", [7, 600, 1024, 3000])
+def test_tiny_lm_resident_kernel(pairs, B):
+    """SURVEY.md §8(f) f4 tiny-LM path: a keyword-biasing-sized LM is answered from
+    a copy in every CTA's shared memory (AUTO) — bit-identical to the global-memory
+    warp kernel and to the oracle."""
+    m, o, _ = pairs["tri64"]
+    assert m.info.tiny_resident == 1
+    states = synth.uniform_states(o.num_states, B, seed=B + 1)
+    s, n, f = gpu_advance(m, states)
+    with using(m, kernel=ng.ADVANCE_WARP):
+        s2, n2, f2 = gpu_advance(m, states)
+    assert same_bits(s, s2) and np.array_equal(n, n2) and same_bits(f, f2)
+    uniq, inv = np.unique(states, return_inverse=True)
+    s32, _, n_o, _ = o.rows(uniq, want64=False)
+    assert np.array_equal(n, n_o[inv]) and same_bits(s, s32[inv])
