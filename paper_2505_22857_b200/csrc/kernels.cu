@@ -618,6 +618,7 @@ __device__ __forceinline__ void load_window(const DevModel& m, const WSlice& s, 
     }
 #pragma unroll
     for (int u = g; u < g + 8; ++u) {
+      if (u > g && k0 + u >= nslots) break;  // (uniform) no load for slots past the row's last one
       if (kSmem) {  // two 16-byte shared loads of the staged quad
         a.tok[u] = s.st_q[2 * qv[u - g]];
         const int4 x = s.st_q[2 * qv[u - g] + 1];
@@ -649,6 +650,7 @@ __device__ __forceinline__ void write_window(const WSlice& s, const Window<kW, k
     if (g > 0 && k0 + g >= nslots) break;
 #pragma unroll
     for (int u = g; u < g + 8; ++u) {
+      if (u > g && k0 + u >= nslots) break;  // (uniform) past the row's last slot: nothing to write
       if (u > 0) __syncwarp();  // slots in level order: a lower order is done before a higher one
       const int32_t x[4] = {a.tok[u].x, a.tok[u].y, a.tok[u].z, a.tok[u].w};
       const float ww[4] = {a.w[u].x, a.w[u].y, a.w[u].z, a.w[u].w};
