@@ -446,6 +446,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #ifndef NGPULM_STORE_HINT
 #define NGPULM_STORE_HINT 1
 #endif
+#ifndef NGPULM_PAIR_MAX_B
+#define NGPULM_PAIR_MAX_B (4 * 148)  // transducer steps: two warps per row up to 4 rows per SM (measured:
+                                     // RNN-T B=512 4.36 -> 4.00 us; CTC/AED lose, they keep one warp)
+#endif
 #ifndef NGPULM_FUSED_MAX_ROWS
 #define NGPULM_FUSED_MAX_ROWS 8
 #endif
@@ -1226,6 +1230,29 @@ __device__ __forceinline__ int32_t warp_argmax_cols(const float (&v)[kMaxColsPer
   return (int32_t)__reduce_min_sync(kFull, (uint32_t)cm);
 }
 
+// The same over the lane columns j in [J0, J1) only; also returns the maximum
+// (-inf with column INT_MAX when every value there is NaN).
+template <int J0, int J1>
+__device__ __forceinline__ int32_t warp_argmax_range(const float (&v)[kMaxColsPerLane], float& M) {
+  const int lane = threadIdx.x & 31;
+  constexpr int N = J1 - J0;
+  float mx[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) mx[j] = v[J0 + j];
+#pragma unroll
+  for (int d = 1; d < N; d *= 2)
+#pragma unroll
+    for (int j = 0; j + d < N; j += 2 * d) mx[j] = fmaxf(mx[j], mx[j + d]);
+  const float lmax = mx[0] == mx[0] ? mx[0] : -INFINITY;
+  const uint32_t kmax = __reduce_max_sync(kFull, fkey(lmax));
+  M = __uint_as_float((kmax & 0x80000000u) ? (kmax ^ 0x80000000u) : ~kmax);
+  int32_t cm = INT_MAX;
+#pragma unroll
+  for (int j = J1 - 1; j >= J0; --j)
+    if (v[j] == M) cm = lane + 32 * j;
+  return (int32_t)__reduce_min_sync(kFull, (uint32_t)cm);
+}
+
 // Transducer label-looping bookkeeping (
 // SPEC.md:317-325): with kMode == kLoop the fused step makes the RNN-T
 // two-stage decision for the rows whose frame index is inside their length,
@@ -1423,6 +1450,220 @@ __global__ void __launch_bounds__(256, 1)
   }
   STAMP(8);
   if (w == 0) STAMPS_OUT(row);
+}
+
+// ---------------------------------------------------------------- fused greedy step, two warps per row
+// The same step with the row's work split over a warp pair: warp A builds
+// the LM row (state, chain record, gathers, level writes) exactly as
+// fused_warp_kernel; warp B, which does not need the state, copies the
+// logits as soon as the wait allows and computes the transducer's stage 1
+// (the raw argmax) while A builds. After a pair barrier each warp evaluates
+// half of the columns (lane columns j < 17 / j >= 17) and the two halves'
+// winners are merged through shared memory (R14 order). Used for the
+// transducer modes while there are at most 4 rows per SM (CTC and AED have
+// no stage 1 to overlap: for them the pair's barriers cost more than the
+// halved argmax saves).
+constexpr int kPairSplit = 17;
+
+template <int kMode, bool kTable, bool kPacked, bool kAux>
+__global__ void __launch_bounds__(256, 1)
+    fused_pair_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int32_t B,
+                      int32_t* __restrict__ states, int32_t* __restrict__ prev, const uint8_t* __restrict__ active,
+                      float lambda, int32_t sp, AuxRow aux, Loop lp, int32_t* __restrict__ tokens_out) {
+  constexpr int kW = 8;
+  constexpr bool kTwo = kMode == NGPULM_RNNT || kMode == kLoop;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int32_t V = m.V, ncols = V + 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, pair = w >> 1, role = w & 1, R = blockDim.x >> 6;
+  unsigned char* base = smem + (size_t)pair * (fslice_bytes(V, m.order) + 64);
+  const WSlice s = wcarve(base, V, m.order, 0);
+  uint64_t* lbar = s.abar;
+  float* lbuf = reinterpret_cast<float*>(base + wslice_bytes(V, m.order, 0));
+  volatile int32_t* xch = reinterpret_cast<int32_t*>(base + fslice_bytes(V, m.order));  // exchange words
+  const int32_t row = (int32_t)blockIdx.x * R + pair;
+  const uint32_t bid = 1 + pair;  // named barrier of the pair (0 is __syncthreads)
+  auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bid) : "memory"); };
+  pdl_trigger();
+  if (row >= B) return;
+  if (lane == 0) {  // A: root targets -> next-state slots; B: the logits barrier (model data / no inputs: before the wait)
+    const uint64_t* bb = role == 0 ? s.bar : lbar;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bb)) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (role == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)),
+                   "r"((uint32_t)V * 4u)
+                   : "memory");
+      bulk_g2s(s.row_n, m.arc_to, (uint32_t)V * 4u, s.bar);
+    }
+  }
+  float4 rw[8];
+  if (role == 0) {
+    const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (lane + 32 * j < V / 4) rw[j] = __ldg(w4 + lane + 32 * j);
+  }
+  pdl_wait();
+  const float* lrow = logits + (size_t)row * row_stride;
+  const float* lb = lbuf + (reinterpret_cast<uintptr_t>(lrow) & 15) / 4;  // column c at lb[c]
+  const bool on = kMode == kLoop ? __ldg(&lp.frame[row]) < __ldg(&lp.len[row]) : (!active || __ldg(&active[row]));
+  const int32_t pc = (kMode == NGPULM_CTC) ? __ldg(&prev[row]) : -2;
+  float ilm[kAux ? kMaxColsPerLane : 1];
+  if (kAux) {  // this warp's half of the row's ILM scores
+    const float* arow = aux.p + (size_t)row * aux.stride;
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j) {
+      const int32_t col = lane + 32 * j;
+      ilm[j] = 0.f;
+      if ((j < kPairSplit) == (role == 0) && col < ncols && col != sp) ilm[j] = __ldg(arow + (col - (col > sp)));
+    }
+  }
+  float xs[kMaxColsPerLane];
+  float fin = 0.f;
+  if (role == 1) {
+    if (on) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      issue_frame(lrow, ncols, lbuf, lbar, pol);
+      mbar_wait(lbar, 0);
+#pragma unroll
+      for (int j = 0; j < kMaxColsPerLane; ++j) {
+        const int32_t col = lane + 32 * j;
+        xs[j] = __int_as_float(0x7fc00000);
+        if ((kTwo || j >= kPairSplit) && col < ncols) xs[j] = lb[col];
+      }
+      if (kTwo) {
+        const int32_t rc = warp_argmax_cols(xs);  // stage 1: standard greedy prediction
+        if (lane == 0) xch[2] = rc;
+      }
+    }
+    pair_sync();  // (1) the row is built (or the row is done)
+    if (xch[3]) return;
+    fin = __int_as_float(xch[4]);
+  } else {
+    WLevel lv;
+    int32_t nslots;
+    const Row r = warp_row<kTable>(m, states + row, s, lv, nslots);
+    if (!on || r.bad) {
+      if (lane == 0) {
+        tokens_out[row] = -1;
+        if (on) atomicMin(m.bad_row, (unsigned long long)row);
+        if (kMode == kLoop && on) lp.frame[row] = lp.len[row];
+        xch[3] = 1;
+      }
+      mbar_wait(s.bar, 0);
+      pair_sync();
+      return;
+    }
+    Window<kW, kPacked> a;
+    load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
+    {
+      float4* s4 = reinterpret_cast<float4*>(s.row_s);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (lane + 32 * j < V / 4) {
+          float4 y = rw[j];
+          y.x = __fadd_rn(r.acc_root, y.x);
+          y.y = __fadd_rn(r.acc_root, y.y);
+          y.z = __fadd_rn(r.acc_root, y.z);
+          y.w = __fadd_rn(r.acc_root, y.w);
+          s4[lane + 32 * j] = y;
+        }
+    }
+    mbar_wait(s.bar, 0);
+    __syncwarp();
+    for (int32_t k0 = 0; k0 < nslots;) {
+      write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
+      k0 += kW;
+      if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
+    }
+    fin = r.fin;
+    if (lane == 0) {
+      xch[3] = 0;
+      xch[4] = __float_as_int(r.fin);
+    }
+    pair_sync();  // (1)
+    mbar_wait(lbar, 0);  // the logits (B saw them land; observe the phase here too)
+#pragma unroll
+    for (int j = 0; j < kPairSplit; ++j) {
+      const int32_t col = lane + 32 * j;
+      xs[j] = __int_as_float(0x7fc00000);
+      if (col < ncols) xs[j] = lb[col];
+    }
+  }
+  const int32_t rc = kTwo ? xch[2] : 0;
+  int32_t bc;
+  if (kTwo && rc == sp) {
+    bc = sp;  // stage 1 keeps blank
+    if (role == 1) return;
+  } else {
+    const float sp_val = (kMode == NGPULM_AED) ? fin : 0.f;
+    float val[kMaxColsPerLane];
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j) {
+      const int32_t col = lane + 32 * j;
+      const float x = xs[j];
+      float v = __int_as_float(0x7fc00000);
+      if ((j < kPairSplit) == (role == 0)) {
+        const float lmv = col < ncols && col != sp ? s.row_s[col - (col > sp)] : sp_val;
+        v = __fmaf_rn(lambda, lmv, x);
+        if (kAux && col != sp) v = __fmaf_rn(-aux.lam, ilm[j], v);
+        if (kMode == NGPULM_CTC && (col == sp || col == pc)) v = x;
+        if (kTwo && col == sp) v = __int_as_float(0x7fc00000);
+      }
+      val[j] = v;
+    }
+    float M;
+    const int32_t c = role == 0 ? warp_argmax_range<0, kPairSplit>(val, M)
+                                : warp_argmax_range<kPairSplit, kMaxColsPerLane>(val, M);
+    if (lane == 0) {
+      xch[5 + 2 * role] = __float_as_int(M);
+      xch[6 + 2 * role] = c;
+    }
+    pair_sync();  // (2) both halves' winners
+    if (role == 1) return;
+    const float M1 = __int_as_float(xch[7]);
+    const int32_t c1 = xch[8];
+    bc = (M1 > M || (M1 == M && c1 < c)) ? c1 : c;  // (B's columns are all higher; equal values: lower column)
+  }
+  if (kMode == kLoop) {
+    if (lane == 0) {
+      const bool ok = bc >= 0 && bc < ncols;
+      tokens_out[row] = ok ? bc : -1;
+      int32_t fr = lp.frame[row], sy = lp.sym[row];
+      if (!ok || bc == sp) {
+        ++fr;
+        sy = 0;
+      } else {
+        const int32_t tok = bc < sp ? bc : bc - 1;
+        const int32_t e = lp.emit_len[row];
+        if (e < lp.max_len) lp.emit[(size_t)row * lp.max_len + e] = bc;
+        lp.emit_len[row] = e + 1;
+        if (lp.last) lp.last[row] = tok;
+        states[row] = s.row_n[tok];
+        if (++sy >= lp.max_sym) {
+          ++fr;
+          sy = 0;
+        }
+      }
+      lp.frame[row] = fr;
+      lp.sym[row] = sy;
+    }
+    return;
+  }
+  if (lane == 0) {
+    if (bc < 0 || bc >= ncols) {
+      tokens_out[row] = -1;
+    } else {
+      tokens_out[row] = bc;
+      if (bc == sp) {
+        if (kMode == NGPULM_CTC) prev[row] = -1;
+      } else if (!(kMode == NGPULM_CTC && bc == pc)) {
+        states[row] = s.row_n[bc < sp ? bc : bc - 1];
+        if (kMode == NGPULM_CTC) prev[row] = bc;
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------- fused top-k
@@ -1951,11 +2192,26 @@ int launch_fused_mode(const DevModel& m, const float* logits, int64_t row_stride
                       int32_t* prev, const uint8_t* active, float lambda, int32_t blank, AuxRow aux,
                       int32_t* tokens_out, cudaStream_t st) {
   if (m.V % 4 == 0 && m.V <= 1024 && m.adv_kind != NGPULM_ADVANCE_CTA) {
+    const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
+    if (kMode == NGPULM_RNNT && B <= NGPULM_PAIR_MAX_B) {  // two warps per row (stage 1 beside the row build)
+      int R = (B + 147) / 148;
+      R = R < 1 ? 1 : (R > 4 ? 4 : R);
+      const size_t psm = (size_t)R * (fslice_bytes(m.V, m.order) + 64);
+      const dim3 pg((B + R - 1) / R), pb(64 * R);
+#define NGPULM_PAIR_LAUNCH(T, P)                                                                                  \
+  return aux.p ? launch(fused_pair_kernel<kMode, T, P, true>, pg, pb, psm, st, m, logits, row_stride, B, states,   \
+                        prev, active, lambda, blank, aux, Loop{}, tokens_out)                                      \
+               : launch(fused_pair_kernel<kMode, T, P, false>, pg, pb, psm, st, m, logits, row_stride, B, states,  \
+                        prev, active, lambda, blank, aux, Loop{}, tokens_out)
+      if (table) { if (pk) NGPULM_PAIR_LAUNCH(true, true); NGPULM_PAIR_LAUNCH(true, false); }
+      if (pk) NGPULM_PAIR_LAUNCH(false, true);
+      NGPULM_PAIR_LAUNCH(false, false);
+#undef NGPULM_PAIR_LAUNCH
+    }
     int R = (B + 147) / 148;
     R = R < 1 ? 1 : (R > NGPULM_FUSED_MAX_ROWS ? NGPULM_FUSED_MAX_ROWS : R);
     const size_t wsm = (size_t)R * fslice_bytes(m.V, m.order);
     const dim3 wg((B + R - 1) / R), wb(32 * R);
-    const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
 #define NGPULM_FUSED_LAUNCH(T, P)                                                                                 \
   return aux.p ? launch(fused_warp_kernel<kMode, T, P, true>, wg, wb, wsm, st, m, logits, row_stride, B, states,    \
                         prev, active, lambda, blank, aux, Loop{}, tokens_out)                                       \
@@ -2029,6 +2285,21 @@ int launch_transducer_loop(const DevModel& m, const float* logits, int64_t row_s
   const AuxRow ax{aux, aux_stride, lambda_ilm};
   const Loop lp{frame, sym, lengths, emit, emit_len, last, max_sym, max_len};
   cudaStream_t st = (cudaStream_t)stream;
+  if (B <= NGPULM_PAIR_MAX_B) {  // two warps per row
+    int Rp = (B + 147) / 148;
+    Rp = Rp < 1 ? 1 : (Rp > 4 ? 4 : Rp);
+    const size_t psm = (size_t)Rp * (fslice_bytes(m.V, m.order) + 64);
+    const dim3 pg((B + Rp - 1) / Rp), pb(64 * Rp);
+#define NGPULM_PAIR_LOOP(T, P)                                                                                     \
+  return aux ? launch(fused_pair_kernel<kLoop, T, P, true>, pg, pb, psm, st, m, logits, row_stride, B, states,      \
+                      (int32_t*)nullptr, (const uint8_t*)nullptr, lambda, blank, ax, lp, tokens_out)                \
+             : launch(fused_pair_kernel<kLoop, T, P, false>, pg, pb, psm, st, m, logits, row_stride, B, states,     \
+                      (int32_t*)nullptr, (const uint8_t*)nullptr, lambda, blank, ax, lp, tokens_out)
+    if (table) { if (pk) NGPULM_PAIR_LOOP(true, true); NGPULM_PAIR_LOOP(true, false); }
+    if (pk) NGPULM_PAIR_LOOP(false, true);
+    NGPULM_PAIR_LOOP(false, false);
+#undef NGPULM_PAIR_LOOP
+  }
 #define NGPULM_LOOP_LAUNCH(T, P)                                                                                     \
   return aux ? launch(fused_warp_kernel<kLoop, T, P, true>, wg, wb, wsm, st, m, logits, row_stride, B, states,       \
                       (int32_t*)nullptr, (const uint8_t*)nullptr, lambda, blank, ax, lp, tokens_out)                 \
