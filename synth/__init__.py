@@ -64,6 +64,7 @@ def make_lm(
     minlen: int = 5,
     maxlen: int = 25,
     tag: str | None = None,
+    prune: str | None = None,
 ) -> LMFiles:
     """Generate (deterministically from the arguments) an ARPA LM in out_dir."""
     build_lmgen()
@@ -74,6 +75,8 @@ def make_lm(
            "--seed", str(seed), "--absent", str(absent), "--lexicon", str(lexicon),
            "--minlen", str(minlen), "--maxlen", str(maxlen)]
     corpus = held = None
+    if prune:
+        cmd += ["--prune", prune]
     if corpus_in is not None:
         cmd += ["--corpus-in", corpus_in]
         corpus = corpus_in

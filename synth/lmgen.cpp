@@ -33,6 +33,7 @@
 //         [--corpus-out FILE] [--heldout N --heldout-out FILE]
 //         [--corpus-in FILE]   (use these sentences instead of sampling)
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -190,6 +191,7 @@ void usage() {
 
 int main(int argc, char** argv) {
   std::string arpa_out, corpus_out, heldout_out, corpus_in;
+  std::string prune_arg;  // "t1,t2,...": drop n-grams of order k with count <= t_k (k >= 2)
   int V = 0, order = 0, absent = 1, W = 20000, minlen = 5, maxlen = 25, heldout = 0;
   long long target_tokens = 0;
   uint64_t seed = 1;
@@ -209,6 +211,7 @@ int main(int argc, char** argv) {
     else if (a == "--corpus-in") corpus_in = nxt();
     else if (a == "--heldout") heldout = std::atoi(nxt());
     else if (a == "--heldout-out") heldout_out = nxt();
+    else if (a == "--prune") prune_arg = nxt();
     else usage();
   }
   if (arpa_out.empty() || V <= 0 || order <= 0 || (target_tokens <= 0 && corpus_in.empty())) usage();
@@ -305,6 +308,62 @@ int main(int argc, char** argv) {
     }
   }
 
+  // ---- optional count pruning (the paper's SPGI LM is pruned):
+  // an n-gram of order k >= 2 is dropped when its count <= t_k, unless it is a
+  // prefix of a kept n-gram (ARPA contexts must exist). Kept n-grams keep their
+  // interpolated probability; back-off weights are renormalized so that every
+  // context still sums to one:  bo(c) = (1 - sum_{kept v} P(v|c)) /
+  // (1 - sum_{kept v} Pm(v|c[1:])), Pm = the pruned model's back-off
+  // probability (a missing context contributes a weight of 1, i.e. log 0).
+  // Thresholds that are not monotone (t_2 > t_3) leave kept n-grams whose
+  // suffix was dropped: missing back-off contexts (R7/R8).
+  std::vector<char> keep(nn, 1);
+  std::vector<double> BO(nn, 0.0);  // natural back-off of kept contexts (probability ratio)
+  bool pruned = false;
+  if (!prune_arg.empty()) {
+    std::vector<uint64_t> th(order + 1, 0);
+    size_t pos = 0;
+    for (int k = 1; k <= order && pos <= prune_arg.size(); ++k) {
+      size_t e = prune_arg.find(',', pos);
+      if (e == std::string::npos) e = prune_arg.size();
+      th[k] = std::strtoull(prune_arg.substr(pos, e - pos).c_str(), nullptr, 10);
+      pos = e + 1;
+    }
+    pruned = true;
+    for (int d = order; d >= 2; --d)
+      for (uint32_t n : byd[d]) {
+        if (tr.count[n] <= th[d] && !keep[n]) continue;
+        if (tr.count[n] <= th[d]) keep[n] = 0;
+      }
+    for (int d = order; d >= 2; --d)  // prefix closure
+      for (uint32_t n : byd[d])
+        if (keep[n]) keep[tr.parent[n]] = 1;
+    // Pm(v | context node c): kept (c, v) -> P; else bo(c) * Pm(v | c[1:]); the
+    // suffix context of a node is tr.suf (the node of context[1:], always observed)
+    std::function<double(uint32_t, int32_t)> pm = [&](uint32_t c, int32_t v) -> double {
+      const uint32_t x = tr.get(c, v);
+      if (x != ~0u && keep[x]) return P[x];
+      if (c == 0) return 0.0;  // (children of a context are observed unigrams: not reached)
+      const double b = (keep[c] && BO[c] > 0) ? BO[c] : 1.0;
+      return b * pm(tr.suf[c], v);
+    };
+    std::vector<std::vector<uint32_t>> kids(nn);
+    for (size_t n = 1; n < nn; ++n) kids[tr.parent[n]].push_back((uint32_t)n);
+    for (int d = 1; d < order; ++d)
+      for (uint32_t c : byd[d]) {
+        if (!keep[c]) continue;
+        double num = 1.0, den = 1.0;
+        bool any = false;
+        for (uint32_t x : kids[c]) {
+          if (!keep[x]) continue;
+          any = true;
+          num -= P[x];
+          den -= pm(tr.suf[c], tr.tok[x]);
+        }
+        BO[c] = any ? (den > 1e-12 ? num / den : 1.0) : 1.0;
+      }
+  }
+
   // ---- write ARPA
   FILE* f = std::fopen(arpa_out.c_str(), "w");
   if (!f) { std::perror(arpa_out.c_str()); return 2; }
@@ -316,21 +375,28 @@ int main(int argc, char** argv) {
     else std::sprintf(out, "%d", t);
   };
   std::fprintf(f, "\\data\\\n");
-  for (int d = 1; d <= order; ++d)
-    std::fprintf(f, "ngram %d=%zu\n", d, byd[d].size() + (d == 1 ? 1 : 0));  // + <unk>
+  for (int d = 1; d <= order; ++d) {
+    size_t cnt = 0;
+    for (uint32_t n : byd[d]) cnt += keep[n] ? 1 : 0;
+    std::fprintf(f, "ngram %d=%zu\n", d, cnt + (d == 1 ? 1 : 0));  // + <unk>
+  }
   std::vector<int32_t> tup(order);
   char tb[32];
   for (int d = 1; d <= order; ++d) {
     std::fprintf(f, "\n\\%d-grams:\n", d);
     for (uint32_t n : byd[d]) {
+      if (!keep[n]) continue;
       uint32_t x = n;
       for (int k = d - 1; k >= 0; --k) { tup[k] = tr.tok[x]; x = tr.parent[x]; }
       bool is_bos_unigram = (d == 1 && tr.tok[n] == BOS);
       if (is_bos_unigram) std::fprintf(f, "-99\t");
       else std::fprintf(f, "%.10g\t", std::log10(P[n]));
       for (int k = 0; k < d; ++k) { tokstr(tup[k], tb); std::fprintf(f, k ? " %s" : "%s", tb); }
-      if (d < order && T[n] > 0)
+      if (pruned) {
+        if (d < order && BO[n] > 0 && BO[n] != 1.0) std::fprintf(f, "\t%.10g", std::log10(BO[n]));
+      } else if (d < order && T[n] > 0) {
         std::fprintf(f, "\t%.10g", std::log10((double)T[n] / ((double)C[n] + (double)T[n])));
+      }
       std::fputc('\n', f);
     }
     if (d == 1) std::fprintf(f, "%.10g\t<unk>\n", std::log10(u / ((double)ntok + u)));

@@ -41,6 +41,23 @@ def small_lms(lm_dir):
     return out
 
 
+# count-pruned LMs (lmgen --prune, thresholds per order): non-monotone thresholds
+# drop lower-order n-grams whose extensions survive, so kept n-grams have missing
+# suffix contexts (the SPGI LM of PAPER.md:155 is pruned; readings R7/R8)
+PRUNED_LMS = [
+    ("pr3", 40, 3, 3000, 200, "0,4,0"),
+    ("pr4", 48, 4, 4000, 300, "0,3,0,0"),
+    ("pr6", 32, 6, 3000, 150, "0,2,5,0,1,0"),
+]
+
+
+@pytest.fixture(scope="session")
+def pruned_lms(lm_dir):
+    import synth
+    return {name: synth.make_lm(lm_dir, V, N, tokens=T, seed=3, lexicon=L, heldout=50, tag=name, prune=pr)
+            for name, V, N, T, L, pr in PRUNED_LMS}
+
+
 @pytest.fixture(scope="session")
 def fig1_paths():
     return os.path.join(GOLDEN, "fig1.arpa"), os.path.join(GOLDEN, "fig1.vocab")

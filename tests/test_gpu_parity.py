@@ -369,3 +369,30 @@ def test_tiny_lm_resident_kernel(pairs, B):
     uniq, inv = np.unique(states, return_inverse=True)
     s32, _, n_o, _ = o.rows(uniq, want64=False)
     assert np.array_equal(n, n_o[inv]) and same_bits(s, s32[inv])
+
+
+@pytest.fixture(scope="module")
+def pruned_pairs(pruned_lms):
+    return {n: (ng.load_arpa(f.arpa, vocab_size=f.vocab_size, device=0), Oracle(f.arpa, vocab_size=f.vocab_size), f)
+            for n, f in pruned_lms.items()}
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("chain", [ng.CHAIN_TABLE, ng.CHAIN_WALK])
+@pytest.mark.parametrize("name", ["pr3", "pr4", "pr6"])
+def test_pruned_lms_exhaustive(pruned_pairs, name, chain, kernel):
+    """Count-pruned LMs with missing suffix contexts (R7/R8, the paper's pruned SPGI
+    LM): every state x every token bit-exact vs the oracle, and the fused steps."""
+    m, o, f = pruned_pairs[name]
+    states = np.arange(o.num_states, dtype=np.int32)
+    with using(m, chain, kernel):
+        s, n, fin = gpu_advance(m, states)
+        x = synth.rnnt_logits(o.num_states, 1, o.V, seed=81)[0]
+        steps = [gpu_step(m, mode, x, states, np.full(o.num_states, -1, np.int32) if mode == CTC else None, None, 1.3)
+                 for mode in (CTC, RNNT, AED)]
+    s32, _, n_o, _ = o.rows(states, want64=False)
+    f32, _ = o.finals(states)
+    assert np.array_equal(n, n_o) and same_bits(s, s32) and same_bits(fin, f32)
+    for mode, (tg, sg, _) in zip((CTC, RNNT, AED), steps):
+        to, so, _ = o.fused_step(mode, x, states, prev=np.full(o.num_states, -1) if mode == CTC else None, lam=1.3)
+        assert np.array_equal(tg, to) and np.array_equal(sg, so), mode

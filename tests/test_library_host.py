@@ -133,3 +133,27 @@ def test_touched_bytes(fig1):
     # states 7 (the cat) -> 2 (cat) -> root: 2 state records + 1 + 1 arcs + root arcs + finals
     b = fig1.touched_bytes(np.array([7, 7], dtype=np.int32))
     assert b == 6 * 12 + 2 * 4 + 2 * 16 + 2 * 12
+
+
+@pytest.mark.parametrize("name", ["pr3", "pr4", "pr6"])
+def test_builder_on_pruned_lms(pruned_lms, name):
+    """Pruned ARPAs with missing suffix contexts (R7/R8): the library's arc targets
+    equal the oracle's next ids, its back-off targets are the longest proper suffix
+    that is a state, and state numbering / state_of agree with the oracle."""
+    from oracle import Oracle
+    f = pruned_lms[name]
+    m = ng.load_arpa(f.arpa, vocab_size=f.vocab_size, device=-1)
+    o = Oracle(f.arpa, vocab_size=f.vocab_size)
+    assert m.num_states == o.num_states
+    h = m.host_arrays()
+    off, tok, to, bt = h["arc_offsets"], h["arc_tokens"], h["arc_to_states"], h["boff_to_states"]
+    st = np.arange(o.num_states, dtype=np.int32)
+    _, _, nx, _ = o.rows(st, want64=False)
+    for s in range(o.num_states):
+        for a in range(off[s], off[s + 1]):
+            assert to[a] == nx[s, tok[a]], (s, tok[a])
+        if s == 0:
+            continue
+        ctx = o.context(s)[1:]
+        bos = len(ctx) > 0 and ctx[0] == o.V
+        assert bt[s] == o.state_of(bos, ctx[1:] if bos else ctx), s

@@ -148,3 +148,44 @@ def test_bad_arpa_rejected(tmp_path, fig1_paths):
         p.write_text(t)
         with pytest.raises(ValueError):
             Oracle(str(p), vocab)
+
+
+# ---------------------------------------------------------------- pruned LMs: missing contexts (R7, R8)
+def _arpa_entries(path):
+    ents, sec = set(), 0
+    for line in open(path):
+        line = line.strip()
+        if line.startswith("\\") and line.endswith("-grams:"):
+            sec = int(line[1:].split("-")[0])
+        elif sec and line and not line.startswith("\\"):
+            ents.add(tuple(line.split("\t")[1].split()))
+    return ents
+
+
+@pytest.mark.parametrize("name", ["pr3", "pr4", "pr6"])
+def test_pruned_lms_have_missing_suffixes_and_stay_normalized(pruned_lms, name):
+    """lmgen renormalizes the back-off weights of a pruned LM (its own derivation);
+    the oracle's back-off definition must then still sum to one for every state —
+    with kept n-grams whose suffix context is missing, this pins the oracle's
+    reading of missing contexts (they add log 1 = 0 and the walk goes on to the
+    next shorter suffix, R8) and its arc targets (longest suffix that is a state,
+    R7: replay below)."""
+    f = pruned_lms[name]
+    ents = _arpa_entries(f.arpa)
+    missing = sum(1 for e in ents if len(e) >= 3 and e[1:] not in ents)
+    assert missing > 10, "the thresholds must leave missing suffixes"
+    o = Oracle(f.arpa, vocab_size=f.vocab_size)
+    st = np.arange(o.num_states, dtype=np.int32)
+    s32, s64, nx, lv = o.rows(st)
+    _, f64 = o.finals(st)
+    tot = np.exp(s64).sum(1) + np.exp(f64)
+    assert np.max(np.abs(tot - 1)) < 1e-7
+    assert (lv <= f.order).all()                       # depth bound (PAPER.md:123)
+    # next ids = the state of the longest suffix of context + v (replayed histories)
+    sents = synth.read_sentences(f.heldout)
+    for snt in sents[:20]:
+        s = o.state_of(True, [])
+        for i, v in enumerate(snt):
+            _, _, n1, _ = o.rows(np.array([s], np.int32), want64=False)
+            s = int(n1[0, v])
+            assert s == o.state_of(True, snt[: i + 1])
