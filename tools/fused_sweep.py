@@ -37,4 +37,26 @@ for name, mode, B, gen in (("ctc", ng.CTC, 256, synth.rnnt_logits), ("rnnt", ng.
         s.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3 / n)
     out.append(f"{name}_b{B} {statistics.median(ts):.2f}")
+# CTC frame steps reading [B, T, V+1] logits from HBM (the bench's configs[2] leg)
+B, T = 256, 500
+x = torch.from_numpy(synth.ctc_logits(synth.read_sentences(f.heldout), B, T, V, seed=4)).cuda()
+st = torch.zeros(B, dtype=torch.int32, device="cuda")
+pv = torch.full((B,), -1, dtype=torch.int32, device="cuda")
+fr = torch.empty((T, B), dtype=torch.int32, device="cuda")
+g = torch.cuda.CUDAGraph()
+with torch.cuda.stream(s):
+    for t in range(2):
+        m.fused_greedy_step(ng.CTC, x[:, t], st, prev=pv, lam=0.3, tokens_out=fr[t], stream=s)
+    s.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        for t in range(T):
+            m.fused_greedy_step(ng.CTC, x[:, t], st, prev=pv, lam=0.3, tokens_out=fr[t], stream=s)
+ts = []
+for _ in range(3):
+    with torch.cuda.stream(s):
+        st.zero_(); pv.fill_(-1)
+        e0.record(s); g.replay(); e1.record(s)
+    s.synchronize()
+    ts.append(e0.elapsed_time(e1) * 1e3 / T)
+out.append(f"ctc_hbm_b256 {statistics.median(ts):.2f}")
 print("fused us/step:", " ".join(out), flush=True)
