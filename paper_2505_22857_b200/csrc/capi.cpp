@@ -427,7 +427,8 @@ int ngpulm_advance_host(ngpulm_model* m, const int32_t* states_host, int32_t B, 
   if (B == 0) return NGPULM_OK;
   if (!states_host || !scores_host || !next_host) return err(NGPULM_EUSAGE, "NULL host buffer");
   const size_t V = (size_t)m->h.V;
-  const size_t o_sc = 256, o_nx = align256(o_sc + (size_t)B * V * 4), o_fi = align256(o_nx + (size_t)B * V * 4);
+  const size_t o_sc = align256((size_t)B * 4), o_nx = align256(o_sc + (size_t)B * V * 4),
+               o_fi = align256(o_nx + (size_t)B * V * 4);
   const size_t need = align256(o_fi + (size_t)B * 4);
   std::lock_guard<std::mutex> lk(m->mu);
   if (m->scratch_bytes < need) {

@@ -450,6 +450,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #define NGPULM_PAIR_MAX_B (4 * 148)  // transducer steps: two warps per row up to 4 rows per SM (measured:
                                      // RNN-T B=512 4.36 -> 4.00 us; CTC/AED lose, they keep one warp)
 #endif
+#ifndef NGPULM_SPECULATE
+#define NGPULM_SPECULATE 1
+#endif
 #ifndef NGPULM_FUSED_MAX_ROWS
 #define NGPULM_FUSED_MAX_ROWS 8
 #endif
@@ -717,7 +720,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // level into the warp's staging area (when they fit), so the gathers do not
 // queue in the SM's load pipeline; the write loop then reads shared memory.
 template <bool kTable, int kW, bool kPacked, bool kRegRoot, bool kStage>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, kW == 8 ? 2 : 1)  // 8-slot windows: more than one wave, 2 CTAs per SM
     advance_warp_kernel(DevModel m, const int32_t* __restrict__ states, int32_t B, float* __restrict__ scores,
                         int32_t* __restrict__ next, float* __restrict__ final_out) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -778,100 +781,143 @@ __global__ void __launch_bounds__(256, 1)
     for (int j = 0; j < 8; ++j)
       if (lane + 32 * j < V / 4) dst[lane + 32 * j] = src[lane + 32 * j];
   }
-  pdl_wait();
-  STAMP(2);
   if (row >= B) return;  // warp 0 always has a row and waits for the CTA's bulk copy
 #ifdef NGPULM_PHASE_TIMING
   const int skip = g_skip;
 #else
   constexpr int skip = 0;
 #endif
-  WLevel lv;
-  int32_t nslots;
-  const Row r = warp_row<kTable>(m, states + row, s, lv, nslots);
-  STAMP(11);
   float* srow = scores + (size_t)row * V;
   int32_t* nrow = next + (size_t)row * V;
+  // Steps 1-3 for state st into shared memory (nothing global is written).
+  // ph: parity of this build's mbarrier phases (0: first build, 1: rebuild).
+  auto build = [&](int32_t st, uint32_t ph) -> Row {
+    WLevel lv;
+    int32_t nslots;
+    const Row r = warp_row_src<kTable>(m, ValState{st}, s, lv, nslots);
+    STAMP(11);
+    if (r.bad) return r;
+    STAMP(3);
+    Window<kW, kPacked> a;
+    bool staged = false;
+    if (kStage) {
+      // staging offsets: levels in slot order (the last level first), packed tight
+      const int32_t nq = lv.info & 0xffff;
+      int32_t inc = nq;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_down_sync(kFull, inc, o);
+        if (lane + o < 32) inc += y;
+      }
+      const int32_t total = __shfl_sync(kFull, inc, 0);
+      staged = total <= kSQ && !(skip & 4);
+      if (staged) {
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.abar)),
+                       "r"((uint32_t)total * 32u)
+                       : "memory");
+        __syncwarp();
+        const int32_t off = inc - nq;
+        if (nq > 0)  // lanes 1..nlev: one bulk copy per level
+          bulk_g2s(s.st_q + 2 * off, reinterpret_cast<const uint4*>(m.arc_q) + 2 * (lv.beg >> 2),
+                   (uint32_t)nq * 32u, s.abar);
+        lv.qbase = off;
+      }
+    }
+    if (kRegRoot) {
+      if (skip & 4) nslots = 0;
+      if (!staged && !(skip & 4)) load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
+      STAMP(12);
+      if (!(skip & 8)) {  // root scores: acc_root + root weight, while the gathers fly
+        float4* s4 = reinterpret_cast<float4*>(s.row_s);
+        const float ar = r.acc_root;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (lane + 32 * j < V / 4) {
+            float4 y = rw[j];
+            y.x = __fadd_rn(ar, y.x);
+            y.y = __fadd_rn(ar, y.y);
+            y.z = __fadd_rn(ar, y.z);
+            y.w = __fadd_rn(ar, y.w);
+            s4[lane + 32 * j] = y;
+          }
+      }
+    } else {
+      mbar_wait(bar, 0);  // the CTA's root weights have landed (long ago, normally)
+      // the root fill goes first: its shared-memory loads would otherwise return
+      // behind the arc gathers
+      if (!(skip & 8)) root_fill(s, root_w, r.acc_root, V);
+      STAMP(12);
+      if (skip & 4) nslots = 0;
+      if (!(skip & 4)) load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
+    }
+    STAMP(4);
+    if (!kCtaRoot) mbar_wait(s.bar, ph);  // root targets in row_n (kCtaRoot: copied synchronously)
+    __syncwarp();
+    STAMP(5);
+    if (staged) {
+      mbar_wait(s.abar, ph);  // the row's arcs are in the staging area
+      for (int32_t k0 = 0; k0 < nslots; k0 += kW) {
+        load_window<kW, kPacked, true>(m, s, lv, r.nlev, k0, nslots, a);
+        write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
+      }
+    } else {
+      for (int32_t k0 = 0; k0 < nslots;) {
+        write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
+        k0 += kW;
+        if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
+      }
+    }
+    return r;
+  };
+  // Speculative build: the row only needs the model (immutable)
+  // and the row's state, so it is built from the state read BEFORE
+  // griddepcontrol.wait — overlapping the previous kernel — and the state is
+  // read again after the wait; only if it changed (the previous kernel wrote
+  // it) is the row rebuilt. Outputs are written after the wait only. Both
+  // reads are coherent (ld.relaxed.gpu: no stale non-coherent cache line).
+  auto load_state = [&]() {
+    int32_t v = 0;
+    if (lane == 0) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(states + row) : "memory");
+    return __shfl_sync(kFull, v, 0);
+  };
+  bool waited = !NGPULM_SPECULATE;
+  if (waited) pdl_wait();
+  int32_t st = load_state();
+  uint32_t ph = 0;
+  Row r;
+  for (;;) {  // one build site: at most two passes
+    r = build(st, ph);
+    if (r.bad && !kCtaRoot) mbar_wait(s.bar, ph);  // the phase is over before any re-arm
+    if (waited) break;
+    pdl_wait();
+    waited = true;
+    STAMP(2);
+    const int32_t st1 = load_state();
+    if (st1 == st) break;
+    st = st1;  // the previous kernel changed the state: rebuild after the wait
+    ph = 1;
+    if (kCtaRoot) {  // the root targets again (the first build overwrote them)
+      const int4* src = reinterpret_cast<const int4*>(root_w);
+      int4* dst = reinterpret_cast<int4*>(s.row_n);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (lane + 32 * j < V / 4) dst[lane + 32 * j] = src[lane + 32 * j];
+    } else if (lane == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)), "r"(bytes)
+                   : "memory");
+      bulk_g2s(s.row_n, m.arc_to, bytes, s.bar);
+    }
+    __syncwarp();
+  }
   if (lane == 0) {
     if (r.bad) atomicMin(m.bad_row, (unsigned long long)row);
     if (final_out) final_out[row] = r.bad ? __int_as_float(0x7fc00000) : r.fin;
   }
   if (r.bad) {
     for (int32_t v = lane; v < V; v += 32) { srow[v] = __int_as_float(0x7fc00000); nrow[v] = -1; }
-    mbar_wait(s.bar, 0);  // no exit with a bulk copy in flight
     if (w == 0 && !kRegRoot) mbar_wait(bar, 0);
     return;
-  }
-  STAMP(3);
-  Window<kW, kPacked> a;
-  bool staged = false;
-  if (kStage) {
-    // staging offsets: levels in slot order (the last level first), packed tight
-    const int32_t nq = lv.info & 0xffff;
-    int32_t inc = nq;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int32_t y = __shfl_down_sync(kFull, inc, o);
-      if (lane + o < 32) inc += y;
-    }
-    const int32_t total = __shfl_sync(kFull, inc, 0);
-    staged = total <= kSQ && !(skip & 4);
-    if (staged) {
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.abar)),
-                     "r"((uint32_t)total * 32u)
-                     : "memory");
-      __syncwarp();
-      const int32_t off = inc - nq;
-      if (nq > 0)  // lanes 1..nlev: one bulk copy per level
-        bulk_g2s(s.st_q + 2 * off, reinterpret_cast<const uint4*>(m.arc_q) + 2 * (lv.beg >> 2), (uint32_t)nq * 32u,
-                 s.abar);
-      lv.qbase = off;
-    }
-  }
-  if (kRegRoot) {
-    if (skip & 4) nslots = 0;
-    if (!staged && !(skip & 4)) load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
-    STAMP(12);
-    if (!(skip & 8)) {  // root scores: acc_root + root weight, while the gathers fly
-      float4* s4 = reinterpret_cast<float4*>(s.row_s);
-      const float ar = r.acc_root;
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (lane + 32 * j < V / 4) {
-          float4 y = rw[j];
-          y.x = __fadd_rn(ar, y.x);
-          y.y = __fadd_rn(ar, y.y);
-          y.z = __fadd_rn(ar, y.z);
-          y.w = __fadd_rn(ar, y.w);
-          s4[lane + 32 * j] = y;
-        }
-    }
-  } else {
-    mbar_wait(bar, 0);  // the CTA's root weights have landed (long ago, normally)
-    // the root fill goes first: its shared-memory loads would otherwise return
-    // behind the arc gathers
-    if (!(skip & 8)) root_fill(s, root_w, r.acc_root, V);
-    STAMP(12);
-    if (skip & 4) nslots = 0;
-    if (!(skip & 4)) load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
-  }
-  STAMP(4);
-  mbar_wait(s.bar, 0);  // root targets in row_n
-  __syncwarp();
-  STAMP(5);
-  if (staged) {
-    mbar_wait(s.abar, 0);  // the row's arcs are in the staging area
-    for (int32_t k0 = 0; k0 < nslots; k0 += kW) {
-      load_window<kW, kPacked, true>(m, s, lv, r.nlev, k0, nslots, a);
-      write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
-    }
-  } else {
-    for (int32_t k0 = 0; k0 < nslots;) {
-      write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
-      k0 += kW;
-      if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
-    }
   }
   STAMP(6);
   // step 4: the row leaves by two bulk stores issued by lane 0

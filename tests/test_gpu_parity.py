@@ -396,3 +396,46 @@ def test_pruned_lms_exhaustive(pruned_pairs, name, chain, kernel):
     for mode, (tg, sg, _) in zip((CTC, RNNT, AED), steps):
         to, so, _ = o.fused_step(mode, x, states, prev=np.full(o.num_states, -1) if mode == CTC else None, lam=1.3)
         assert np.array_equal(tg, to) and np.array_equal(sg, so), mode
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_speculative_build_states_written_by_previous_kernel(lm6, graph):
+    """The advance kernel builds each row from the state read before
+    griddepcontrol.wait and re-reads it after the wait. Here the
+    previous kernel (a fused RNN-T step, launched with PDL) rewrites the states in
+    place right before every advance, so the early read can be stale: the rows
+    must still be those of the new states."""
+    m, o, f = lm6
+    B, K = 512, 6
+    st0, _ = trajectory_states(m, f, B, seed=91)
+    xs = torch.from_numpy(synth.rnnt_logits(B, K, m.V, seed=92)).to(dev())
+    st = torch.from_numpy(st0.copy()).to(dev())
+    sc = torch.empty((K, B, m.V), dtype=torch.float32, device=dev())
+    nx = torch.empty((K, B, m.V), dtype=torch.int32, device=dev())
+    snap = torch.empty((K, B), dtype=torch.int32, device=dev())
+    s = torch.cuda.Stream()
+
+    def seq():
+        for k in range(K):
+            m.fused_greedy_step(RNNT, xs[k], st, lam=0.3, stream=s)
+            m.advance(st, sc[k], nx[k], want_final=False, stream=s)
+            snap[k].copy_(st)
+    with torch.cuda.stream(s):
+        if graph:
+            g = torch.cuda.CUDAGraph()
+            seq()  # warm-up, then replay from the same start
+            s.synchronize()
+            st.copy_(torch.from_numpy(st0))
+            with torch.cuda.graph(g, stream=s):
+                seq()
+            st.copy_(torch.from_numpy(st0))
+            g.replay()
+        else:
+            seq()
+    s.synchronize()
+    snap_np, sc_np, nx_np = snap.cpu().numpy(), sc.cpu().numpy(), nx.cpu().numpy()
+    assert (snap_np[0] != st0).any()  # the steps did change states
+    for k in range(K):
+        rows = np.arange(k, B, 37)
+        s32, _, n_o, _ = o.rows(snap_np[k, rows], want64=False)
+        assert np.array_equal(nx_np[k, rows], n_o) and same_bits(sc_np[k, rows], s32), k
