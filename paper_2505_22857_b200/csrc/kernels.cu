@@ -453,11 +453,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #ifndef NGPULM_SPECULATE
 #define NGPULM_SPECULATE 1
 #endif
+#ifndef NGPULM_WIDE_ROWS
+#define NGPULM_WIDE_ROWS 1  // one row per CTA (B=1024: 3.29 -> 2.99 us): a CTA leaves as soon as its row is stored,
+#endif                      // and the next call's CTA takes its place and starts its speculative build
+#ifndef NGPULM_NARROW_ROWS
+#define NGPULM_NARROW_ROWS 1  // B > 1184: 10.14 -> 9.47 us at B=4096
+#endif
 #ifndef NGPULM_FUSED_MAX_ROWS
 #define NGPULM_FUSED_MAX_ROWS 8
 #endif
 #ifndef NGPULM_CTA_ROOT
-#define NGPULM_CTA_ROOT 1  // the 16-slot path (148 < B <= 1184): measured 3.74 -> 3.64 us at B = 1024
+#define NGPULM_CTA_ROOT 0  // (with 7 rows per CTA: 3.74 -> 3.64 us at B = 1024; with one row per CTA: 2.83 vs 3.00)
 #endif
 #ifndef NGPULM_WIDE_MAX_B
 #define NGPULM_WIDE_MAX_B (8 * 148)  // up to 8 rows per SM: 16-slot windows (measured)
@@ -2196,6 +2202,7 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
     const int sq = stage ? kStageQuads : 0;
     int R = (B + 147) / 148;
     R = R < 1 ? 1 : (R > 8 ? 8 : R);
+    if (R > (wide ? NGPULM_WIDE_ROWS : NGPULM_NARROW_ROWS)) R = wide ? NGPULM_WIDE_ROWS : NGPULM_NARROW_ROWS;
     while (R > 1 && wcta_smem(m.V, m.order, R, sq) > 227 * 1024) --R;
     if (wcta_smem(m.V, m.order, R, sq) <= 227 * 1024) {
       const size_t wsm = wcta_smem(m.V, m.order, R, sq);
