@@ -459,6 +459,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #ifndef NGPULM_NARROW_ROWS
 #define NGPULM_NARROW_ROWS 1  // B > 1184: 10.14 -> 9.47 us at B=4096
 #endif
+#ifndef NGPULM_TINY_ROWS
+#define NGPULM_TINY_ROWS 8
+#endif
 #ifndef NGPULM_FUSED_MAX_ROWS
 #define NGPULM_FUSED_MAX_ROWS 8
 #endif
@@ -1013,18 +1016,74 @@ __global__ void __launch_bounds__(256, 1)
     for (int j = 0; j < 8; ++j)
       if (lane + 32 * j < V / 4) dst[lane + 32 * j] = src[lane + 32 * j];
   }
-  pdl_wait();
   if (row >= B) return;  // warp 0 of every CTA has a row (and waited for the CTA's copy)
-  // the row's state and its chain-table record (lane l+1 = level l), from shared memory
-  const int32_t st = __shfl_sync(kFull, lane == 0 ? __ldg(states + row) : 0, 0);
   float* srow = scores + (size_t)row * V;
   int32_t* nrow = next + (size_t)row * V;
-  const bool bad = st < 0 || st >= m.S;
-  int4 x = make_int4(0, 0, 0, 0);
-  if (!bad && lane < m.chain_slots) x = chain_s[(size_t)st * m.chain_slots + lane];
-  const int32_t nlev = __shfl_sync(kFull, x.x, 0);
-  const float acc_root = __int_as_float(__shfl_sync(kFull, x.y, 0));
-  const float fin = __int_as_float(__shfl_sync(kFull, x.z, 0));
+  // the row for state st from the shared copies (speculatively before the wait, as advance_warp_kernel)
+  auto build = [&](int32_t st, bool& bad, float& fin) {
+    bad = st < 0 || st >= m.S;
+    int4 x = make_int4(0, 0, 0, 0);
+    if (!bad && lane < m.chain_slots) x = chain_s[(size_t)st * m.chain_slots + lane];
+    const int32_t nlev = __shfl_sync(kFull, x.x, 0);
+    const float acc_root = __int_as_float(__shfl_sync(kFull, x.y, 0));
+    fin = __int_as_float(__shfl_sync(kFull, x.z, 0));
+    if (bad) return;
+    WLevel lv;
+    lv.beg = 0; lv.qbase = 0; lv.info = 0; lv.eslot = INT_MAX; lv.acc = 0.f;
+    if (lane >= 1 && lane <= nlev) {
+      lv.beg = x.x;
+      lv.acc = __int_as_float(x.z);
+      lv.info = x.w;
+      lv.eslot = (lv.info >> 16) + (((lv.info & 0xffff) + 31) >> 5);
+    }
+    lv.qbase = lv.beg >> 2;
+    const int32_t nslots = nlev > 0 ? __shfl_sync(kFull, lv.eslot, 1) : 0;
+    Window<kW, true> a;
+    load_window<kW, true, true>(m, s, lv, nlev, 0, nslots, a);
+    {  // root scores: acc_root + root weight
+      float4* s4 = reinterpret_cast<float4*>(s.row_s);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (lane + 32 * j < V / 4) {
+          float4 y = rw[j];
+          y.x = __fadd_rn(acc_root, y.x);
+          y.y = __fadd_rn(acc_root, y.y);
+          y.z = __fadd_rn(acc_root, y.z);
+          y.w = __fadd_rn(acc_root, y.w);
+          s4[lane + 32 * j] = y;
+        }
+    }
+    __syncwarp();
+    for (int32_t k0 = 0; k0 < nslots;) {
+      write_window<kW, true>(s, a, k0, nslots, m.pk_bits);
+      k0 += kW;
+      if (k0 < nslots) load_window<kW, true, true>(m, s, lv, nlev, k0, nslots, a);
+    }
+  };
+  auto load_state = [&]() {
+    int32_t v = 0;
+    if (lane == 0) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(states + row) : "memory");
+    return __shfl_sync(kFull, v, 0);
+  };
+  bool waited = !NGPULM_SPECULATE, bad = false;
+  float fin = 0.f;
+  if (waited) pdl_wait();
+  int32_t st = load_state();
+  for (;;) {
+    build(st, bad, fin);
+    if (waited) break;
+    pdl_wait();
+    waited = true;
+    const int32_t st1 = load_state();
+    if (st1 == st) break;
+    st = st1;  // rebuild: the root targets again (the first build overwrote them)
+    const int4* src = reinterpret_cast<const int4*>(root_to);
+    int4* dst = reinterpret_cast<int4*>(s.row_n);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (lane + 32 * j < V / 4) dst[lane + 32 * j] = src[lane + 32 * j];
+    __syncwarp();
+  }
   if (lane == 0) {
     if (bad) atomicMin(m.bad_row, (unsigned long long)row);
     if (final_out) final_out[row] = bad ? __int_as_float(0x7fc00000) : fin;
@@ -1032,37 +1091,6 @@ __global__ void __launch_bounds__(256, 1)
   if (bad) {
     for (int32_t v = lane; v < V; v += 32) { srow[v] = __int_as_float(0x7fc00000); nrow[v] = -1; }
     return;
-  }
-  WLevel lv;
-  lv.beg = 0; lv.qbase = 0; lv.info = 0; lv.eslot = INT_MAX; lv.acc = 0.f;
-  if (lane >= 1 && lane <= nlev) {
-    lv.beg = x.x;
-    lv.acc = __int_as_float(x.z);
-    lv.info = x.w;
-    lv.eslot = (lv.info >> 16) + (((lv.info & 0xffff) + 31) >> 5);
-  }
-  lv.qbase = lv.beg >> 2;
-  const int32_t nslots = nlev > 0 ? __shfl_sync(kFull, lv.eslot, 1) : 0;
-  Window<kW, true> a;
-  load_window<kW, true, true>(m, s, lv, nlev, 0, nslots, a);
-  {  // root scores: acc_root + root weight
-    float4* s4 = reinterpret_cast<float4*>(s.row_s);
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (lane + 32 * j < V / 4) {
-        float4 y = rw[j];
-        y.x = __fadd_rn(acc_root, y.x);
-        y.y = __fadd_rn(acc_root, y.y);
-        y.z = __fadd_rn(acc_root, y.z);
-        y.w = __fadd_rn(acc_root, y.w);
-        s4[lane + 32 * j] = y;
-      }
-  }
-  __syncwarp();
-  for (int32_t k0 = 0; k0 < nslots;) {
-    write_window<kW, true>(s, a, k0, nslots, m.pk_bits);
-    k0 += kW;
-    if (k0 < nslots) load_window<kW, true, true>(m, s, lv, nlev, k0, nslots, a);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
@@ -2181,7 +2209,7 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
     // tiny LM: model resident in every CTA's shared memory
     const size_t mb = tiny_model_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes, m.V);
     int R = (B + 147) / 148;
-    R = R < 1 ? 1 : (R > 8 ? 8 : R);
+    R = R < 1 ? 1 : (R > NGPULM_TINY_ROWS ? NGPULM_TINY_ROWS : R);
     while (R > 1 && mb + (size_t)R * wslice_bytes(m.V, m.order, 0) > 227 * 1024) --R;
     const size_t tsm = mb + (size_t)R * wslice_bytes(m.V, m.order, 0);
     if (tsm <= 227 * 1024) {
