@@ -453,12 +453,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #ifndef NGPULM_SPECULATE
 #define NGPULM_SPECULATE 1
 #endif
-#ifndef NGPULM_WIDE_ROWS
-#define NGPULM_WIDE_ROWS 1  // one row per CTA (B=1024: 3.29 -> 2.99 us): a CTA leaves as soon as its row is stored,
-#endif                      // and the next call's CTA takes its place and starts its speculative build
-#ifndef NGPULM_NARROW_ROWS
-#define NGPULM_NARROW_ROWS 1  // B > 1184: 10.14 -> 9.47 us at B=4096
-#endif
+// launch bounds of the warp advance kernel: with one row per CTA (32
+// threads), the minimum CTAs per SM sets the register budget
+// (one warp per CTA; 8-slot windows and the staged path: 16 CTAs per SM =
+// 128 registers, measured B=4096 9.46 -> 8.16 us, B=128 1.90 -> 1.66 us;
+// the 16-slot path keeps its 245 registers: capped it spills, B=1024 2.82 -> 4.29)
+#define NGPULM_ADV_MINB(kW, kPacked, kStage) ((kStage) ? 16 : (kW) == 8 ? ((kPacked) ? 16 : 10) : 8)
 #ifndef NGPULM_TINY_ROWS
 #define NGPULM_TINY_ROWS 8
 #endif
@@ -729,7 +729,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // level into the warp's staging area (when they fit), so the gathers do not
 // queue in the SM's load pipeline; the write loop then reads shared memory.
 template <bool kTable, int kW, bool kPacked, bool kRegRoot, bool kStage>
-__global__ void __launch_bounds__(256, kW == 8 ? 2 : 1)  // 8-slot windows: more than one wave, 2 CTAs per SM
+__global__ void __launch_bounds__(32, NGPULM_ADV_MINB(kW, kPacked, kStage))
     advance_warp_kernel(DevModel m, const int32_t* __restrict__ states, int32_t B, float* __restrict__ scores,
                         int32_t* __restrict__ next, float* __restrict__ final_out) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -2228,10 +2228,10 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
     const bool wide = B <= NGPULM_WIDE_MAX_B, pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO;
     const bool small_v = m.V <= 1024, stage = B >= 2 && B <= NGPULM_STAGE_MAX_B && pk && small_v && table;
     const int sq = stage ? kStageQuads : 0;
-    int R = (B + 147) / 148;
-    R = R < 1 ? 1 : (R > 8 ? 8 : R);
-    if (R > (wide ? NGPULM_WIDE_ROWS : NGPULM_NARROW_ROWS)) R = wide ? NGPULM_WIDE_ROWS : NGPULM_NARROW_ROWS;
-    while (R > 1 && wcta_smem(m.V, m.order, R, sq) > 227 * 1024) --R;
+    // one row (warp) per CTA: a CTA leaves as soon as its row is stored and the
+    // next call's CTA starts its speculative build in its place (B=1024: 7 rows
+    // per CTA 3.29 us, 1 row 2.83 us; B=4096: 10.1 -> 9.4 us)
+    const int R = 1;
     if (wcta_smem(m.V, m.order, R, sq) <= 227 * 1024) {
       const size_t wsm = wcta_smem(m.V, m.order, R, sq);
       const dim3 wg((B + R - 1) / R), wb(32 * R);
