@@ -384,19 +384,21 @@ def advance_variants(m, states, scores, nxt, fin, R, stream):
 
 def tiny_lm_variant(workdir, dev, stream):
     """A keyword-biasing-sized LM (a 200-keyword LM; here a 3-gram from
-    600 corpus tokens, V=1024, ~800 states): advance at B=1024 with the model resident
-    in shared memory (AUTO) vs read from global memory (WARP)."""
+    600 corpus tokens, V=1024, ~800 states): advance at B=128 with the model resident
+    in shared memory (AUTO selects it up to one row per SM) vs read from global memory
+    (WARP), and at B=1024 (AUTO: the global one-row-per-CTA kernel)."""
     import torch
     import paper_2505_22857_b200 as ng
     import synth
     f = synth.make_lm(workdir + "_tiny", V, 3, tokens=600, seed=11, heldout=200, tag="tiny_bias")
     m = ng.load_arpa(f.arpa, vocab_size=V, device=dev.index)
-    B, R = 1024, 32
-    st = torch.from_numpy(synth.uniform_states(m.num_states, B * R, seed=12).reshape(R, B)).to(dev)
-    sc = torch.empty((R, B, V), dtype=torch.float32, device=dev)
-    nx = torch.empty((R, B, V), dtype=torch.int32, device=dev)
+    R = 32
     out = {"tiny_lm_states": m.num_states, "tiny_resident": int(m.info.tiny_resident)}
-    for name, kind in (("tiny_lm_b1024_smem_us", ng.ADVANCE_AUTO), ("tiny_lm_b1024_global_us", ng.ADVANCE_WARP)):
+    for name, B, kind in (("tiny_lm_b128_smem_us", 128, ng.ADVANCE_AUTO), ("tiny_lm_b128_global_us", 128, ng.ADVANCE_WARP),
+                          ("tiny_lm_b1024_auto_us", 1024, ng.ADVANCE_AUTO)):
+        st = torch.from_numpy(synth.uniform_states(m.num_states, B * R, seed=12).reshape(R, B)).to(dev)
+        sc = torch.empty((R, B, V), dtype=torch.float32, device=dev)
+        nx = torch.empty((R, B, V), dtype=torch.int32, device=dev)
         m.set_advance_kernel(kind)
 
         def calls():

@@ -459,6 +459,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 // 128 registers, measured B=4096 9.46 -> 8.16 us, B=128 1.90 -> 1.66 us;
 // the 16-slot path keeps its 245 registers: capped it spills, B=1024 2.82 -> 4.29)
 #define NGPULM_ADV_MINB(kW, kPacked, kStage) ((kStage) ? 16 : (kW) == 8 ? ((kPacked) ? 16 : 10) : 8)
+#ifndef NGPULM_TINY_MAX_B
+#define NGPULM_TINY_MAX_B 148  // tiny LM in shared memory up to one row per SM (B=128: 1.34 vs 1.66 us);
+#endif                         // beyond, the one-row-per-CTA global kernel wins (B=1024: 2.53 vs 3.08)
 #ifndef NGPULM_TINY_ROWS
 #define NGPULM_TINY_ROWS 8
 #endif
@@ -2205,7 +2208,7 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
   const bool vec = (m.V % 4 == 0) && ((uintptr_t)scores % 16 == 0) && ((uintptr_t)next % 16 == 0);
   const bool table = m.chain != nullptr;
   cudaStream_t st = (cudaStream_t)stream;
-  if (vec && table && m.tiny_chain_bytes > 0 && m.adv_kind == NGPULM_ADVANCE_AUTO) {
+  if (vec && table && m.tiny_chain_bytes > 0 && m.adv_kind == NGPULM_ADVANCE_AUTO && B <= NGPULM_TINY_MAX_B) {
     // tiny LM: model resident in every CTA's shared memory
     const size_t mb = tiny_model_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes, m.V);
     int R = (B + 147) / 148;

@@ -354,7 +354,7 @@ def test_vocab_tiled_unaligned_v(lm_dir):
     assert np.array_equal(n, n_o) and same_bits(s, s32)
 
 
-@pytest.mark.parametrize("B", [7, 600, 1024, 3000])
+@pytest.mark.parametrize("B", [7, 100, 148, 600, 3000])
 def test_tiny_lm_resident_kernel(pairs, B):
     """SURVEY.md §8(f) f4 tiny-LM path: a keyword-biasing-sized LM is answered from
     a copy in every CTA's shared memory (AUTO) — bit-identical to the global-memory
