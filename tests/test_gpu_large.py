@@ -105,3 +105,27 @@ def test_config4_advance_b4096_sharded_and_replica(lm10):
     s2, n2, f2 = gpu_advance(r, states)
     assert same_bits(s2, s) and np.array_equal(n2, n) and same_bits(f2, fin)
     assert m.check() == -1
+
+
+def test_config3_label_looping_decode_b512(lm8):
+    """configs[3] end to end: label-looping greedy transducer decoding with fusion
+    (B=512 utterances, 8-gram ~4.9M n-grams, lambda=0.3) through the CUDA-graph
+    driver, against the oracle's frame-by-frame loop on sampled utterances."""
+    from paper_2505_22857_b200.decode import transducer_greedy_decode
+    m, o, f = lm8
+    B = 512
+    lengths = np.random.default_rng(41).integers(20, 60, size=B).astype(np.int32)
+    seed, temp, bias = 8080, 8.0, 0.75
+
+    def joint(frame, u, last, out):
+        synth.joint_gpu(seed, frame, u, last, out, temperature=temp, blank=m.V, blank_bias=bias)
+    res = transducer_greedy_decode(m, joint, torch.from_numpy(lengths).to(dev()), lam=0.3, max_symbols=10)
+    torch.cuda.synchronize()
+    rows = np.arange(0, B, 32)
+    eo, elo, so = o.transducer_decode(seed, lengths[rows], np.zeros(rows.size, np.int32), lam=0.3, max_symbols=10,
+                                      temperature=temp, max_len=res.emitted.shape[1], blank_bias=bias)
+    em, el, st = res.emitted.cpu().numpy()[rows], res.emit_len.cpu().numpy()[rows], res.states.cpu().numpy()[rows]
+    assert np.array_equal(el, elo) and np.array_equal(st, so)
+    for i in range(rows.size):
+        assert np.array_equal(em[i, : el[i]], eo[i, : el[i]])
+    assert el.sum() > 0
