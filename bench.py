@@ -293,6 +293,17 @@ def run_ours(args):
     e2e = {"value": world * B * V * Ke / (ms_e / 1e3), "unit": "queries/s",
            "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": 8 * B * V + 4 * B, "steps": Ke}
 
+    # per-rank results to every rank (BASELINE north_star: "NCCL is used only to gather
+    # per-rank results"): outside the timed region, never part of the metric
+    gather = None
+    if world > 1:
+        from paper_2505_22857_b200.dist import gather_rows
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        allfin = gather_rows(fin[(K - 1) % R].contiguous(), device=dev)
+        torch.cuda.synchronize(dev)
+        gather = {"what": "final weights of each rank's last step ([B] f32 per rank), all_gather over NCCL",
+                  "rows": int(allfin.shape[0]), "us": (time.perf_counter() - t0) * 1e6}
     variants = advance_variants(m, states, scores, nxt, fin, R, stream)
     variants.update(tiny_lm_variant(f"{args.workdir}_r{rank}", dev, stream))
     fused = {}
@@ -334,6 +345,7 @@ def run_ours(args):
         "e2e": e2e,
         "clocks": sampler.summary(),
         "advance_us_per_call": variants,
+        "results_gather": gather,
         "fused_step_us": fused,
         "cpu_baseline": cpu,
     }
