@@ -298,12 +298,16 @@ def run_ours(args):
     gather = None
     if world > 1:
         from paper_2505_22857_b200.dist import gather_rows
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
         torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
+        g0.record()
         allfin = gather_rows(fin[(K - 1) % R].contiguous(), device=dev)
+        g1.record()
         torch.cuda.synchronize(dev)
         gather = {"what": "final weights of each rank's last step ([B] f32 per rank), all_gather over NCCL",
-                  "rows": int(allfin.shape[0]), "us": (time.perf_counter() - t0) * 1e6}
+                  "rows": int(allfin.shape[0]), "us": max_over_ranks(g0.elapsed_time(g1), dev) * 1e3,
+                  "timing": "CUDA events on the current stream, max over ranks"}
     variants = advance_variants(m, states, scores, nxt, fin, R, stream)
     variants.update(tiny_lm_variant(f"{args.workdir}_r{rank}", dev, stream))
     fused = {}
