@@ -129,3 +129,23 @@ def test_config3_label_looping_decode_b512(lm8):
     for i in range(rows.size):
         assert np.array_equal(em[i, : el[i]], eo[i, : el[i]])
     assert el.sum() > 0
+
+
+def test_config4_binary_reload(lm10, tmp_path):
+    """f4: the 20M-n-gram model saved as NGLM and reloaded without the ARPA parse
+    answers bit-identically (and loads several times faster than the ARPA)."""
+    import time
+    m, o, f = lm10
+    p = str(tmp_path / "lm10.nglm")
+    m.save(p)
+    t0 = time.perf_counter()
+    r = ng.load_binary(p, device=0)
+    t_bin = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ng.load_arpa(f.arpa, vocab_size=1024, device=-1)
+    t_arpa = time.perf_counter() - t0
+    states, _ = trajectory_states(m, f, 1024, seed=33)
+    a, b = gpu_advance(m, states), gpu_advance(r, states)
+    assert same_bits(a[0], b[0]) and np.array_equal(a[1], b[1]) and same_bits(a[2], b[2])
+    print(f"NGLM reload {t_bin:.1f} s (incl. upload) vs ARPA parse+build {t_arpa:.1f} s (host only)")
+    assert t_bin < t_arpa
