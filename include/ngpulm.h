@@ -160,7 +160,13 @@ int ngpulm_state_of(const ngpulm_model* model, int32_t with_bos, const int32_t* 
  *                     is a state, R7)
  *   final_out[b]    = final weight of states[b], when non-NULL.
  * states: dev [B] int32. scores: dev [B,V] float32, next: dev [B,V] int32,
- * both row-major and caller-owned; final_out: dev [B] float32 or NULL. */
+ * both row-major and caller-owned; final_out: dev [B] float32 or NULL.
+ * The outputs must not overlap `states` (the kernel may read states[b] again
+ * after other rows' outputs are written). Rows are built from the state read
+ * before the kernel's programmatic-dependent-launch wait and re-checked after
+ * it, so a preceding kernel on the stream may still be writing
+ * `states` when this call starts: the result is always that of the final
+ * states. */
 int ngpulm_advance(const ngpulm_model* model, const int32_t* states, int32_t B, float* scores,
                    int32_t* next, float* final_out, ngpulm_stream stream);
 
