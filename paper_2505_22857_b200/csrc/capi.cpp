@@ -297,6 +297,15 @@ int ngpulm_advance(const ngpulm_model* m, const int32_t* states, int32_t B, floa
   if (int r = check_hot(m, B)) return r;
   if (B == 0) return NGPULM_OK;
   if (!states || !scores || !next) return err(NGPULM_EUSAGE, "NULL device buffer");
+  {  // the outputs must not overlap the states (rows re-read their state after others are written)
+    auto overlap = [](const void* a, size_t na, const void* b, size_t nb) {
+      const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+      return x < y + nb && y < x + na;
+    };
+    const size_t sb = (size_t)B * 4, ob = (size_t)B * m->h.V * 4;
+    if (overlap(states, sb, scores, ob) || overlap(states, sb, next, ob) || (final_out && overlap(states, sb, final_out, sb)))
+      return err(NGPULM_EUSAGE, "advance outputs overlap the states");
+  }
   int e = ngpulm::launch_advance(m->dm, states, B, scores, next, final_out, stream);
   if (e) return cuda_err((cudaError_t)e, "advance launch");
   return NGPULM_OK;

@@ -439,3 +439,12 @@ def test_speculative_build_states_written_by_previous_kernel(lm6, graph):
         rows = np.arange(k, B, 37)
         s32, _, n_o, _ = o.rows(snap_np[k, rows], want64=False)
         assert np.array_equal(nx_np[k, rows], n_o) and same_bits(sc_np[k, rows], s32), k
+
+
+def test_advance_rejects_outputs_overlapping_states(pairs):
+    m, o, _ = pairs["tri64"]
+    buf = torch.zeros(8 * m.V + 8, dtype=torch.int32, device=dev())
+    st = buf[:8]
+    sc = torch.empty((8, m.V), dtype=torch.float32, device=dev())
+    with pytest.raises(ng.NgpulmError):
+        m.advance(st, sc, buf[4:4 + 8 * m.V].view(8, m.V))
