@@ -8,8 +8,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libngpulm.so")
-SOURCES = ["kernels.cu", "capi.cpp", "build.cpp", "nglm.cpp"]
-HEADERS = ["ngpulm_internal.h", os.path.join("..", "..", "include", "ngpulm.h")]
+KERNELS = ["advance.cu", "fused.cu", "decode.cu"]
+SOURCES = KERNELS + ["capi.cpp", "build.cpp", "nglm.cpp"]
+HEADERS = ["kcommon.cuh", "ngpulm_internal.h", os.path.join("..", "..", "include", "ngpulm.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
@@ -34,9 +35,11 @@ def build_variant(name: str, defines: list[str]) -> str:
 
 
 def build_phase_timing() -> str:
-    """Debug variant with per-CTA phase stamps (tools/phase_timing.py); not the product."""
+    """Debug variant with per-CTA phase stamps (tools/phase_timing.py); not the product.
+    All kernels in one translation unit (unity_timing.cu): one phase-stamp buffer."""
     out = os.path.join(LIBDIR, "libngpulm_timing.so")
-    cmd = [NVCC, *ARCH, *FLAGS, "-DNGPULM_PHASE_TIMING", "-o", out, *[os.path.join(CSRC, s) for s in SOURCES]]
+    srcs = ["unity_timing.cu"] + [x for x in SOURCES if x not in KERNELS]
+    cmd = [NVCC, *ARCH, *FLAGS, "-DNGPULM_PHASE_TIMING", "-o", out, *[os.path.join(CSRC, s) for s in srcs]]
     subprocess.run(cmd, check=True)
     return out
 

@@ -89,7 +89,7 @@ struct DevModel {
   int32_t tiny_chain_bytes, tiny_arcq_bytes;
 };
 
-// Kernel launchers (kernels.cu). Return cudaError_t as int.
+// Kernel launchers (advance.cu, fused.cu, decode.cu). Return cudaError_t as int.
 int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* scores,
                    int32_t* next, float* final_out, void* stream);
 int launch_final(const DevModel& m, const int32_t* states, int32_t B, float* out, void* stream);
