@@ -5,35 +5,29 @@
 // NGPU-LM hot path for sm_100a: batched full-vocabulary query (Algorithm 1,
 // PAPER.md:54-89) and the fused greedy shallow-fusion step.
 //
-// Design: one CTA of 256 threads per batch row; the row
+// A row (the LM scores and next states of one state over the vocabulary)
 // lives in shared memory as (score, next state) per token, 8 KB at V = 1024,
-// so 8 CTAs fit per SM and B = 1024 rows run as one wave. Bulk data moves by
-// TMA (cp.async.bulk), so the SM's load/store queue only carries the
-// latency-critical gathers (state, chain record, arcs), which complete in
-// issue order behind whatever else that queue holds.
-//  0. prologue, independent of earlier kernels (model data is immutable): one
-//     thread bulk-copies the root level (an arc for every token,
-//     [0, V)) into the row: weights into the score slots, targets into the
-//     next-state slots. Then griddepcontrol.wait (programmatic dependent
-//     launch), so launch and prologue overlap the previous kernel.
-//  1. warp 0 reads the row's state and its back-off levels (Algorithm 1 lines
-//     72, 81-82) — from the load-time chain table (one 16-byte record slot per
-//     level and lane, acc_boff pre-accumulated left to right in float, R10)
-//     or, in walk mode, lane 0 walks boff_to_states level by level exactly as
-//     Algorithm 1 does. One barrier publishes them.
-//  2. every thread gathers up to 4 arcs of the row into registers, all loads
-//     in flight together (a level's arcs are contiguous: arcs are sorted by
-//     (from_state, token)), while the root slots get acc_root
-//     added (root score = acc_root + root weight).
-//  3. the gathered arcs are written into the row level by level from the
-//     lowest order up, one barrier per level, so a higher-order arc
+// and is built in four steps:
+//  0. prologue on immutable model data, before griddepcontrol.wait
+//     (programmatic dependent launch): the root level (an arc
+//     for every token) — targets by TMA bulk copy into the next-state slots,
+//     weights into registers;
+//  1. the row's back-off levels (Algorithm 1 lines 72, 81-82) from the
+//     load-time chain table (one 16-byte record slot per level and lane,
+//     acc_boff accumulated left to right in float, R10), or Algorithm 1's
+//     literal walk;
+//  2. the levels' arcs, cut into slots of 32 16-byte quads, gathered into
+//     registers a window of slots at a time, while the root scores
+//     acc_root + root weight are stored;
+//  3. slots written in level order, lowest order first, so a higher-order arc
 //     overwrites a lower-order one — Algorithm 1's "first level found wins"
 //     (lines 77-79) with plain shared-memory stores, no atomics.
-//  4. advance: the finished row leaves by two TMA bulk stores (scores, next);
-//     fused step: the columns' fused values feed a shuffle argmax, so the LM
-//     row never touches HBM.
-// Rows with more than 1024 non-root arcs repeat steps 2-3 per 1024-arc chunk.
-// No tensor cores: gather/scatter + store bandwidth only.
+// advance.cu stores the row by TMA bulk copies (one warp per row and per CTA,
+// steps 1-3 speculatively before the PDL wait); fused.cu and decode.cu feed
+// it to the fused argmax and it never touches HBM. The CTA-per-row kernels
+// (one 256-thread CTA per row or vocabulary tile) serve unaligned outputs and
+// rows beyond shared memory. No tensor cores: gathers, shared-memory scatter
+// and store bandwidth only (DESIGN.md §7 Roofline).
 #include <cuda_runtime.h>
 
 #include <climits>
