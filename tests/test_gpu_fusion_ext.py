@@ -106,3 +106,21 @@ def test_topk_invalid_state_and_bad_k(pairs):
         m.fused_topk(T(x), T(st), 0)
     with pytest.raises(ng.NgpulmError):
         m.fused_topk(T(x), T(st), ng.MAX_TOPK + 1)
+
+
+@pytest.mark.parametrize("B", [100, 592, 593, 1500])
+@pytest.mark.parametrize("mode", [CTC, RNNT, AED])
+def test_fused_step_kernel_paths_by_batch(pairs, mode, B):
+    """Both transducer paths (the warp pair up to 4 rows per SM, one warp per row
+    beyond) and the CTC/AED warp kernel across batch sizes, vs the oracle."""
+    m, o, _ = pairs["five48"]
+    x = synth.rnnt_logits(B, 1, o.V, seed=B)[0]
+    st = synth.uniform_states(o.num_states, B, seed=B + 1)
+    prev = np.random.default_rng(B).integers(-1, o.V, size=B).astype(np.int32) if mode == CTC else None
+    st_d, pv_d = T(st), (T(prev) if prev is not None else None)
+    tok = m.fused_greedy_step(mode, T(x), st_d, prev=pv_d, lam=0.8)
+    torch.cuda.synchronize()
+    to, so, po = o.fused_step(mode, x, st, prev=prev, lam=0.8)
+    assert np.array_equal(tok.cpu().numpy(), to) and np.array_equal(st_d.cpu().numpy(), so)
+    if mode == CTC:
+        assert np.array_equal(pv_d.cpu().numpy(), po)

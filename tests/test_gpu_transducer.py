@@ -111,3 +111,15 @@ def test_driver_config3_shape(lm6):
     for i in range(rows.size):
         assert np.array_equal(em[i, : el[i]], ref[0][i, : el[i]])
     assert el.sum() > 0
+
+
+def test_driver_large_batch_single_warp_path(pairs):
+    """B > 592 rows: the loop step runs one warp per row (not the pair kernel)."""
+    m, o, f = pairs["tri64"]
+    B = 700
+    lengths = np.random.default_rng(55).integers(0, 12, size=B).astype(np.int32)
+    seed, temp = 777, 2.0
+    res = transducer_greedy_decode(m, synth_joint(seed, temp, o.V), T(lengths), lam=0.7, max_symbols=3)
+    torch.cuda.synchronize()
+    check(res, o.transducer_decode(seed, lengths, np.zeros(B, np.int32), lam=0.7, max_symbols=3, temperature=temp,
+                                   max_len=res.emitted.shape[1], blank_bias=BIAS))
