@@ -120,6 +120,51 @@ __global__ void __launch_bounds__(256, 1)
     for (int j = 0; j < 8; ++j)
       if (lane + 32 * j < V / 4) rw[j] = __ldg(w4 + lane + 32 * j);
   }
+  // The LM row of state st into shared memory (no global writes); ph: the
+  // parity of this build's root-target copy.
+  auto build = [&](int32_t st, uint32_t ph) -> Row {
+    WLevel lv;
+    int32_t nslots;
+    const Row r = warp_row_src<kTable>(m, ValState{st}, s, lv, nslots);
+    if (r.bad) {
+      mbar_wait(s.bar, ph);  // the copy of this phase is over before any re-arm or exit
+      return r;
+    }
+    Window<kW, kPacked> a;
+    load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
+    {  // root scores: acc_root + root weight, while the gathers fly
+      float4* s4 = reinterpret_cast<float4*>(s.row_s);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (lane + 32 * j < V / 4) {
+          float4 y = rw[j];
+          y.x = __fadd_rn(r.acc_root, y.x);
+          y.y = __fadd_rn(r.acc_root, y.y);
+          y.z = __fadd_rn(r.acc_root, y.z);
+          y.w = __fadd_rn(r.acc_root, y.w);
+          s4[lane + 32 * j] = y;
+        }
+    }
+    mbar_wait(s.bar, ph);
+    __syncwarp();
+    for (int32_t k0 = 0; k0 < nslots;) {
+      write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
+      k0 += kW;
+      if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
+    }
+    return r;
+  };
+  auto load_state = [&]() {
+    int32_t v = 0;
+    if (lane == 0) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(states + row) : "memory");
+    return __shfl_sync(kFull, v, 0);
+  };
+  // Speculative build (as advance_warp_kernel): the LM row from the state read
+  // before griddepcontrol.wait, re-checked after it. Inputs (logits, prev,
+  // active, ILM rows) are read after the wait only.
+  int32_t st = NGPULM_FUSED_SPECULATE ? load_state() : 0;
+  Row r;
+  if (NGPULM_FUSED_SPECULATE) r = build(st, 0);
   pdl_wait();
   STAMP(2);
   const float* lrow = logits + (size_t)row * row_stride;
@@ -136,56 +181,36 @@ __global__ void __launch_bounds__(256, 1)
   // used only after the state and record loads are issued
   const bool on = kMode == kLoop ? __ldg(&lp.frame[row]) < __ldg(&lp.len[row]) : (!active || __ldg(&active[row]));
   const int32_t pc = (kMode == NGPULM_CTC) ? __ldg(&prev[row]) : -2;
-  WLevel lv;
-  int32_t nslots;
-  bool started = false;
-  auto begin_logits = [&]() {  // the logits' copy, issued once the chain record is in flight
+  if (on) {  // the logits (an input: after the wait), copied while the state is checked
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));  // read once
     issue_frame(lrow, ncols, lbuf, lbar, pol);
-    started = true;
-  };
-  const Row r = warp_row<kTable>(m, states + row, s, lv, nslots, begin_logits);
+  }
   const float* lb = lbuf + (reinterpret_cast<uintptr_t>(lrow) & 15) / 4;  // column c at lb[c]
+  {
+    const int32_t st1 = load_state();
+    if (!NGPULM_FUSED_SPECULATE || st1 != st) {
+      if (NGPULM_FUSED_SPECULATE && lane == 0) {  // the root targets again (the first build overwrote them)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)),
+                     "r"((uint32_t)V * 4u)
+                     : "memory");
+        bulk_g2s(s.row_n, m.arc_to, (uint32_t)V * 4u, s.bar);
+      }
+      __syncwarp();
+      st = st1;
+      r = build(st, NGPULM_FUSED_SPECULATE ? 1u : 0u);
+    }
+  }
   STAMP(11);
-  if (!on || r.bad) {  // inactive rows are untouched (their state is not even checked)
+  if (!on || r.bad) {  // inactive rows are untouched
     if (lane == 0) {
       tokens_out[row] = -1;
       if (on) atomicMin(m.bad_row, (unsigned long long)row);
       if (kMode == kLoop && on) lp.frame[row] = lp.len[row];  // an invalid state ends the row's loop
     }
-    mbar_wait(s.bar, 0);  // no exit with a bulk copy in flight
-    if (started) mbar_wait(lbar, 0);
+    if (on) mbar_wait(lbar, 0);  // no exit with a bulk copy in flight
     return;
   }
-  // (RNN-T: the LM row is built before stage 1 is known — it waits for the
-  // logits — and is simply not used when blank wins)
-  Window<kW, kPacked> a;
-  load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
-  STAMP(3);
-  {  // root scores: acc_root + root weight, while the gathers fly
-    float4* s4 = reinterpret_cast<float4*>(s.row_s);
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (lane + 32 * j < V / 4) {
-        float4 y = rw[j];
-        y.x = __fadd_rn(r.acc_root, y.x);
-        y.y = __fadd_rn(r.acc_root, y.y);
-        y.z = __fadd_rn(r.acc_root, y.z);
-        y.w = __fadd_rn(r.acc_root, y.w);
-        s4[lane + 32 * j] = y;
-      }
-  }
-  STAMP(4);
-  mbar_wait(s.bar, 0);
-  __syncwarp();
-  STAMP(5);
-  for (int32_t k0 = 0; k0 < nslots;) {
-    write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
-    k0 += kW;
-    if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
-  }
-  STAMP(6);
   mbar_wait(lbar, 0);
   __syncwarp();
   STAMP(12);

@@ -374,6 +374,9 @@ __device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, con
 // lanes store into a trash word behind the row, so the write loop has no
 // branches. No CTA-wide barrier after the prologue: rows never wait for each
 // other.
+#ifndef NGPULM_FUSED_SPECULATE
+#define NGPULM_FUSED_SPECULATE 1
+#endif
 #ifndef NGPULM_STORE_HINT
 #define NGPULM_STORE_HINT 1
 #endif
