@@ -448,3 +448,31 @@ def test_advance_rejects_outputs_overlapping_states(pairs):
     sc = torch.empty((8, m.V), dtype=torch.float32, device=dev())
     with pytest.raises(ng.NgpulmError):
         m.advance(st, sc, buf[4:4 + 8 * m.V].view(8, m.V))
+
+
+from hypothesis import HealthCheck, given, settings  # noqa: E402
+from hypothesis import strategies as hst  # noqa: E402
+
+
+@settings(max_examples=10, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+@given(V=hst.sampled_from([8, 20, 32, 64]), order=hst.integers(1, 6), tokens=hst.integers(60, 2000),
+       seed=hst.integers(1, 10_000), prune=hst.lists(hst.integers(0, 3), min_size=6, max_size=6),
+       lam=hst.sampled_from([0.0, 0.4, 2.5]))
+def test_random_lms_exhaustive(tmp_path_factory, V, order, tokens, seed, prune, lam):
+    """Random small LMs (order, vocabulary, corpus, count pruning): every state x
+    token of advance, and the three fused steps, bit-exact vs the oracle."""
+    d = str(tmp_path_factory.mktemp("rndg"))
+    pr = ",".join(["0"] + [str(x) for x in prune[: order - 1]]) if order >= 2 else None
+    f = synth.make_lm(d, V, order, tokens=tokens, seed=seed, lexicon=max(20, V * 3), heldout=5, tag="r", prune=pr)
+    m, o = ng.load_arpa(f.arpa, vocab_size=V, device=0), Oracle(f.arpa, vocab_size=V)
+    states = np.arange(o.num_states, dtype=np.int32)
+    s, n, fin = gpu_advance(m, states)
+    s32, _, n_o, _ = o.rows(states, want64=False)
+    f32, _ = o.finals(states)
+    assert np.array_equal(n, n_o) and same_bits(s, s32) and same_bits(fin, f32)
+    x = synth.rnnt_logits(o.num_states, 1, V, seed=seed)[0]
+    for mode in (CTC, RNNT, AED):
+        pv = np.full(o.num_states, -1, np.int32) if mode == CTC else None
+        tg, sg, _ = gpu_step(m, mode, x, states, pv, None, lam)
+        to, so, _ = o.fused_step(mode, x, states, prev=pv, lam=lam)
+        assert np.array_equal(tg, to) and np.array_equal(sg, so), mode
