@@ -124,3 +124,68 @@ def test_fused_step_kernel_paths_by_batch(pairs, mode, B):
     assert np.array_equal(tok.cpu().numpy(), to) and np.array_equal(st_d.cpu().numpy(), so)
     if mode == CTC:
         assert np.array_equal(pv_d.cpu().numpy(), po)
+
+
+def test_every_hot_call_is_graph_capturable(pairs):
+    """advance, final, fused step (3 modes), ILM step, top-k, CTC decode and the
+    loop step captured in one CUDA graph: replaying it gives the eager results."""
+    m, o, f = pairs["five48"]
+    B, V = 64, o.V
+    rng = np.random.default_rng(5)
+    st0 = synth.uniform_states(o.num_states, B, seed=6)
+    x = T(synth.rnnt_logits(B, 1, V, seed=7)[0])
+    xc = T(synth.ctc_logits(synth.read_sentences(f.heldout), B, 9, V, seed=8))
+    ilm = T(rng.normal(-4, 2, size=(B, V)).astype(np.float32))
+    lengths = T(rng.integers(0, 6, size=B).astype(np.int32))
+    s = torch.cuda.Stream()
+
+    def run(bufs):
+        st, sc, nx, fi, fo, toks, tk, dec, loop = bufs
+        m.advance(st[0], sc, nx, fi, stream=s)
+        m.final(st[0], fo, stream=s)
+        for i, mode in enumerate((CTC, RNNT, AED)):
+            m.fused_greedy_step(mode, x, st[1 + i], prev=st[4], lam=0.7, tokens_out=toks[i], stream=s)
+        m.fused_greedy_step_ilm(RNNT, x, st[5], ilm, 0.3, lam=0.7, tokens_out=toks[3], stream=s)
+        r = m.fused_topk(x, st[0], 3, lam=0.7, stream=s)
+        tk[0].copy_(r[1])
+        m.ctc_greedy_decode(xc, st[6], st[7], lam=0.7, frames_out=dec[0], emit_out=dec[1], emit_len=dec[2][0],
+                            stream=s)
+        m.transducer_loop_step(x, st[8], loop[0], loop[1], lengths, loop[2], loop[3], lam=0.7, max_symbols=2,
+                               tokens_out=toks[4], stream=s)
+
+    def fresh():
+        st = torch.from_numpy(np.stack([st0] * 9)).to(dev())
+        st[4].fill_(-1)
+        st[7].fill_(-1)
+        return (st, torch.empty((B, V), device=dev()), torch.empty((B, V), dtype=torch.int32, device=dev()),
+                torch.empty(B, device=dev()), torch.empty(B, device=dev()),
+                torch.empty((5, B), dtype=torch.int32, device=dev()), torch.empty((1, B, 3), dtype=torch.int32,
+                                                                                  device=dev()),
+                (torch.empty((B, 9), dtype=torch.int32, device=dev()), torch.empty((B, 9), dtype=torch.int32,
+                                                                                   device=dev()),
+                 torch.empty((1, B), dtype=torch.int32, device=dev())),
+                (torch.zeros(B, dtype=torch.int32, device=dev()), torch.zeros(B, dtype=torch.int32, device=dev()),
+                 torch.empty((B, 4), dtype=torch.int32, device=dev()), torch.zeros(B, dtype=torch.int32,
+                                                                                    device=dev())))
+    eager = fresh()
+    with torch.cuda.stream(s):
+        run(eager)
+    s.synchronize()
+    graphed = fresh()
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            run(graphed)
+        g.replay()
+    s.synchronize()
+
+    def flat(b):
+        out = []
+        for t in b:
+            out.extend(flat(t) if isinstance(t, tuple) else [t])
+        return out
+    for a, b in zip(flat(eager), flat(graphed)):
+        if a.dtype == torch.float32:
+            assert same_bits(a.cpu().numpy(), b.cpu().numpy())
+        else:
+            assert torch.equal(a.cpu(), b.cpu())
