@@ -128,7 +128,8 @@ def test_fused_step_kernel_paths_by_batch(pairs, mode, B):
 
 def test_every_hot_call_is_graph_capturable(pairs):
     """advance, final, fused step (3 modes), ILM step, top-k, CTC decode and the
-    loop step captured in one CUDA graph: replaying it gives the eager results."""
+    loop step captured in one CUDA graph: replaying it gives the eager results
+    (emission buffers start at -1: entries past the emission counts are not written)."""
     m, o, f = pairs["five48"]
     B, V = 64, o.V
     rng = np.random.default_rng(5)
@@ -161,11 +162,11 @@ def test_every_hot_call_is_graph_capturable(pairs):
                 torch.empty(B, device=dev()), torch.empty(B, device=dev()),
                 torch.empty((5, B), dtype=torch.int32, device=dev()), torch.empty((1, B, 3), dtype=torch.int32,
                                                                                   device=dev()),
-                (torch.empty((B, 9), dtype=torch.int32, device=dev()), torch.empty((B, 9), dtype=torch.int32,
-                                                                                   device=dev()),
+                (torch.empty((B, 9), dtype=torch.int32, device=dev()), torch.full((B, 9), -1, dtype=torch.int32,
+                                                                                  device=dev()),
                  torch.empty((1, B), dtype=torch.int32, device=dev())),
                 (torch.zeros(B, dtype=torch.int32, device=dev()), torch.zeros(B, dtype=torch.int32, device=dev()),
-                 torch.empty((B, 4), dtype=torch.int32, device=dev()), torch.zeros(B, dtype=torch.int32,
+                 torch.full((B, 4), -1, dtype=torch.int32, device=dev()), torch.zeros(B, dtype=torch.int32,
                                                                                     device=dev())))
     eager = fresh()
     with torch.cuda.stream(s):
