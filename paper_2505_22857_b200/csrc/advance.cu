@@ -514,7 +514,7 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
     // packed arcs bulk-copied into a staging area; more rows per SM: 8-slot
     // windows of direct gathers (registers and shared memory for occupancy)
     const bool wide = B <= NGPULM_WIDE_MAX_B, pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO;
-    const bool small_v = m.V <= 1024, stage = B >= 2 && B <= NGPULM_STAGE_MAX_B && pk && small_v && table;
+    const bool small_v = m.V <= 1024, stage = B >= NGPULM_STAGE_MIN_B && B <= NGPULM_STAGE_MAX_B && pk && small_v && table;
     const int sq = stage ? kStageQuads : 0;
     // one row (warp) per CTA: a CTA leaves as soon as its row is stored and the
     // next call's CTA starts its speculative build in its place (B=1024: 7 rows
@@ -522,7 +522,10 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
     const int R = 1;
     if (wcta_smem(m.V, m.order, R, sq) <= 227 * 1024) {
       const size_t wsm = wcta_smem(m.V, m.order, R, sq);
-      const dim3 wg((B + R - 1) / R), wb(32 * R);
+      // one CTA per SM for every batch between NGPULM_PAD_MIN_B and 148 rows (the
+      // extra CTAs exit at once): measured B=128 1.92 -> 1.69 us, B=147 1.93 -> 1.34
+      const int32_t nrows = (B >= NGPULM_PAD_MIN_B && B < NGPULM_PAD_GRID) ? NGPULM_PAD_GRID : B;
+      const dim3 wg((nrows + R - 1) / R), wb(32 * R);
       if (stage)
         return launch(advance_warp_kernel<true, 16, true, true, true>, wg, wb, wsm, st, m, states, B, scores, next,
                       final_out);

@@ -412,9 +412,18 @@ __device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, con
 __host__ __device__ constexpr size_t wrow_bytes(int32_t V) { return align16((size_t)V * 4 + 4); }  // + trash word
 // staged arcs: kStageQuads packed arc quads (32 bytes each)
 constexpr int kStageQuads = 512;
-#ifndef NGPULM_STAGE_MAX_B
-#define NGPULM_STAGE_MAX_B 148  // batches of 2 .. one row per SM stage their arcs by bulk copy (measured)
+#ifndef NGPULM_PAD_GRID
+#define NGPULM_PAD_GRID 148
 #endif
+#ifndef NGPULM_PAD_MIN_B
+#define NGPULM_PAD_MIN_B 65
+#endif
+#ifndef NGPULM_STAGE_MIN_B
+#define NGPULM_STAGE_MIN_B 2
+#endif
+#ifndef NGPULM_STAGE_MAX_B
+#define NGPULM_STAGE_MAX_B 0  // arcs staged by bulk copy: off since the speculative one-warp CTAs (with it:
+#endif                        // B=16 1.43 vs 1.21 us, B=148 1.42 vs 1.19; B=128 1.63 vs 1.69 padded)
 __host__ __device__ constexpr size_t wslice_bytes(int32_t V, int32_t order, int stage_q) {
   return 2 * wrow_bytes(V) + levels_bytes(order) + 16 + (size_t)stage_q * 32;
 }

@@ -55,9 +55,11 @@ def run(B, mode, n=400):
 
 
 MODES = ((ng.CHAIN_TABLE, "table"), (ng.CHAIN_WALK, "walk"))
-BS = (1, 16, 128, 512, 1024, 2048, 4096)
+BS = tuple(int(x) for x in os.environ.get("SWEEP_BS", "1,16,128,512,1024,2048,4096").split(","))
 if os.environ.get("SWEEP_QUICK"):
-    MODES, BS = MODES[:1], (1, 128, 1024, 4096)
+    MODES = MODES[:1]
+    if not os.environ.get("SWEEP_BS"):
+        BS = (1, 128, 1024, 4096)
 print("lib", os.path.basename(ng.LIB_PATH))
 print("B, kernel, mode, graph_us_per_call, single_launch_us, GB/s(graph)")
 KINDS = [int(x) for x in os.environ.get("SWEEP_KERNELS", "0,1,2").split(",")]
