@@ -650,7 +650,7 @@ int launch_fused_mode(const DevModel& m, const float* logits, int64_t row_stride
                       int32_t* tokens_out, cudaStream_t st) {
   if (m.V % 4 == 0 && m.V <= 1024 && m.adv_kind != NGPULM_ADVANCE_CTA) {
     const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
-    if (kMode == NGPULM_RNNT && B <= NGPULM_PAIR_MAX_B) {  // two warps per row (stage 1 beside the row build)
+    if constexpr (kMode == NGPULM_RNNT) if (B <= NGPULM_PAIR_MAX_B) {  // two warps per row (stage 1 beside the row build)
       int R = (B + 147) / 148;
       R = R < 1 ? 1 : (R > 4 ? 4 : R);
       const size_t psm = (size_t)R * (fslice_bytes(m.V, m.order) + 64);
