@@ -123,6 +123,30 @@ def _dev_ptr(t, dtype, name, numel=None):
     return t.data_ptr()
 
 
+def _rows_ptr(t, B, ncols, name, row_stride=None):
+    """Pointer to B rows of `ncols` contiguous float32 columns, row b at b*row_stride
+    elements (default: the tensor's leading stride). Checks the column count and that
+    every row the kernels read lies inside the tensor's storage."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
+        raise TypeError(f"{name}: expected a CUDA float32 tensor")
+    if t.dim() == 0 or t.shape[-1] != ncols or (t.dim() >= 2 and t.stride(-1) != 1):
+        raise ValueError(f"{name}: needs {ncols} contiguous columns, got shape {tuple(t.shape)}")
+    if t.dim() == 1 and B > 1:
+        raise ValueError(f"{name}: a 1-D tensor holds one row, B = {B}")
+    if t.dim() >= 2 and t.shape[0] < B:
+        raise ValueError(f"{name}: needs {B} rows, has {t.shape[0]}")
+    if row_stride is None:
+        row_stride = t.stride(0) if t.dim() >= 2 else ncols
+    if B > 1 and row_stride < ncols:
+        raise ValueError(f"{name}: row stride {row_stride} < {ncols} columns")
+    if B > 0:
+        last = t.storage_offset() + (B - 1) * row_stride + ncols
+        if last * 4 > t.untyped_storage().nbytes():
+            raise ValueError(f"{name}: rows reach past the tensor's storage")
+    return t.data_ptr(), row_stride
+
+
 class NgpuLM:
     """A resident NGPU-LM model (one replica per device)."""
 
@@ -232,17 +256,12 @@ class NgpuLM:
         import torch
         if B is None:
             B = states.numel()
-        if logits.dtype != torch.float32 or not logits.is_cuda:
-            raise TypeError("logits: expected a CUDA float32 tensor")
-        if row_stride is None:
-            row_stride = logits.stride(0) if logits.dim() >= 2 else self.V + 1
-            if logits.dim() == 2 and logits.stride(1) != 1:
-                raise ValueError("logits rows must be contiguous")
+        lp, row_stride = _rows_ptr(logits, B, self.V + 1, "logits", row_stride)
         if tokens_out is None:
             tokens_out = torch.empty(B, dtype=torch.int32, device=states.device)
         blank = self.V if blank_id is None else blank_id
         _check(lib().ngpulm_fused_greedy_step(
-            self._h, mode, logits.data_ptr(), row_stride, B,
+            self._h, mode, lp, row_stride, B,
             _dev_ptr(states, torch.int32, "states", B),
             _dev_ptr(prev, torch.int32, "prev", B) if prev is not None else None,
             _dev_ptr(active, torch.uint8, "active", B) if active is not None else None,
@@ -255,19 +274,17 @@ class NgpuLM:
         LM-rescored columns. ilm: [B, V] CUDA f32 (rows contiguous)."""
         import torch
         B = states.numel()
-        if logits.dtype != torch.float32 or not logits.is_cuda or logits.dim() != 2 or logits.stride(1) != 1:
-            raise TypeError("logits: expected a [B, V+1] CUDA float32 tensor with contiguous rows")
-        if ilm.dtype != torch.float32 or not ilm.is_cuda or ilm.dim() != 2 or ilm.stride(1) != 1:
-            raise TypeError("ilm: expected a [B, V] CUDA float32 tensor with contiguous rows")
+        lp, ls = _rows_ptr(logits, B, self.V + 1, "logits")
+        ip, istr = _rows_ptr(ilm, B, self.V, "ilm")
         if tokens_out is None:
             tokens_out = torch.empty(B, dtype=torch.int32, device=states.device)
         blank = self.V if blank_id is None else blank_id
         _check(lib().ngpulm_fused_greedy_step_ilm(
-            self._h, mode, logits.data_ptr(), logits.stride(0), B,
+            self._h, mode, lp, ls, B,
             _dev_ptr(states, torch.int32, "states", B),
             _dev_ptr(prev, torch.int32, "prev", B) if prev is not None else None,
             _dev_ptr(active, torch.uint8, "active", B) if active is not None else None,
-            float(lam), blank, ilm.data_ptr(), ilm.stride(0), float(lam_ilm),
+            float(lam), blank, ip, istr, float(lam_ilm),
             _dev_ptr(tokens_out, torch.int32, "tokens_out", B), _stream(stream)))
         return tokens_out
 
@@ -279,18 +296,17 @@ class NgpuLM:
         CUDA tensors updated in place; emit_out [B, max_len])."""
         import torch
         B = states.numel()
-        if logits.dtype != torch.float32 or not logits.is_cuda or logits.dim() != 2 or logits.stride(1) != 1:
-            raise TypeError("logits: expected a [B, V+1] CUDA float32 tensor with contiguous rows")
+        lp, ls = _rows_ptr(logits, B, self.V + 1, "logits")
+        ip, istr = _rows_ptr(ilm, B, self.V, "ilm") if ilm is not None else (None, 0)
         if tokens_out is None:
             tokens_out = torch.empty(B, dtype=torch.int32, device=states.device)
         max_len = emit_out.shape[1] if emit_out.dim() == 2 else 0
         blank = self.V if blank_id is None else blank_id
         _check(lib().ngpulm_transducer_loop_step(
-            self._h, logits.data_ptr(), logits.stride(0), B, _dev_ptr(states, torch.int32, "states", B),
+            self._h, lp, ls, B, _dev_ptr(states, torch.int32, "states", B),
             _dev_ptr(frame_idx, torch.int32, "frame_idx", B), _dev_ptr(sym_count, torch.int32, "sym_count", B),
             _dev_ptr(lengths, torch.int32, "lengths", B), int(max_symbols), float(lam), blank,
-            ilm.data_ptr() if ilm is not None else None, ilm.stride(0) if ilm is not None else 0,
-            float(lam_ilm), _dev_ptr(tokens_out, torch.int32, "tokens_out", B),
+            ip, istr, float(lam_ilm), _dev_ptr(tokens_out, torch.int32, "tokens_out", B),
             _dev_ptr(emit_out, torch.int32, "emit_out", B * max_len) if max_len else None,
             _dev_ptr(emit_len, torch.int32, "emit_len", B),
             _dev_ptr(last_token, torch.int32, "last_token", B) if last_token is not None else None,
@@ -302,18 +318,15 @@ class NgpuLM:
         """ngpulm_fused_topk -> (scores [B,k] f32, cols [B,k] i32, next [B,k] i32 or None)."""
         import torch
         B = states.numel()
-        if logits.dtype != torch.float32 or not logits.is_cuda or logits.dim() != 2 or logits.stride(1) != 1:
-            raise TypeError("logits: expected a [B, V+1] CUDA float32 tensor with contiguous rows")
+        lp, ls = _rows_ptr(logits, B, self.V + 1, "logits")
+        ip, istr = _rows_ptr(ilm, B, self.V, "ilm") if ilm is not None else (None, 0)
         dev = logits.device
         sc = torch.empty((B, k), dtype=torch.float32, device=dev)
         cols = torch.empty((B, k), dtype=torch.int32, device=dev)
         nx = torch.empty((B, k), dtype=torch.int32, device=dev) if want_next else None
         eos = self.V if eos_id is None else eos_id
-        if ilm is not None and (ilm.dtype != torch.float32 or not ilm.is_cuda or ilm.stride(-1) != 1):
-            raise TypeError("ilm: expected a [B, V] CUDA float32 tensor with contiguous rows")
         _check(lib().ngpulm_fused_topk(
-            self._h, logits.data_ptr(), logits.stride(0), B, _dev_ptr(states, torch.int32, "states", B),
-            ilm.data_ptr() if ilm is not None else None, ilm.stride(0) if ilm is not None else 0,
+            self._h, lp, ls, B, _dev_ptr(states, torch.int32, "states", B), ip, istr,
             float(lam), float(lam_ilm), eos, k, sc.data_ptr(), cols.data_ptr(),
             nx.data_ptr() if nx is not None else None, _stream(stream)))
         return sc, cols, nx

@@ -228,6 +228,10 @@ int build_from_arpa(const char* arpa_path, const char* vocab_path, int32_t V, Ho
       continue;
     }
     const int k = section;
+    // a section above the order N is declared empty (N = highest non-empty order,
+    // <= NGPULM_MAX_ORDER): any line in it is a count mismatch, rejected before
+    // its tokens are read into toks[NGPULM_MAX_ORDER]
+    if (k > N) return fail(NGPULM_EDOMAIN, "n-gram in a section declared empty in \\data\\" + where);
     // ---- one n-gram line: log10p tokens... [log10bo]
     char* q = nullptr;
     double lp = std::strtod(s, &q);

@@ -98,7 +98,16 @@ def test_bad_arpa_rejected(tmp_path, fig1_paths):
         "prefix": txt.replace("\\3-grams:\n", "\\3-grams:\n-0.1\tmat the cat\n").replace("ngram 3=6", "ngram 3=7"),
         "predict_bos": txt.replace("\\2-grams:\n", "\\2-grams:\n-0.1\tthe <s>\n").replace("ngram 2=7", "ngram 2=8"),
         "nounk": txt.replace("-0.90308998699194354\t<unk>\n", "").replace("ngram 1=8", "ngram 1=7"),
+        # a line in a section declared empty (order above N)
+        "empty4": txt.replace("ngram 3=6\n", "ngram 3=6\nngram 4=0\n")
+                     .replace("\\end\\", "\\4-grams:\n-0.1\tthe cat sat on\n\n\\end\\"),
     }
+    # sections up to 200 declared empty, then a 200-token line —
+    # more tokens than NGPULM_MAX_ORDER; must be EDOMAIN, never a buffer overrun
+    decl = "".join(f"ngram {k}=0\n" for k in range(4, 201))
+    hdrs = "".join(f"\\{k}-grams:\n" for k in range(4, 200))
+    cases["order200"] = (txt.replace("ngram 3=6\n", "ngram 3=6\n" + decl)
+                         .replace("\\end\\", hdrs + "\\200-grams:\n-0.1\t" + " ".join(["the"] * 200) + "\n\n\\end\\"))
     for name, t in cases.items():
         p = tmp_path / f"{name}.arpa"
         p.write_text(t)
