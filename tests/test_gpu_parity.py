@@ -138,17 +138,18 @@ def test_config1_b128_full_rows(lm6, chain, kernel):
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-def test_headline_b1024_sampled_rows(lm6, kernel):
-    """The bench launch (B=1024 trajectory rows) checked on sampled rows."""
+def test_headline_b1024_every_row(lm6, kernel):
+    """The bench launch (B=1024 trajectory rows, the same states bench.py times):
+    EVERY row against the oracle (score32 bit-exact, next ids, finals), plus
+    the f64 definition within 1e-5 and normalization of every row."""
     m, o, f = lm6
     states, _ = trajectory_states(m, f, 1024, seed=2)
     with using(m, kernel=kernel):
         s, n, fin = gpu_advance(m, states)
-    rows = np.random.default_rng(5).choice(1024, 48, replace=False)
-    s32, s64, n_o, _ = o.rows(states[rows])
-    assert np.array_equal(n[rows], n_o) and same_bits(s[rows], s32)
-    assert np.max(np.abs(s[rows] - s64)) < 1e-5
-    # properties that hold for every row: normalization against the final weight
+    s32, s64, n_o, _ = o.rows(states)
+    f32, _ = o.finals(states)
+    assert np.array_equal(n, n_o) and same_bits(s, s32) and same_bits(fin, f32)
+    assert np.max(np.abs(s - s64)) < 1e-5
     tot = np.exp(s.astype(np.float64)).sum(1) + np.exp(fin.astype(np.float64))
     assert np.max(np.abs(tot - 1)) < 1e-4
     # sharded == unsharded, bit for bit (rows are independent, SPEC.md:197)
@@ -159,25 +160,42 @@ def test_headline_b1024_sampled_rows(lm6, kernel):
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-def test_large_batch_b4096_sampled_rows(lm6, kernel):
-    """More rows than 8 per SM (the warp kernel's 8-slot windows) and the heaviest rows."""
+def test_large_batch_b4096_every_row(lm6, kernel):
+    """More rows than 8 per SM (the warp kernel's 8-slot windows), every row vs the oracle."""
     m, o, f = lm6
     states, _ = trajectory_states(m, f, 4096, seed=4)
     with using(m, kernel=kernel):
-        s, n, _ = gpu_advance(m, states)
-    h = m.host_arrays()
-    off, bt = h["arc_offsets"], h["boff_to_states"]
+        s, n, fin = gpu_advance(m, states)
+    s32, _, n_o, _ = o.rows(states, want64=False)
+    f32, _ = o.finals(states)
+    assert np.array_equal(n, n_o) and same_bits(s, s32) and same_bits(fin, f32)
 
-    def total(x):
-        t = 0
-        while x != 0:
-            t += int(off[x + 1] - off[x])
-            x = int(bt[x])
-        return t
-    T = np.array([total(int(x)) for x in states])
-    rows = np.unique(np.concatenate([np.argsort(-T)[:24], np.random.default_rng(8).choice(4096, 24, replace=False)]))
-    s32, _, n_o, _ = o.rows(states[rows], want64=False)
-    assert np.array_equal(n[rows], n_o) and same_bits(s[rows], s32)
+
+@pytest.mark.parametrize("name", SMALL + ["fig1"])
+def test_final_every_state(pairs, name):
+    """ngpulm_final on its own: every state of each small LM,
+    bit-exact vs the oracle's final32 (R9), B in one launch and in a ragged tail."""
+    m, o, _ = pairs[name]
+    states = np.arange(o.num_states, dtype=np.int32)
+    f32, f64 = o.finals(states)
+    got = m.final(torch.from_numpy(states).to(dev())).cpu().numpy()
+    assert same_bits(got, f32)
+    assert np.max(np.abs(got - f64)) < 1e-5
+    perm = np.random.default_rng(1).permutation(states)[: max(1, o.num_states - 3)]
+    got2 = m.final(torch.from_numpy(perm).to(dev())).cpu().numpy()
+    assert same_bits(got2, f32[perm])
+    assert m.check() == -1
+
+
+def test_final_b1024_trajectory(lm6):
+    """ngpulm_final at the bench batch (1024 trajectory states of the 6-gram) and
+    across more than one 256-thread block, bit-exact vs the oracle."""
+    m, o, f = lm6
+    states, _ = trajectory_states(m, f, 1024, seed=2)
+    states = np.concatenate([states, synth.uniform_states(m.num_states, 301, seed=9)])
+    f32, _ = o.finals(states)
+    got = m.final(torch.from_numpy(states).to(dev())).cpu().numpy()
+    assert same_bits(got, f32)
 
 
 def test_advance_host_and_replica_and_streams(lm6):
