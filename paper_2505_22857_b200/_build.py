@@ -28,9 +28,7 @@ def _stale() -> bool:
 def build_variant(name: str, defines: list[str]) -> str:
     """Tuning variants (tools/): same sources, other compile-time constants."""
     out = os.path.join(LIBDIR, f"libngpulm_{name}.so")
-    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-o", out,
-           *[os.path.join(CSRC, s) for s in SOURCES]]
-    subprocess.run(cmd, check=True)
+    _compile_link(out, [f"-D{d}" for d in defines], os.path.join(HERE, "build", name))
     return out
 
 
@@ -44,15 +42,31 @@ def build_phase_timing() -> str:
     return out
 
 
+def _compile_link(out: str, extra: list[str], objdir: str, verbose: bool = False) -> None:
+    """Each source compiles to an object in parallel, then one nvcc link."""
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"] + extra
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        cmd = [NVCC, *ARCH, *cflags, "-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose and src.endswith(".cu"):
+            cmd.insert(1, "-Xptxas=-v")
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", out + ".tmp", *objs], check=True)
+    os.replace(out + ".tmp", out)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
+    _compile_link(LIB, [], os.path.join(HERE, "build", "main"), verbose)
     return LIB
 
 

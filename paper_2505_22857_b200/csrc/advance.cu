@@ -74,8 +74,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   STAMPS_OUT(b);
 }
 
-template <bool kTable, int kW, bool kPacked, bool kRegRoot, bool kStage>
-__global__ void __launch_bounds__(32, NGPULM_ADV_MINB(kW, kPacked, kStage))
+// kRegRoot (V <= 1024): every lane keeps its 32 root weights in registers,
+// loaded before the wait, so the root fill is register -> shared stores that
+// overlap the arc gathers (shared-memory loads issued after the gathers would
+// return behind them); otherwise the CTA bulk-copies the root weights once.
+template <bool kTable, int kW, bool kPacked, bool kRegRoot>
+__global__ void __launch_bounds__(32, NGPULM_ADV_MINB(kW, kPacked))
     advance_warp_kernel(DevModel m, const int32_t* __restrict__ states, int32_t B, float* __restrict__ scores,
                         int32_t* __restrict__ next, float* __restrict__ final_out) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -84,40 +88,26 @@ __global__ void __launch_bounds__(32, NGPULM_ADV_MINB(kW, kPacked, kStage))
   const size_t rb = align16((size_t)V * 4);
   const float* root_w = reinterpret_cast<const float*>(smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + rb);
-  constexpr int kSQ = kStage ? kStageQuads : 0;
-  static_assert(!kStage || (kPacked && kRegRoot), "staging holds packed arcs");
-  const WSlice s = wcarve(smem + rb + 16 + (size_t)w * wslice_bytes(V, m.order, kSQ), V, m.order, kSQ);
+  const WSlice s = wcarve(smem + rb + 16 + (size_t)w * wslice_bytes(V, m.order, 0), V, m.order, 0);
   const int32_t row = (int32_t)blockIdx.x * R + w;
   const uint32_t bytes = (uint32_t)V * 4u;
   STAMP(0);
-  STAMP(1);
   STAMP(9);
   pdl_trigger();
-  // step 0, on immutable model data, so before the wait: the root weights
-  // once per CTA, and the root targets straight into every row's next-state
-  // slots (the root has an arc for every token, [0, V)).
-  // kCtaRoot (register root): the root targets reach the CTA once (one bulk
-  // copy into the otherwise unused root-weight buffer) and every row copies
-  // them shared -> shared, so the 4 KB root level is read from L2 once per CTA
-  // instead of once per row (1024 rows reading the same 32 lines at once
-  // queue on their L2 slices).
-  constexpr bool kCtaRoot = kRegRoot && kW == 16 && !kStage && NGPULM_CTA_ROOT;
+  // step 0, on immutable model data, so before the wait: the root targets
+  // straight into the row's next-state slots (the root has an
+  // arc for every token, [0, V)), the root weights into registers (or once
+  // per CTA into shared memory).
   if (lane == 0 && row < B) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(s.bar)) : "memory");
-    if (kStage) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(s.abar)) : "memory");
-    if (w == 0 && (!kRegRoot || kCtaRoot))
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    if (w == 0 && !kRegRoot) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (!kCtaRoot) {
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)), "r"(bytes)
-                   : "memory");
-      bulk_g2s(s.row_n, m.arc_to, bytes, s.bar);
-    } else {
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(s.bar)) : "memory");  // unused phase
-    }
-    if (w == 0 && (!kRegRoot || kCtaRoot)) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)), "r"(bytes)
+                 : "memory");
+    bulk_g2s(s.row_n, m.arc_to, bytes, s.bar);
+    if (w == 0 && !kRegRoot) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-      bulk_g2s(const_cast<float*>(root_w), kCtaRoot ? static_cast<const void*>(m.arc_to) : m.arc_w, bytes, bar);
+      bulk_g2s(const_cast<float*>(root_w), m.arc_w, bytes, bar);
     }
   }
   float4 rw[kRegRoot ? 8 : 1];
@@ -127,143 +117,95 @@ __global__ void __launch_bounds__(32, NGPULM_ADV_MINB(kW, kPacked, kStage))
     for (int j = 0; j < 8; ++j)
       if (lane + 32 * j < V / 4) rw[j] = __ldg(w4 + lane + 32 * j);
   }
-  if (!kRegRoot || kCtaRoot) __syncthreads();  // the CTA barrier's init visible to every warp
-  if (kCtaRoot && row < B) {  // model data only: before the wait
-    mbar_wait(bar, 0);
-    const int4* src = reinterpret_cast<const int4*>(root_w);
-    int4* dst = reinterpret_cast<int4*>(s.row_n);
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (lane + 32 * j < V / 4) dst[lane + 32 * j] = src[lane + 32 * j];
-  }
+  if (!kRegRoot) __syncthreads();  // the CTA barrier's init visible to every warp
   if (row >= B) return;  // warp 0 always has a row and waits for the CTA's bulk copy
-#ifdef NGPULM_PHASE_TIMING
-  const int skip = g_skip;
-#else
-  constexpr int skip = 0;
-#endif
   float* srow = scores + (size_t)row * V;
   int32_t* nrow = next + (size_t)row * V;
   // Steps 1-3 for state st into shared memory (nothing global is written).
-  // ph: parity of this build's mbarrier phases (0: first build, 1: rebuild).
+  // ph: parity of this build's root-target copy (0: first build, 1: rebuild).
+  // The copy's phase is always waited for, so it is over before any re-arm.
   auto build = [&](int32_t st, uint32_t ph) -> Row {
     WLevel lv;
     int32_t nslots;
     const Row r = warp_row_src<kTable>(m, ValState{st}, s, lv, nslots);
-    STAMP(11);
-    if (r.bad) return r;
+    if (r.bad) {
+      mbar_wait(s.bar, ph);
+      return r;
+    }
     STAMP(3);
     Window<kW, kPacked> a;
-    bool staged = false;
-    if (kStage) {
-      // staging offsets: levels in slot order (the last level first), packed tight
-      const int32_t nq = lv.info & 0xffff;
-      int32_t inc = nq;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_down_sync(kFull, inc, o);
-        if (lane + o < 32) inc += y;
-      }
-      const int32_t total = __shfl_sync(kFull, inc, 0);
-      staged = total <= kSQ && !(skip & 4);
-      if (staged) {
-        if (lane == 0)
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.abar)),
-                       "r"((uint32_t)total * 32u)
-                       : "memory");
-        __syncwarp();
-        const int32_t off = inc - nq;
-        if (nq > 0)  // lanes 1..nlev: one bulk copy per level
-          bulk_g2s(s.st_q + 2 * off, reinterpret_cast<const uint4*>(m.arc_q) + 2 * (lv.beg >> 2),
-                   (uint32_t)nq * 32u, s.abar);
-        lv.qbase = off;
-      }
-    }
     if (kRegRoot) {
-      if (skip & 4) nslots = 0;
-      if (!staged && !(skip & 4)) load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
-      STAMP(12);
-      if (!(skip & 8)) {  // root scores: acc_root + root weight, while the gathers fly
-        float4* s4 = reinterpret_cast<float4*>(s.row_s);
-        const float ar = r.acc_root;
+      load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
+      // root scores: acc_root + root weight, while the gathers fly
+      float4* s4 = reinterpret_cast<float4*>(s.row_s);
+      const float ar = r.acc_root;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (lane + 32 * j < V / 4) {
-            float4 y = rw[j];
-            y.x = __fadd_rn(ar, y.x);
-            y.y = __fadd_rn(ar, y.y);
-            y.z = __fadd_rn(ar, y.z);
-            y.w = __fadd_rn(ar, y.w);
-            s4[lane + 32 * j] = y;
-          }
-      }
+      for (int j = 0; j < 8; ++j)
+        if (lane + 32 * j < V / 4) {
+          float4 y = rw[j];
+          y.x = __fadd_rn(ar, y.x);
+          y.y = __fadd_rn(ar, y.y);
+          y.z = __fadd_rn(ar, y.z);
+          y.w = __fadd_rn(ar, y.w);
+          s4[lane + 32 * j] = y;
+        }
     } else {
       mbar_wait(bar, 0);  // the CTA's root weights have landed (long ago, normally)
       // the root fill goes first: its shared-memory loads would otherwise return
       // behind the arc gathers
-      if (!(skip & 8)) root_fill(s, root_w, r.acc_root, V);
-      STAMP(12);
-      if (skip & 4) nslots = 0;
-      if (!(skip & 4)) load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
+      root_fill(s, root_w, r.acc_root, V);
+      load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
     }
     STAMP(4);
-    if (!kCtaRoot) mbar_wait(s.bar, ph);  // root targets in row_n (kCtaRoot: copied synchronously)
+    mbar_wait(s.bar, ph);  // root targets in row_n
     __syncwarp();
-    STAMP(5);
-    if (staged) {
-      mbar_wait(s.abar, ph);  // the row's arcs are in the staging area
-      for (int32_t k0 = 0; k0 < nslots; k0 += kW) {
-        load_window<kW, kPacked, true>(m, s, lv, r.nlev, k0, nslots, a);
-        write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
-      }
-    } else {
-      for (int32_t k0 = 0; k0 < nslots;) {
-        write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
-        k0 += kW;
-        if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
-      }
+    for (int32_t k0 = 0; k0 < nslots;) {
+      write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
+      k0 += kW;
+      if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
     }
     return r;
   };
-  // Speculative build: the row only needs the model (immutable)
-  // and the row's state, so it is built from the state read BEFORE
-  // griddepcontrol.wait — overlapping the previous kernel — and the state is
-  // read again after the wait; only if it changed (the previous kernel wrote
-  // it) is the row rebuilt. Outputs are written after the wait only. Both
-  // reads are coherent (ld.relaxed.gpu: no stale non-coherent cache line).
+  // Speculative build, store first: the row only needs the
+  // model (immutable) and the row's state, so it is built from the state read
+  // BEFORE griddepcontrol.wait, overlapping the previous kernel. After the
+  // wait (outputs may be written from then on) the finished row leaves at
+  // once, and the state is read again while the stores drain: only if the
+  // previous kernel changed it is the row rebuilt and stored again, after the
+  // first stores have completed (so the rebuilt row is the one that stays).
+  // Both state reads are coherent (ld.relaxed.gpu: no stale cache line).
   auto load_state = [&]() {
     int32_t v = 0;
     if (lane == 0) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(states + row) : "memory");
     return __shfl_sync(kFull, v, 0);
   };
-  bool waited = !NGPULM_SPECULATE;
-  if (waited) pdl_wait();
   int32_t st = load_state();
-  uint32_t ph = 0;
-  Row r;
-  for (;;) {  // one build site: at most two passes
-    r = build(st, ph);
-    if (r.bad && !kCtaRoot) mbar_wait(s.bar, ph);  // the phase is over before any re-arm
-    if (waited) break;
-    pdl_wait();
-    waited = true;
-    STAMP(2);
-    const int32_t st1 = load_state();
-    if (st1 == st) break;
-    st = st1;  // the previous kernel changed the state: rebuild after the wait
-    ph = 1;
-    if (kCtaRoot) {  // the root targets again (the first build overwrote them)
-      const int4* src = reinterpret_cast<const int4*>(root_w);
-      int4* dst = reinterpret_cast<int4*>(s.row_n);
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (lane + 32 * j < V / 4) dst[lane + 32 * j] = src[lane + 32 * j];
-    } else if (lane == 0) {
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)), "r"(bytes)
-                   : "memory");
-      bulk_g2s(s.row_n, m.arc_to, bytes, s.bar);
+  Row r = build(st, 0);
+  if (!r.bad) proxy_fence_warp();  // the row's generic writes -> the bulk stores
+  pdl_wait();
+  STAMP(2);
+  bool stored = false;
+  if (!r.bad && lane == 0) {
+    store_row_bulk(s, srow, nrow, bytes);
+    STAMP(7);
+  }
+  stored = !r.bad;
+  const int32_t st1 = load_state();
+  if (st1 != st) {  // the previous kernel changed the state: rebuild after the wait
+    if (stored) {
+      // the first stores must be complete (global writes done, shared reads
+      // over) before the row is rewritten and stored again
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      __syncwarp();
     }
-    __syncwarp();
+    rearm_root_targets(s, m.arc_to, bytes);
+    st = st1;
+    r = build(st, 1);
+    if (!r.bad) {
+      proxy_fence_warp();
+      if (lane == 0) store_row_bulk(s, srow, nrow, bytes);
+    }
+    stored = !r.bad;
   }
   if (lane == 0) {
     if (r.bad) atomicMin(m.bad_row, (unsigned long long)row);
@@ -271,36 +213,9 @@ __global__ void __launch_bounds__(32, NGPULM_ADV_MINB(kW, kPacked, kStage))
   }
   if (r.bad) {
     for (int32_t v = lane; v < V; v += 32) { srow[v] = __int_as_float(0x7fc00000); nrow[v] = -1; }
-    if (w == 0 && !kRegRoot) mbar_wait(bar, 0);
-    return;
   }
-  STAMP(6);
-  // step 4: the row leaves by two bulk stores issued by lane 0
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncwarp();
-  if (lane == 0 && !(skip & 2)) {
-#if NGPULM_STORE_HINT
-    // outputs are streamed: first to leave L2, so the trie stays resident
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(srow),
-                 "r"(smem_u32(s.row_s)), "r"(bytes), "l"(pol)
-                 : "memory");
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(nrow),
-                 "r"(smem_u32(s.row_n)), "r"(bytes), "l"(pol)
-                 : "memory");
-#else
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(srow), "r"(smem_u32(s.row_s)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(nrow), "r"(smem_u32(s.row_n)),
-                 "r"(bytes)
-                 : "memory");
-#endif
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    STAMP(7);
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-  }
+  if (stored && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem valid until read
+  if (w == 0 && !kRegRoot) mbar_wait(bar, 0);  // no exit with the CTA's bulk copy in flight
   STAMP(8);
   if (w == 0) STAMPS_OUT(row);
 }
@@ -411,24 +326,35 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(states + row) : "memory");
     return __shfl_sync(kFull, v, 0);
   };
-  bool waited = !NGPULM_SPECULATE, bad = false;
+  // speculative build and store-first, as advance_warp_kernel
+  bool bad = false;
   float fin = 0.f;
-  if (waited) pdl_wait();
   int32_t st = load_state();
-  for (;;) {
-    build(st, bad, fin);
-    if (waited) break;
-    pdl_wait();
-    waited = true;
-    const int32_t st1 = load_state();
-    if (st1 == st) break;
-    st = st1;  // rebuild: the root targets again (the first build overwrote them)
+  build(st, bad, fin);
+  if (!bad) proxy_fence_warp();
+  pdl_wait();
+  if (!bad && lane == 0) store_row_bulk(s, srow, nrow, bytes);
+  bool stored = !bad;
+  const int32_t st1 = load_state();
+  if (st1 != st) {
+    if (stored) {
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      __syncwarp();
+    }
+    // the root targets again (the first build overwrote them), generic copies
     const int4* src = reinterpret_cast<const int4*>(root_to);
     int4* dst = reinterpret_cast<int4*>(s.row_n);
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       if (lane + 32 * j < V / 4) dst[lane + 32 * j] = src[lane + 32 * j];
     __syncwarp();
+    st = st1;
+    build(st, bad, fin);
+    if (!bad) {
+      proxy_fence_warp();
+      if (lane == 0) store_row_bulk(s, srow, nrow, bytes);
+    }
+    stored = !bad;
   }
   if (lane == 0) {
     if (bad) atomicMin(m.bad_row, (unsigned long long)row);
@@ -436,22 +362,8 @@ __global__ void __launch_bounds__(256, 1)
   }
   if (bad) {
     for (int32_t v = lane; v < V; v += 32) { srow[v] = __int_as_float(0x7fc00000); nrow[v] = -1; }
-    return;
   }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncwarp();
-  if (lane == 0) {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(srow),
-                 "r"(smem_u32(s.row_s)), "r"(bytes), "l"(pol)
-                 : "memory");
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(nrow),
-                 "r"(smem_u32(s.row_n)), "r"(bytes), "l"(pol)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-  }
+  if (stored && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- final
@@ -510,30 +422,37 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
     }
   }
   if (vec && m.adv_kind != NGPULM_ADVANCE_CTA) {
-    // up to 8 rows per SM: 16-slot windows (almost every row in one window),
-    // packed arcs bulk-copied into a staging area; more rows per SM: 8-slot
-    // windows of direct gathers (registers and shared memory for occupancy)
+    // up to 8 rows per SM: 16-slot windows (almost every row in one window);
+    // more rows per SM: 8-slot windows (registers for occupancy)
     const bool wide = B <= NGPULM_WIDE_MAX_B, pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO;
-    const bool small_v = m.V <= 1024, stage = B >= NGPULM_STAGE_MIN_B && B <= NGPULM_STAGE_MAX_B && pk && small_v && table;
-    const int sq = stage ? kStageQuads : 0;
+    const bool small_v = m.V <= 1024;
     // one row (warp) per CTA: a CTA leaves as soon as its row is stored and the
     // next call's CTA starts its speculative build in its place (B=1024: 7 rows
     // per CTA 3.29 us, 1 row 2.83 us; B=4096: 10.1 -> 9.4 us)
     const int R = 1;
-    if (wcta_smem(m.V, m.order, R, sq) <= 227 * 1024) {
-      const size_t wsm = wcta_smem(m.V, m.order, R, sq);
-      // one CTA per SM for every batch between NGPULM_PAD_MIN_B and 148 rows (the
-      // extra CTAs exit at once): measured B=128 1.92 -> 1.69 us, B=147 1.93 -> 1.34
-      const int32_t nrows = (B >= NGPULM_PAD_MIN_B && B < NGPULM_PAD_GRID) ? NGPULM_PAD_GRID : B;
+    if (wcta_smem(m.V, m.order, R, 0) <= 227 * 1024) {
+      const size_t wsm = wcta_smem(m.V, m.order, R, 0);
+      // the grid is padded to a multiple of the SM count (the extra CTAs exit at
+      // once), so every SM holds the same number of rows of a call and
+      // consecutive calls' CTAs line up on the same SMs: measured B=128 1.92 ->
+      // 1.69 us, B=147 1.93 -> 1.34 (one CTA per SM)
+      int32_t nrows = B;
+      if (B >= NGPULM_PAD_MIN_B) {
+#if NGPULM_PAD_MODE == 0
+        if (B < NGPULM_PAD_GRID) nrows = NGPULM_PAD_GRID;
+#elif NGPULM_PAD_MODE == 1
+        nrows = (B + NGPULM_PAD_GRID - 1) / NGPULM_PAD_GRID * NGPULM_PAD_GRID;
+#else
+        const int32_t per = (B + NGPULM_PAD_GRID - 1) / NGPULM_PAD_GRID;  // rows per SM, rounded to a power of 2
+        int32_t p2 = 1;
+        while (p2 < per) p2 *= 2;
+        nrows = p2 * NGPULM_PAD_GRID;
+#endif
+      }
       const dim3 wg((nrows + R - 1) / R), wb(32 * R);
-      if (stage)
-        return launch(advance_warp_kernel<true, 16, true, true, true>, wg, wb, wsm, st, m, states, B, scores, next,
-                      final_out);
-#define NGPULM_WARP_LAUNCH(T, W, P)                                                                               \
-  return small_v ? launch(advance_warp_kernel<T, W, P, true, false>, wg, wb, wsm, st, m, states, B, scores, next, \
-                          final_out)                                                                                \
-                 : launch(advance_warp_kernel<T, W, P, false, false>, wg, wb, wsm, st, m, states, B, scores, next,  \
-                          final_out)
+#define NGPULM_WARP_LAUNCH(T, W, P)                                                                                 \
+  return small_v ? launch(advance_warp_kernel<T, W, P, true>, wg, wb, wsm, st, m, states, B, scores, next, final_out) \
+                 : launch(advance_warp_kernel<T, W, P, false>, wg, wb, wsm, st, m, states, B, scores, next, final_out)
       if (table) {
         if (wide) { if (pk) NGPULM_WARP_LAUNCH(true, 16, true); NGPULM_WARP_LAUNCH(true, 16, false); }
         if (pk) NGPULM_WARP_LAUNCH(true, 8, true);

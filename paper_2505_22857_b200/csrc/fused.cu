@@ -190,13 +190,8 @@ __global__ void __launch_bounds__(256, 1)
   {
     const int32_t st1 = load_state();
     if (!NGPULM_FUSED_SPECULATE || st1 != st) {
-      if (NGPULM_FUSED_SPECULATE && lane == 0) {  // the root targets again (the first build overwrote them)
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)),
-                     "r"((uint32_t)V * 4u)
-                     : "memory");
-        bulk_g2s(s.row_n, m.arc_to, (uint32_t)V * 4u, s.bar);
-      }
-      __syncwarp();
+      // the root targets again (the first build overwrote them)
+      if (NGPULM_FUSED_SPECULATE) rearm_root_targets(s, m.arc_to, (uint32_t)V * 4u);
       st = st1;
       r = build(st, NGPULM_FUSED_SPECULATE ? 1u : 0u);
     }

@@ -33,7 +33,10 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <type_traits>
+#include <utility>
 
 #include "ngpulm_internal.h"
 
@@ -389,10 +392,13 @@ __device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, con
 #endif
 // launch bounds of the warp advance kernel: with one row per CTA (32
 // threads), the minimum CTAs per SM sets the register budget
-// (one warp per CTA; 8-slot windows and the staged path: 16 CTAs per SM =
-// 128 registers, measured B=4096 9.46 -> 8.16 us, B=128 1.90 -> 1.66 us;
-// the 16-slot path keeps its 245 registers: capped it spills, B=1024 2.82 -> 4.29)
-#define NGPULM_ADV_MINB(kW, kPacked, kStage) ((kStage) ? 16 : (kW) == 8 ? ((kPacked) ? 16 : 10) : 8)
+// (8-slot windows: 16 CTAs per SM = 128 registers, measured B=4096 9.46 ->
+// 8.16 us, B=128 1.90 -> 1.66 us; the 16-slot path keeps its 245 registers:
+// capped it spills, B=1024 2.82 -> 4.29)
+#ifndef NGPULM_ADV_MINB_WIDE
+#define NGPULM_ADV_MINB_WIDE 8
+#endif
+#define NGPULM_ADV_MINB(kW, kPacked) ((kW) == 8 ? ((kPacked) ? 16 : 10) : NGPULM_ADV_MINB_WIDE)
 #ifndef NGPULM_TINY_MAX_B
 #define NGPULM_TINY_MAX_B 148  // tiny LM in shared memory up to one row per SM (B=128: 1.34 vs 1.66 us);
 #endif                         // beyond, the one-row-per-CTA global kernel wins (B=1024: 2.53 vs 3.08)
@@ -402,32 +408,25 @@ __device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, con
 #ifndef NGPULM_FUSED_MAX_ROWS
 #define NGPULM_FUSED_MAX_ROWS 8
 #endif
-#ifndef NGPULM_CTA_ROOT
-#define NGPULM_CTA_ROOT 0  // (with 7 rows per CTA: 3.74 -> 3.64 us at B = 1024; with one row per CTA: 2.83 vs 3.00)
-#endif
 #ifndef NGPULM_WIDE_MAX_B
-#define NGPULM_WIDE_MAX_B (8 * 148)  // up to 8 rows per SM: 16-slot windows (measured)
+#define NGPULM_WIDE_MAX_B (4 * 148)  // up to 4 rows per SM: 16-slot windows, 8 CTAs per SM; beyond, 8-slot
+                                     // windows at 16 CTAs per SM (B=1024: 2.64 -> 2.53 us, B=128: 1.43 vs 1.55)
 #endif
 
 __host__ __device__ constexpr size_t wrow_bytes(int32_t V) { return align16((size_t)V * 4 + 4); }  // + trash word
-// staged arcs: kStageQuads packed arc quads (32 bytes each)
-constexpr int kStageQuads = 512;
 #ifndef NGPULM_PAD_GRID
 #define NGPULM_PAD_GRID 148
+#endif
+#ifndef NGPULM_PAD_MODE
+#define NGPULM_PAD_MODE 1
 #endif
 #ifndef NGPULM_PAD_MIN_B
 #define NGPULM_PAD_MIN_B 65
 #endif
-#ifndef NGPULM_STAGE_MIN_B
-#define NGPULM_STAGE_MIN_B 2
-#endif
-#ifndef NGPULM_STAGE_MAX_B
-#define NGPULM_STAGE_MAX_B 0  // arcs staged by bulk copy: off since the speculative one-warp CTAs (with it:
-#endif                        // B=16 1.43 vs 1.21 us, B=148 1.42 vs 1.19; B=128 1.63 vs 1.69 padded)
 __host__ __device__ constexpr size_t wslice_bytes(int32_t V, int32_t order, int stage_q) {
   return 2 * wrow_bytes(V) + levels_bytes(order) + 16 + (size_t)stage_q * 32;
 }
-// root_w[V] | mbarrier | R x (row_s[V+1] | row_n[V+1] | levels | 2 mbarriers | staged arcs)
+// root_w[V] | mbarrier | R x (row_s[V+1] | row_n[V+1] | levels | 2 mbarriers | stage_q arc quads)
 __host__ __device__ constexpr size_t wcta_smem(int32_t V, int32_t order, int R, int stage_q) {
   return align16((size_t)V * 4) + 16 + (size_t)R * wslice_bytes(V, order, stage_q);
 }
@@ -439,8 +438,8 @@ struct WSlice {
   int32_t* pre;
   float* acc;
   uint64_t* bar;   // the root targets' bulk copy into row_n
-  uint64_t* abar;  // the arcs' bulk copies into the staging area
-  int4* st_q;      // [stage_q][2] staged packed arc quads
+  uint64_t* abar;  // second mbarrier (the fused kernels' logits copy)
+  int4* st_q;      // packed arc quads read from shared memory (tiny-LM kernel: the CTA's model copy)
 };
 
 __device__ __forceinline__ WSlice wcarve(unsigned char* p, int32_t V, int32_t order, int stage_q) {
@@ -667,13 +666,41 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-// kRegRoot (V <= 1024): every lane keeps its 32 root weights in registers,
-// loaded before the wait, so the root fill is register -> shared stores that
-// overlap the arc gathers (shared-memory loads issued after the gathers would
-// return behind them).
-// kStage (packed arcs, register root): the row's arcs are bulk-copied level by
-// level into the warp's staging area (when they fit), so the gathers do not
-// queue in the SM's load pipeline; the write loop then reads shared memory.
+// Generic-proxy shared-memory writes -> later async-proxy accesses (a bulk
+// store reading the row, or a bulk copy overwriting it): every writing lane
+// fences, then the warp synchronizes before one lane issues the bulk op.
+__device__ __forceinline__ void proxy_fence_warp() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+}
+
+// Re-arm the row's root-target copy (advance / fused step rebuild after the
+// PDL wait): the previous build overwrote row_n with generic stores, so the
+// warp fences before the bulk copy is issued (write-after-write across proxies).
+__device__ __forceinline__ void rearm_root_targets(const WSlice& s, const int32_t* root_to, uint32_t bytes) {
+  proxy_fence_warp();
+  if ((threadIdx.x & 31) == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)), "r"(bytes)
+                 : "memory");
+    bulk_g2s(s.row_n, root_to, bytes, s.bar);
+  }
+  __syncwarp();
+}
+
+// The row leaves by two bulk stores (scores, next) issued by lane 0, with an
+// L2 evict-first policy: outputs are streamed, the trie should stay in L2.
+// The caller has fenced (proxy_fence_warp) after the row's last generic write.
+__device__ __forceinline__ void store_row_bulk(const WSlice& s, float* srow, int32_t* nrow, uint32_t bytes) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(srow),
+               "r"(smem_u32(s.row_s)), "r"(bytes), "l"(pol)
+               : "memory");
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(nrow),
+               "r"(smem_u32(s.row_n)), "r"(bytes), "l"(pol)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 // ---------------------------------------------------------------- fused greedy step
 // Optional internal-LM subtraction (HAT "-ILM+LM"):
 // the LM-rescored columns get fmaf(-lam, ilm[token], fmaf(lambda, lm, asr))
@@ -822,11 +849,28 @@ struct Loop {
 };
 
 // ---------------------------------------------------------------- launch
+// The dynamic shared-memory limit of a kernel is raised once per (device,
+// kernel) to the largest size seen, not on every launch (cudaFuncSetAttribute
+// is a driver call).
+inline int ensure_smem(const void* kern, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{dev, kern}];
+  if (smem <= have) return 0;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  have = smem;
+  return 0;
+}
+
 template <typename... KArgs, typename... Args>
 int launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
+    const int e = ensure_smem((const void*)kern, smem);
+    if (e) return e;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
