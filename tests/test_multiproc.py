@@ -61,3 +61,22 @@ def test_gloo_world2_sharded_equals_unsharded(small_lms, tmp_path):
     assert np.array_equal(np.load(tmp_path / "s.npy").view(np.int32), s32.view(np.int32))
     assert np.array_equal(np.load(tmp_path / "n.npy"), nx)
     assert np.load(tmp_path / "t.npy")[0] == 2.0  # the slowest rank's time
+
+
+def test_bench_launcher_world2(tmp_path):
+    """`bench.py --gpus 2` without a torchrun environment launches two ranks itself
+    (torch.distributed.run, 127.0.0.1); the plumbing bench.py uses at N > 1 — rank 0
+    writing shared inputs while the others wait, the row partition, the rank-order
+    gather and the bit-identity check, rank 0 alone printing — runs over gloo."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "LOCAL_RANK", "WORLD_SIZE")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--launcher-selftest",
+                        "--workdir", str(tmp_path)], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    d = lines[0]
+    assert d["world"] == 2 and d["gpus"] == 2 and d["bit_identical"] and d["max_over_ranks"] == 2.0
