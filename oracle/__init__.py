@@ -61,6 +61,8 @@ def lib():
                                   C.c_int32, C.c_int32, f32p, i32p, i32p, C.c_int]
         L.oracle_transducer_decode.argtypes = [P, C.c_uint64, C.c_float, C.c_float, i32p, C.c_int64, i32p, C.c_float,
                                                C.c_int32, C.c_int32, C.c_int32, P, C.c_float, i32p, i32p, C.c_int]
+        L.oracle_tdt_decode.argtypes = [P, C.c_uint64, C.c_float, C.c_float, i32p, C.c_int64, i32p, C.c_float,
+                                        C.c_int32, i32p, C.c_int32, C.c_int32, C.c_int32, i32p, i32p, i32p, C.c_int]
         L.oracle_ctc_decode.argtypes = [P, f32p, C.c_int64, C.c_int64, C.c_int64, C.c_int32, P, i32p, i32p,
                                         C.c_float, C.c_int32, i32p, i32p, i32p, C.c_int]
         _lib = L
@@ -204,3 +206,23 @@ class Oracle:
                                        int(blank), int(max_symbols), int(max_len), _ptr(a), float(lam_ilm),
                                        em, el, nthreads)
         return em[:, :max_len], el, st
+
+    def tdt_decode(self, seed: int, lengths, states, durations, lam: float = 0.3, blank_id: int | None = None,
+                   max_symbols: int = 10, max_len: int = 0, temperature: float = 8.0, blank_bias: float = 0.0,
+                   nthreads: int = 0):
+        """Greedy TDT loop (R25) over the synthetic joint with
+        V+1+D columns (token columns, then one per entry of `durations`).
+        Returns (emitted [n, max_len], emit_len [n], states, steps [n])."""
+        ln = np.ascontiguousarray(lengths, dtype=np.int32)
+        n = ln.size
+        st = np.array(states, dtype=np.int32, copy=True).reshape(n)
+        du = np.ascontiguousarray(durations, dtype=np.int32)
+        max_len = max_len or int(ln.max(initial=0)) * max_symbols
+        em = np.full((n, max(1, max_len)), -1, dtype=np.int32)
+        el = np.empty(n, dtype=np.int32)
+        steps = np.empty(n, dtype=np.int32)
+        blank = self.V if blank_id is None else blank_id
+        lib().oracle_tdt_decode(self.h, seed & ((1 << 64) - 1), float(temperature), float(blank_bias), ln, n, st,
+                                float(lam), int(blank), du, int(du.size), int(max_symbols), int(max_len), em, el,
+                                steps, nthreads)
+        return em[:, :max_len], el, st, steps

@@ -514,6 +514,55 @@ void oracle_transducer_decode(void* h, uint64_t seed, float temp, float blank_bi
   });
 }
 
+// Greedy Token-and-Duration Transducer (TDT) decoding with fusion (PAPER.md:135:
+// NGPU-LM in "the Token-and-Duration Transducer (TDT)" label-looping greedy
+// decoder; R25). The joint row for (t, u, last) has V+1 token columns
+// followed by D duration columns (duration index j <-> durations[j] frames).
+// Per step: the token is the RNN-T two-stage fused decision over the token
+// columns; the duration is the raw argmax over the duration
+// columns (lowest index on ties, R14), untouched by the LM. A blank advances
+// the frame by max(d, 1) (a blank must consume a frame); a label is emitted
+// (LM state advanced) and advances the frame by d; a label with d = 0 stays on
+// the frame, and after max_sym labels on one frame the frame advances by 1.
+void oracle_tdt_decode(void* h, uint64_t seed, float temp, float blank_bias, const int32_t* lengths, int64_t n,
+                       int32_t* states, float lambda, int32_t blank_id, const int32_t* durations, int32_t D,
+                       int32_t max_sym, int32_t max_len, int32_t* emitted, int32_t* emit_len, int32_t* steps_out,
+                       int nthreads) {
+  auto* o = (Oracle*)h;
+  const int32_t ntok = o->V + 1, ncols = ntok + D;
+  parallel_rows(n, nthreads, [&](int64_t i) {
+    std::vector<float> row(ncols);
+    int32_t u = 0, last = -1, sym = 0, steps = 0;
+    for (int32_t t = 0; t < lengths[i];) {
+      joint_row(seed, t, u, last, ncols, blank_id, blank_bias, temp, row.data());
+      int32_t tok = -1, dummy = -1;
+      o->fused_step(1, row.data(), blank_id, lambda, &states[i], &dummy, &tok);
+      int32_t j = 0;  // duration: raw argmax, lowest index on ties
+      for (int32_t k = 1; k < D; ++k)
+        if (row[ntok + k] > row[ntok + j]) j = k;
+      const int32_t d = durations[j];
+      ++steps;
+      if (tok == blank_id) {
+        t += std::max(d, 1);
+        sym = 0;
+        continue;
+      }
+      if (u < max_len) emitted[i * max_len + u] = tok;
+      ++u;
+      last = o->tok_of(tok, blank_id);
+      if (d > 0) {
+        t += d;
+        sym = 0;
+      } else if (++sym >= max_sym) {
+        t += 1;
+        sym = 0;
+      }
+    }
+    emit_len[i] = u;
+    if (steps_out) steps_out[i] = steps;
+  });
+}
+
 // Greedy CTC decoding of whole utterances (SPEC.md:307-316 ctc_greedy_fused;
 // PAPER.md:138-139): for t = 0..T-1, frame t of row i (logits + i*row_stride +
 // t*frame_stride) gets one fused CTC step while t < lengths[i] (NULL: T).

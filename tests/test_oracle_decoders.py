@@ -350,3 +350,106 @@ def test_transducer_decode_fused_float64_simulator(tri):
     assert checked > 5 and got[: len(ref)] == ref
     # the LM matters at this weight
     assert got != _plain_transducer(seed, T, o.V, max_sym, temp, 0.25)
+
+
+# ---------------------------------------------------------------- greedy TDT loop (f2, R25)
+TDT_DURATIONS = np.array([0, 1, 2, 3, 4], np.int32)
+
+
+def _plain_tdt(seed, T, V, durations, max_sym, temp=8.0, bias=0.0):
+    """Plain greedy TDT over the synthetic joint (numpy twin), no LM, written from
+    the TDT decoding rule (Xu et al. 2023): token = first argmax of
+    the V+1 token columns, duration = durations[first argmax of the D duration
+    columns]; blank advances max(d, 1) frames, a label d frames (d = 0: same
+    frame, at most max_sym labels there)."""
+    out, t, u, last, sym, steps = [], 0, 0, -1, 0, 0
+    D = len(durations)
+    while t < T:
+        row = synth.synthetic_joint_raw(seed, t, u, last, V + 1 + D, temp, V, bias)
+        c = int(np.argmax(row[: V + 1]))
+        d = int(durations[int(np.argmax(row[V + 1:]))])
+        steps += 1
+        if c == V:
+            t += max(d, 1)
+            sym = 0
+            continue
+        out.append(c)
+        u, last = u + 1, c
+        if d > 0:
+            t, sym = t + d, 0
+        else:
+            sym += 1
+            if sym >= max_sym:
+                t, sym = t + 1, 0
+    return out, steps
+
+
+def test_tdt_decode_lambda0_is_plain_greedy_tdt(tri):
+    o, f = tri
+    lengths = np.array([0, 1, 5, 17, 9], np.int32)
+    for max_sym, bias in ((1, 0.0), (3, 0.5), (10, 0.75)):
+        em, el, st, steps = o.tdt_decode(4321, lengths, np.zeros(5, np.int32), TDT_DURATIONS, lam=0.0,
+                                         max_symbols=max_sym, temperature=2.0, blank_bias=bias)
+        for b, T in enumerate(lengths):
+            ref, nsteps = _plain_tdt(4321, int(T), o.V, TDT_DURATIONS, max_sym, temp=2.0, bias=bias)
+            assert list(em[b, : el[b]]) == ref and steps[b] == nsteps
+            assert st[b] == o.state_of(False, [int(x) for x in ref])
+    # durations > 1 really skip frames: fewer joint evaluations than frames + labels
+    _, el, _, steps = o.tdt_decode(4321, np.array([40], np.int32), np.zeros(1, np.int32), TDT_DURATIONS, lam=0.0,
+                                   max_symbols=3, temperature=2.0, blank_bias=0.5)
+    assert steps[0] < 40 + el[0]
+
+
+@pytest.mark.parametrize("lam", [0.0, 0.5, 2.0])
+def test_tdt_reduces_to_rnnt(tri, lam):
+    """Special cases that reduce to the (separately pinned) RNN-T loop, at any LM
+    weight: the token columns of the joint do not depend on the number of
+    duration columns, so durations = {1} is the RNN-T loop with max_symbols = 1,
+    and durations = {0} is the RNN-T loop with max_symbols labels per frame."""
+    o, f = tri
+    lengths = np.array([3, 11, 0, 8], np.int32)
+    z = np.zeros(4, np.int32)
+    for durs, max_sym in (([1], 1), ([0], 4), ([0], 1)):
+        em, el, st, _ = o.tdt_decode(99, lengths, z, np.array(durs, np.int32), lam=lam, max_symbols=max_sym,
+                                     temperature=4.0, blank_bias=0.5)
+        er, elr, sr = o.transducer_decode(99, lengths, z, lam=lam, max_symbols=max_sym, temperature=4.0,
+                                          blank_bias=0.5, max_len=em.shape[1])
+        assert np.array_equal(el, elr) and np.array_equal(st, sr)
+        for b in range(4):
+            assert list(em[b, : el[b]]) == list(er[b, : elr[b]])
+
+
+def test_tdt_decode_fused_float64_simulator(tri):
+    """lambda = 2 with durations {0..4}: the labels follow a float64 simulator
+    (score64 rows, two-stage token rule, raw duration argmax) while every stage-2
+    decision has a clear margin; the LM changes the result."""
+    o, f = tri
+    seed, T, lam, max_sym, temp, bias = 55, 30, 2.0, 3, 2.0, 0.25
+    D = len(TDT_DURATIONS)
+    em, el, st, _ = o.tdt_decode(seed, np.array([T], np.int32), np.zeros(1, np.int32), TDT_DURATIONS, lam=lam,
+                                 max_symbols=max_sym, temperature=temp, blank_bias=bias)
+    got = list(em[0, : el[0]])
+    ref, t, u, last, s, sym, checked = [], 0, 0, -1, 0, 0, 0
+    while t < T:
+        row = synth.synthetic_joint_raw(seed, t, u, last, o.V + 1 + D, temp, o.V, bias).astype(np.float64)
+        d = int(TDT_DURATIONS[int(np.argmax(row[o.V + 1:]))])
+        if int(np.argmax(row[: o.V + 1])) == o.V:
+            t, sym = t + max(d, 1), 0
+            continue
+        _, s64, nx, _ = o.rows(np.array([s], np.int32))
+        fused = row[: o.V] + lam * s64[0]
+        srt = np.sort(fused)
+        if srt[-1] - srt[-2] < 1e-3:
+            break
+        c = int(np.argmax(fused))
+        ref.append(c)
+        checked += 1
+        s, u, last = int(nx[0, c]), u + 1, c
+        if d > 0:
+            t, sym = t + d, 0
+        else:
+            sym += 1
+            if sym >= max_sym:
+                t, sym = t + 1, 0
+    assert checked > 5 and got[: len(ref)] == ref
+    assert got != _plain_tdt(seed, T, o.V, TDT_DURATIONS, max_sym, temp, bias)[0]
