@@ -49,6 +49,7 @@ enum { NGPULM_OK = 0, NGPULM_EDOMAIN = 1, NGPULM_EUSAGE = 2, NGPULM_ECUDA = 3, N
 enum { NGPULM_CTC = 0, NGPULM_RNNT = 1, NGPULM_AED = 2 };
 enum { NGPULM_MAX_ORDER = 32 };
 enum { NGPULM_MAX_TOPK = 256 };
+enum { NGPULM_MAX_DURATIONS = 32 }; /* TDT duration set size limit (ngpulm_tdt_loop_step) */
 enum { NGPULM_CHAIN_TABLE = 0, NGPULM_CHAIN_WALK = 1 };
 enum { NGPULM_ADVANCE_AUTO = 0, NGPULM_ADVANCE_WARP = 1, NGPULM_ADVANCE_CTA = 2 };
 
@@ -196,6 +197,9 @@ int ngpulm_final(const ngpulm_model* model, const int32_t* states, int32_t B, fl
  *               prev <- column.
  *   NGPULM_AED  token columns fused, the <eos> column fmaf(lambda, final(state),
  *               asr[eos]); eos -> state unchanged; else state <- next.
+ * states == NULL (with lambda == 0, else EUSAGE): plain greedy decoding without
+ * an LM, the same kernel with no LM row — the baseline of the paper's overhead
+ * figure; decisions are those of lambda = 0.
  */
 int ngpulm_fused_greedy_step(const ngpulm_model* model, int32_t mode, const float* logits,
                              int64_t row_stride, int32_t B, int32_t* states, int32_t* prev,
@@ -236,13 +240,52 @@ int ngpulm_fused_greedy_step_ilm(const ngpulm_model* model, int32_t mode, const 
  * bad-row word and ends the row (frame_idx = lengths[b]); an all-NaN logits
  * row counts as blank. All buffers dev int32 [B] except emit_out [B, max_len]
  * and logits (row stride row_stride, V+1 columns, R19); last_token may be
- * NULL. Needs V % 4 == 0 and V <= 1024. Graph-capturable. */
+ * NULL. states == NULL (lambda == 0, no ILM): plain greedy label looping
+ * without an LM. Needs V % 4 == 0 and V <= 1024. Graph-capturable. */
 int ngpulm_transducer_loop_step(const ngpulm_model* model, const float* logits, int64_t row_stride,
                                 int32_t B, int32_t* states, int32_t* frame_idx, int32_t* sym_count,
                                 const int32_t* lengths, int32_t max_symbols, float lambda,
                                 int32_t blank_id, const float* ilm, int64_t ilm_stride, float lambda_ilm,
                                 int32_t* tokens_out, int32_t* emit_out, int32_t* emit_len,
                                 int32_t* last_token, int32_t max_len, ngpulm_stream stream);
+
+/* One iteration of label-looping greedy Token-and-Duration Transducer (TDT)
+ * decoding with fusion (NGPU-LM in the TDT label-looping decoder;
+ * DESIGN.md R25). As ngpulm_transducer_loop_step, with D duration logits per
+ * row at dur_logits + b*dur_stride (dev float32; typically the joint row's
+ * columns V+1 .. V+D), and `durations` (HOST int32 [num_durations], each >= 0,
+ * 1 <= num_durations <= NGPULM_MAX_DURATIONS; copied into the launch, so a
+ * captured graph keeps the values of capture time): the token is the RNN-T
+ * two-stage fused decision; the duration d = durations[j], j = the raw argmax
+ * of the duration logits (lowest index on ties; the LM does not touch them);
+ * blank -> frame_idx += max(d, 1), sym_count = 0; a label -> emitted and LM
+ * advanced as for RNN-T, then d > 0 -> frame_idx += d, sym_count = 0, and
+ * d == 0 -> the frame is kept, sym_count += 1, and at max_symbols the frame
+ * advances by 1. durations = {1} gives the RNN-T loop with max_symbols = 1,
+ * durations = {0} the RNN-T loop with max_symbols. */
+int ngpulm_tdt_loop_step(const ngpulm_model* model, const float* logits, int64_t row_stride,
+                         const float* dur_logits, int64_t dur_stride, const int32_t* durations,
+                         int32_t num_durations, int32_t B, int32_t* states, int32_t* frame_idx,
+                         int32_t* sym_count, const int32_t* lengths, int32_t max_symbols, float lambda,
+                         int32_t blank_id, const float* ilm, int64_t ilm_stride, float lambda_ilm,
+                         int32_t* tokens_out, int32_t* emit_out, int32_t* emit_len, int32_t* last_token,
+                         int32_t max_len, ngpulm_stream stream);
+
+/* The fused greedy step of ngpulm_fused_greedy_step (same modes, rules and
+ * outputs) from LM rows computed beforehand by ngpulm_advance on the SAME
+ * states: lm_scores/lm_next dev [B, *] (row b at b*lm_stride, V entries),
+ * lm_final dev [B] (AED only, else may be NULL). Overlap mode:
+ * in a decode loop the LM query of a step depends only on the states left by
+ * the previous step, so the caller runs ngpulm_advance on a second stream while
+ * its network computes the step's logits, and this call then only reads the
+ * two rows and decides; the LM's cost leaves the loop's critical path. A row
+ * whose LM row carries the advance's invalid-state mark (next = -1) gets
+ * tokens_out = -1 and is untouched. Needs V <= 1024. */
+int ngpulm_fused_greedy_step_rows(const ngpulm_model* model, int32_t mode, const float* logits,
+                                  int64_t row_stride, int32_t B, const float* lm_scores,
+                                  const int32_t* lm_next, const float* lm_final, int64_t lm_stride,
+                                  int32_t* states, int32_t* prev, const uint8_t* active, float lambda,
+                                  int32_t blank_id, int32_t* tokens_out, ngpulm_stream stream);
 
 /* The k best fused expansions of each row, for AED beam search with NGPU-LM
  * shallow fusion. Fused value of a
@@ -287,7 +330,8 @@ int ngpulm_fused_topk(const ngpulm_model* model, const float* logits, int64_t ro
  * Needs V % 4 == 0, V <= 1024 and a finite lambda (EUSAGE otherwise); row_stride/frame_stride
  * must be multiples of 1 float (any alignment). Asynchronous, no allocation,
  * CUDA-graph capturable. An invalid start state sets the bad-row word and the
- * row decides nothing (frames -1, no emissions, state and prev unchanged). */
+ * row decides nothing (frames -1, no emissions, state and prev unchanged).
+ * states == NULL (lambda == 0): plain greedy CTC decoding without an LM. */
 int ngpulm_ctc_greedy_decode(const ngpulm_model* model, const float* logits, int64_t row_stride,
                              int64_t frame_stride, int32_t B, int32_t T, const int32_t* lengths,
                              int32_t* states, int32_t* prev, float lambda, int32_t blank_id,

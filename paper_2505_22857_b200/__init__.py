@@ -69,6 +69,10 @@ SIGNATURES = {
                                                 _P]),
     "ngpulm_transducer_loop_step": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _P, _P, _I32, _F, _I32, _P, _I64, _F,
                                                _P, _P, _P, _P, _I32, _P]),
+    "ngpulm_tdt_loop_step": (C.c_int, [_P, _P, _I64, _P, _I64, _P, _I32, _I32, _P, _P, _P, _P, _I32, _F, _I32,
+                                        _P, _I64, _F, _P, _P, _P, _P, _I32, _P]),
+    "ngpulm_fused_greedy_step_rows": (C.c_int, [_P, _I32, _P, _I64, _I32, _P, _P, _P, _I64, _P, _P, _P, _F, _I32,
+                                                 _P, _P]),
     "ngpulm_fused_topk": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _I64, _F, _F, _I32, _I32, _P, _P, _P, _P]),
     "ngpulm_ctc_greedy_decode": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _F, _I32, _P, _P, _P,
                                             _P]),
@@ -252,17 +256,18 @@ class NgpuLM:
                           B: int | None = None, stream=None):
         """ngpulm_fused_greedy_step. logits: CUDA f32 tensor whose row b starts at
         b*row_stride (default: a [B, V+1] contiguous tensor, or a strided 2-D view
-        such as logits3d[:, t] of a [B, T, V+1] tensor). states/prev updated in place."""
+        such as logits3d[:, t] of a [B, T, V+1] tensor). states/prev updated in place.
+        states=None with lam=0: plain greedy decoding (no LM)."""
         import torch
         if B is None:
-            B = states.numel()
+            B = states.numel() if states is not None else logits.shape[0]
         lp, row_stride = _rows_ptr(logits, B, self.V + 1, "logits", row_stride)
         if tokens_out is None:
-            tokens_out = torch.empty(B, dtype=torch.int32, device=states.device)
+            tokens_out = torch.empty(B, dtype=torch.int32, device=logits.device)
         blank = self.V if blank_id is None else blank_id
         _check(lib().ngpulm_fused_greedy_step(
             self._h, mode, lp, row_stride, B,
-            _dev_ptr(states, torch.int32, "states", B),
+            _dev_ptr(states, torch.int32, "states", B) if states is not None else None,
             _dev_ptr(prev, torch.int32, "prev", B) if prev is not None else None,
             _dev_ptr(active, torch.uint8, "active", B) if active is not None else None,
             float(lam), blank, _dev_ptr(tokens_out, torch.int32, "tokens_out", B), _stream(stream)))
@@ -291,26 +296,60 @@ class NgpuLM:
     def transducer_loop_step(self, logits, states, frame_idx, sym_count, lengths, emit_out, emit_len,
                              last_token=None, lam: float = 0.3, blank_id: int | None = None,
                              max_symbols: int = 10, ilm=None, lam_ilm: float = 0.0, tokens_out=None,
-                             stream=None):
-        """ngpulm_transducer_loop_step: one label-looping iteration over B rows (all int32 [B]
-        CUDA tensors updated in place; emit_out [B, max_len])."""
+                             durations=None, dur_logits=None, stream=None):
+        """One label-looping iteration over B rows (all int32 [B] CUDA tensors updated in
+        place; emit_out [B, max_len]): ngpulm_transducer_loop_step, or with `durations`
+        (a sequence of ints) ngpulm_tdt_loop_step — dur_logits [B, D] (default: the
+        logits tensor's columns V+1 .. V+D). states=None with lam=0: no LM."""
+        import torch
+        B = frame_idx.numel()
+        lp, ls = _rows_ptr(logits[:, : self.V + 1], B, self.V + 1, "logits")
+        ip, istr = _rows_ptr(ilm, B, self.V, "ilm") if ilm is not None else (None, 0)
+        if tokens_out is None:
+            tokens_out = torch.empty(B, dtype=torch.int32, device=frame_idx.device)
+        max_len = emit_out.shape[1] if emit_out.dim() == 2 else 0
+        blank = self.V if blank_id is None else blank_id
+        common = (_dev_ptr(states, torch.int32, "states", B) if states is not None else None,
+                  _dev_ptr(frame_idx, torch.int32, "frame_idx", B), _dev_ptr(sym_count, torch.int32, "sym_count", B),
+                  _dev_ptr(lengths, torch.int32, "lengths", B), int(max_symbols), float(lam), blank,
+                  ip, istr, float(lam_ilm), _dev_ptr(tokens_out, torch.int32, "tokens_out", B),
+                  _dev_ptr(emit_out, torch.int32, "emit_out", B * max_len) if max_len else None,
+                  _dev_ptr(emit_len, torch.int32, "emit_len", B),
+                  _dev_ptr(last_token, torch.int32, "last_token", B) if last_token is not None else None,
+                  max_len, _stream(stream))
+        if durations is None:
+            _check(lib().ngpulm_transducer_loop_step(self._h, lp, ls, B, *common))
+        else:
+            D = len(durations)
+            if dur_logits is None:
+                dur_logits = logits[:, self.V + 1: self.V + 1 + D]
+            dp, dstr = _rows_ptr(dur_logits, B, D, "dur_logits")
+            arr = (C.c_int32 * max(1, D))(*[int(x) for x in durations])
+            _check(lib().ngpulm_tdt_loop_step(self._h, lp, ls, dp, dstr, C.cast(arr, C.c_void_p), D, B, *common))
+        return tokens_out
+
+    def fused_greedy_step_rows(self, mode: int, logits, lm_scores, lm_next, lm_final, states, prev=None,
+                               active=None, lam: float = 0.3, blank_id: int | None = None, tokens_out=None,
+                               stream=None):
+        """ngpulm_fused_greedy_step_rows: the fused step from rows an earlier
+        advance(states) produced (lm_scores/lm_next [B, V], lm_final [B], AED only)."""
         import torch
         B = states.numel()
         lp, ls = _rows_ptr(logits, B, self.V + 1, "logits")
-        ip, istr = _rows_ptr(ilm, B, self.V, "ilm") if ilm is not None else (None, 0)
+        sp_, sstr = _rows_ptr(lm_scores, B, self.V, "lm_scores")
+        if lm_next.dtype != torch.int32 or not lm_next.is_cuda or lm_next.dim() != 2 or lm_next.shape[1] != self.V \
+                or lm_next.stride(0) != sstr or lm_next.stride(1) != 1 or lm_next.shape[0] < B:
+            raise ValueError("lm_next: expected int32 CUDA [B, V] rows with the scores' row stride")
         if tokens_out is None:
             tokens_out = torch.empty(B, dtype=torch.int32, device=states.device)
-        max_len = emit_out.shape[1] if emit_out.dim() == 2 else 0
         blank = self.V if blank_id is None else blank_id
-        _check(lib().ngpulm_transducer_loop_step(
-            self._h, lp, ls, B, _dev_ptr(states, torch.int32, "states", B),
-            _dev_ptr(frame_idx, torch.int32, "frame_idx", B), _dev_ptr(sym_count, torch.int32, "sym_count", B),
-            _dev_ptr(lengths, torch.int32, "lengths", B), int(max_symbols), float(lam), blank,
-            ip, istr, float(lam_ilm), _dev_ptr(tokens_out, torch.int32, "tokens_out", B),
-            _dev_ptr(emit_out, torch.int32, "emit_out", B * max_len) if max_len else None,
-            _dev_ptr(emit_len, torch.int32, "emit_len", B),
-            _dev_ptr(last_token, torch.int32, "last_token", B) if last_token is not None else None,
-            max_len, _stream(stream)))
+        _check(lib().ngpulm_fused_greedy_step_rows(
+            self._h, mode, lp, ls, B, sp_, lm_next.data_ptr(),
+            _dev_ptr(lm_final, torch.float32, "lm_final", B) if lm_final is not None else None, sstr,
+            _dev_ptr(states, torch.int32, "states", B),
+            _dev_ptr(prev, torch.int32, "prev", B) if prev is not None else None,
+            _dev_ptr(active, torch.uint8, "active", B) if active is not None else None,
+            float(lam), blank, _dev_ptr(tokens_out, torch.int32, "tokens_out", B), _stream(stream)))
         return tokens_out
 
     def fused_topk(self, logits, states, k: int, lam: float = 0.3, eos_id: int | None = None, ilm=None,
@@ -354,8 +393,8 @@ class NgpuLM:
         _check(lib().ngpulm_ctc_greedy_decode(
             self._h, logits.data_ptr(), logits.stride(0), logits.stride(1), B, T,
             _dev_ptr(lengths, torch.int32, "lengths", B) if lengths is not None else None,
-            _dev_ptr(states, torch.int32, "states", B), _dev_ptr(prev, torch.int32, "prev", B),
-            float(lam), blank,
+            _dev_ptr(states, torch.int32, "states", B) if states is not None else None,
+            _dev_ptr(prev, torch.int32, "prev", B), float(lam), blank,
             _dev_ptr(frames_out, torch.int32, "frames_out", B * T) if frames_out is not None else None,
             _dev_ptr(emit_out, torch.int32, "emit_out", B * T),
             _dev_ptr(emit_len, torch.int32, "emit_len", B), _stream(stream)))
@@ -410,6 +449,8 @@ ngpulm_fused_greedy_step_ilm = NgpuLM.fused_greedy_step_ilm
 ngpulm_fused_topk = NgpuLM.fused_topk
 ngpulm_save = NgpuLM.save
 ngpulm_transducer_loop_step = NgpuLM.transducer_loop_step
+ngpulm_tdt_loop_step = NgpuLM.transducer_loop_step
+ngpulm_fused_greedy_step_rows = NgpuLM.fused_greedy_step_rows
 ngpulm_load_binary = load_binary
 ngpulm_replicate = NgpuLM.replicate
 ngpulm_set_chain_mode = NgpuLM.set_chain_mode

@@ -329,7 +329,8 @@ int ngpulm_fused_greedy_step(const ngpulm_model* m, int32_t mode, const float* l
   if (blank_id < 0 || blank_id > m->h.V) return err(NGPULM_EUSAGE, "blank_id outside [0, V]");
   if (m->h.V > ngpulm::max_fused_vocab()) return err(NGPULM_EUSAGE, "fused step: the row must fit in shared memory");
   if (B == 0) return NGPULM_OK;
-  if (!logits || !states || !tokens_out || (mode == NGPULM_CTC && !prev))
+  if (!states && lambda != 0.f) return err(NGPULM_EUSAGE, "states NULL (plain greedy, no LM) needs lambda == 0");
+  if (!logits || !tokens_out || (mode == NGPULM_CTC && !prev))
     return err(NGPULM_EUSAGE, "NULL device buffer");
   if (B > 1 && row_stride < (int64_t)m->h.V + 1) return err(NGPULM_EUSAGE, "row_stride < V+1");
   int e = ngpulm::launch_fused(m->dm, mode, logits, row_stride, B, states, prev, active, lambda, blank_id, nullptr,
@@ -357,25 +358,77 @@ int ngpulm_fused_greedy_step_ilm(const ngpulm_model* m, int32_t mode, const floa
   return NGPULM_OK;
 }
 
+static int loop_step(const ngpulm_model* m, const float* logits, int64_t row_stride, const float* dur_logits,
+                     int64_t dur_stride, const int32_t* durations, int32_t D, int32_t B, int32_t* states,
+                     int32_t* frame_idx, int32_t* sym_count, const int32_t* lengths, int32_t max_symbols, float lambda,
+                     int32_t blank_id, const float* ilm, int64_t ilm_stride, float lambda_ilm, int32_t* tokens_out,
+                     int32_t* emit_out, int32_t* emit_len, int32_t* last_token, int32_t max_len,
+                     ngpulm_stream stream) {
+  if (int r = check_hot(m, B)) return r;
+  if (blank_id < 0 || blank_id > m->h.V) return err(NGPULM_EUSAGE, "blank_id outside [0, V]");
+  if (max_symbols < 1 || max_len < 0) return err(NGPULM_EUSAGE, "max_symbols < 1 or max_len < 0");
+  if (m->h.V % 4 != 0 || m->h.V > 1024) return err(NGPULM_EUSAGE, "loop step needs V % 4 == 0 and V <= 1024");
+  if (D < 0 || D > NGPULM_MAX_DURATIONS) return err(NGPULM_EUSAGE, "number of durations outside [1, NGPULM_MAX_DURATIONS]");
+  if (D > 0) {
+    if (!durations) return err(NGPULM_EUSAGE, "NULL durations");
+    for (int32_t j = 0; j < D; ++j)
+      if (durations[j] < 0) return err(NGPULM_EUSAGE, "negative duration");
+  }
+  if (B == 0) return NGPULM_OK;
+  if (!states && (lambda != 0.f || ilm)) return err(NGPULM_EUSAGE, "states NULL (plain greedy, no LM) needs lambda == 0 and no ILM");
+  if (!logits || !frame_idx || !sym_count || !lengths || !tokens_out || !emit_len ||
+      (max_len > 0 && !emit_out) || (D > 0 && !dur_logits))
+    return err(NGPULM_EUSAGE, "NULL device buffer");
+  if (B > 1 && row_stride < (int64_t)m->h.V + 1) return err(NGPULM_EUSAGE, "row_stride < V+1");
+  if (ilm && B > 1 && ilm_stride < (int64_t)m->h.V) return err(NGPULM_EUSAGE, "ilm_stride < V");
+  if (D > 0 && B > 1 && dur_stride < D) return err(NGPULM_EUSAGE, "dur_stride < number of durations");
+  int e = ngpulm::launch_transducer_loop(m->dm, logits, row_stride, B, states, frame_idx, sym_count, lengths,
+                                         max_symbols, lambda, blank_id, ilm, ilm_stride, lambda_ilm, tokens_out,
+                                         emit_out, emit_len, last_token, max_len, dur_logits, dur_stride, durations,
+                                         D, stream);
+  if (e) return cuda_err((cudaError_t)e, "transducer loop step launch");
+  return NGPULM_OK;
+}
+
 int ngpulm_transducer_loop_step(const ngpulm_model* m, const float* logits, int64_t row_stride, int32_t B,
                                 int32_t* states, int32_t* frame_idx, int32_t* sym_count, const int32_t* lengths,
                                 int32_t max_symbols, float lambda, int32_t blank_id, const float* ilm,
                                 int64_t ilm_stride, float lambda_ilm, int32_t* tokens_out, int32_t* emit_out,
                                 int32_t* emit_len, int32_t* last_token, int32_t max_len, ngpulm_stream stream) {
+  return loop_step(m, logits, row_stride, nullptr, 0, nullptr, 0, B, states, frame_idx, sym_count, lengths,
+                   max_symbols, lambda, blank_id, ilm, ilm_stride, lambda_ilm, tokens_out, emit_out, emit_len,
+                   last_token, max_len, stream);
+}
+
+int ngpulm_tdt_loop_step(const ngpulm_model* m, const float* logits, int64_t row_stride, const float* dur_logits,
+                         int64_t dur_stride, const int32_t* durations, int32_t num_durations, int32_t B,
+                         int32_t* states, int32_t* frame_idx, int32_t* sym_count, const int32_t* lengths,
+                         int32_t max_symbols, float lambda, int32_t blank_id, const float* ilm, int64_t ilm_stride,
+                         float lambda_ilm, int32_t* tokens_out, int32_t* emit_out, int32_t* emit_len,
+                         int32_t* last_token, int32_t max_len, ngpulm_stream stream) {
+  if (num_durations < 1) return err(NGPULM_EUSAGE, "number of durations outside [1, NGPULM_MAX_DURATIONS]");
+  return loop_step(m, logits, row_stride, dur_logits, dur_stride, durations, num_durations, B, states, frame_idx,
+                   sym_count, lengths, max_symbols, lambda, blank_id, ilm, ilm_stride, lambda_ilm, tokens_out,
+                   emit_out, emit_len, last_token, max_len, stream);
+}
+
+int ngpulm_fused_greedy_step_rows(const ngpulm_model* m, int32_t mode, const float* logits, int64_t row_stride,
+                                  int32_t B, const float* lm_scores, const int32_t* lm_next, const float* lm_final,
+                                  int64_t lm_stride, int32_t* states, int32_t* prev, const uint8_t* active,
+                                  float lambda, int32_t blank_id, int32_t* tokens_out, ngpulm_stream stream) {
   if (int r = check_hot(m, B)) return r;
+  if (mode != NGPULM_CTC && mode != NGPULM_RNNT && mode != NGPULM_AED) return err(NGPULM_EUSAGE, "bad mode");
   if (blank_id < 0 || blank_id > m->h.V) return err(NGPULM_EUSAGE, "blank_id outside [0, V]");
-  if (max_symbols < 1 || max_len < 0) return err(NGPULM_EUSAGE, "max_symbols < 1 or max_len < 0");
-  if (m->h.V % 4 != 0 || m->h.V > 1024) return err(NGPULM_EUSAGE, "loop step needs V % 4 == 0 and V <= 1024");
+  if (m->h.V > 1024) return err(NGPULM_EUSAGE, "fused step from rows needs V <= 1024");
   if (B == 0) return NGPULM_OK;
-  if (!logits || !states || !frame_idx || !sym_count || !lengths || !tokens_out || !emit_len ||
-      (max_len > 0 && !emit_out))
+  if (!logits || !lm_scores || !lm_next || !states || !tokens_out || (mode == NGPULM_CTC && !prev) ||
+      (mode == NGPULM_AED && !lm_final))
     return err(NGPULM_EUSAGE, "NULL device buffer");
   if (B > 1 && row_stride < (int64_t)m->h.V + 1) return err(NGPULM_EUSAGE, "row_stride < V+1");
-  if (ilm && B > 1 && ilm_stride < (int64_t)m->h.V) return err(NGPULM_EUSAGE, "ilm_stride < V");
-  int e = ngpulm::launch_transducer_loop(m->dm, logits, row_stride, B, states, frame_idx, sym_count, lengths,
-                                         max_symbols, lambda, blank_id, ilm, ilm_stride, lambda_ilm, tokens_out,
-                                         emit_out, emit_len, last_token, max_len, stream);
-  if (e) return cuda_err((cudaError_t)e, "transducer loop step launch");
+  if (B > 1 && lm_stride < (int64_t)m->h.V) return err(NGPULM_EUSAGE, "lm_stride < V");
+  int e = ngpulm::launch_fused_rows(mode, logits, row_stride, lm_scores, lm_next, lm_final, lm_stride, B, m->h.V,
+                                    states, prev, active, lambda, blank_id, tokens_out, stream);
+  if (e) return cuda_err((cudaError_t)e, "fused step (rows) launch");
   return NGPULM_OK;
 }
 
@@ -407,7 +460,8 @@ int ngpulm_ctc_greedy_decode(const ngpulm_model* m, const float* logits, int64_t
   if (m->h.V % 4 != 0 || m->h.V > 1024) return err(NGPULM_EUSAGE, "ctc decode needs V % 4 == 0 and V <= 1024");
   if (!std::isfinite(lambda)) return err(NGPULM_EUSAGE, "lambda must be finite");
   if (B == 0) return NGPULM_OK;
-  if (!states || !prev || (T > 0 && !logits)) return err(NGPULM_EUSAGE, "NULL device buffer");
+  if (!states && lambda != 0.f) return err(NGPULM_EUSAGE, "states NULL (plain greedy, no LM) needs lambda == 0");
+  if (!prev || (T > 0 && !logits)) return err(NGPULM_EUSAGE, "NULL device buffer");
   if (T > 1 && frame_stride < (int64_t)m->h.V + 1 && row_stride < (int64_t)m->h.V + 1)
     return err(NGPULM_EUSAGE, "frames overlap: frame_stride and row_stride < V+1");
   int e = ngpulm::launch_ctc_decode(m->dm, logits, row_stride, frame_stride, B, T, lengths, states, prev, lambda,

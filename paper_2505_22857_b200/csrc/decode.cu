@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
   }
   int32_t len = T;
   if (lengths) len = min(T, max(0, __ldg(&lengths[row])));
-  int32_t st = __ldg(&states[row]);
+  const bool nolm = states == nullptr;  // plain greedy CTC (no LM)
+  int32_t st = nolm ? 0 : __ldg(&states[row]);
   const bool bad = st < 0 || st >= m.S;
   const int32_t run = bad ? 0 : len;  // an invalid state decides nothing (token -1 every frame)
   const float* lrow0 = logits + (size_t)row * row_stride;
@@ -164,6 +165,11 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
 #endif
   float lm[kMaxColsPerLane];
   auto rebuild = [&](int32_t state) {
+    if (nolm) {
+#pragma unroll
+      for (int j = 0; j < kMaxColsPerLane; ++j) lm[j] = 0.f;
+      return;
+    }
     build_row_warp<kTable, kPacked>(m, s, root_w, root_to, state, stamp);
 #pragma unroll
     for (int j = 0; j < kMaxColsPerLane; ++j) {
@@ -220,7 +226,7 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
       if (bc == sp) {
         pc = -1;
       } else if (bc != pc) {  // an emission: LM advance (a repeat of prev is collapsed)
-        const int32_t ns = s.row_n[bc < sp ? bc : bc - 1];
+        const int32_t ns = nolm ? 0 : s.row_n[bc < sp ? bc : bc - 1];
         if (lane == 0 && eout) eout[nemit] = bc;
         ++nemit;
         pc = bc;
@@ -251,7 +257,7 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
   if (fout)
     for (int32_t t = run + lane; t < T; t += 32) fout[t] = -1;
   if (lane == 0) {
-    states[row] = st;
+    if (!nolm) states[row] = st;
     prev[row] = pc;
     if (emit_len) emit_len[row] = nemit;
   }

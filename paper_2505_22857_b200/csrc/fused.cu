@@ -16,6 +16,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   const int t = threadIdx.x;
   const Slice s = carve(smem, V, m.order);
   const bool tma = (V & 3) == 0;
+  const bool nolm = states == nullptr;  // plain greedy decoding (no LM)
   pdl_trigger();
   prologue(m, s, tma);
   pdl_wait();
@@ -37,7 +38,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       if (better(a, col, bv, bc)) { bv = a; bc = col; }
     }
   }
-  const Row r = row_levels<kTable>(m, states + b, s);
+  const Row r = nolm ? Row{} : row_levels<kTable>(m, states + b, s);
   if (r.bad) {
     if (t == 0) { tokens_out[b] = -1; atomicMin(m.bad_row, (unsigned long long)b); }
     if (tma) mbar_wait(s.bar, 0);
@@ -53,7 +54,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     bv = -INFINITY;
     bc = INT_MAX;
   }
-  build_row(m, s, r, tma);
+  if (nolm) {
+    if (tma) mbar_wait(s.bar, 0);  // the root copy of the prologue is over
+  } else {
+    build_row(m, s, r, tma);
+  }
   for (int32_t col = t; col < ncols; col += kThreads) {
     const float a = __ldg(&row[col]);
     float val;
@@ -64,7 +69,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       val = a;                                                        // repeated token: not rescored
     } else {
       const int32_t tok = col < sp ? col : col - 1;
-      val = __fmaf_rn(lambda, s.row_s[tok], a);  // asr + lambda * lm, one rounding
+      val = __fmaf_rn(lambda, nolm ? 0.f : s.row_s[tok], a);  // asr + lambda * lm, one rounding
       if (aux.p) val = __fmaf_rn(-aux.lam, __ldg(aux.p + (size_t)b * aux.stride + tok), val);  // - lambda_ilm * ilm (R21)
     }
     if (better(val, col, bv, bc)) { bv = val; bc = col; }
@@ -78,7 +83,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       if (bc == sp) {
         if (kMode == NGPULM_CTC) prev[b] = -1;
       } else if (!(kMode == NGPULM_CTC && bc == pc)) {  // a repeated CTC token: no LM advance
-        states[b] = s.row_n[bc < sp ? bc : bc - 1];
+        if (!nolm) states[b] = s.row_n[bc < sp ? bc : bc - 1];
         if (kMode == NGPULM_CTC) prev[b] = bc;
       }
     }
@@ -100,12 +105,13 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* lbar = s.abar;
   float* lbuf = reinterpret_cast<float*>(base + wslice_bytes(V, m.order, 0));
   const int32_t row = (int32_t)blockIdx.x * R + w;
+  const bool nolm = states == nullptr;  // plain greedy decoding (no LM): the baseline of PAPER.md:279
   STAMP(0);
   STAMP(1);
   STAMP(9);
   pdl_trigger();
   if (row >= B) return;
-  if (lane == 0) {  // root targets -> the row's next-state slots (immutable model data: before the wait)
+  if (lane == 0 && !nolm) {  // root targets -> the row's next-state slots (immutable model data: before the wait)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(s.bar)) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(lbar)) : "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -113,8 +119,12 @@ __global__ void __launch_bounds__(256, 1)
                  : "memory");
     bulk_g2s(s.row_n, m.arc_to, (uint32_t)V * 4u, s.bar);
   }
+  if (lane == 0 && nolm) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(lbar)) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   float4 rw[8];
-  {
+  if (!nolm) {
     const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
 #pragma unroll
     for (int j = 0; j < 8; ++j)
@@ -162,9 +172,12 @@ __global__ void __launch_bounds__(256, 1)
   // Speculative build (as advance_warp_kernel): the LM row from the state read
   // before griddepcontrol.wait, re-checked after it. Inputs (logits, prev,
   // active, ILM rows) are read after the wait only.
-  int32_t st = NGPULM_FUSED_SPECULATE ? load_state() : 0;
-  Row r;
-  if (NGPULM_FUSED_SPECULATE) r = build(st, 0);
+  int32_t st = 0;
+  Row r{};
+  if (NGPULM_FUSED_SPECULATE && !nolm) {
+    st = load_state();
+    r = build(st, 0);
+  }
   pdl_wait();
   STAMP(2);
   const float* lrow = logits + (size_t)row * row_stride;
@@ -187,7 +200,9 @@ __global__ void __launch_bounds__(256, 1)
     issue_frame(lrow, ncols, lbuf, lbar, pol);
   }
   const float* lb = lbuf + (reinterpret_cast<uintptr_t>(lrow) & 15) / 4;  // column c at lb[c]
-  {
+  int32_t dsel = -1;  // TDT duration (loop mode with durations), else -1
+  if (kMode == kLoop && lp.D > 0 && on) dsel = tdt_duration(lp, row);
+  if (!nolm) {
     const int32_t st1 = load_state();
     if (!NGPULM_FUSED_SPECULATE || st1 != st) {
       // the root targets again (the first build overwrote them)
@@ -234,7 +249,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int j = 0; j < kMaxColsPerLane; ++j) {
         const int32_t col = lane + 32 * j;
         const float x = xs[j];
-        const float lmv = col < ncols && col != sp ? s.row_s[col - (col > sp)] : sp_val;
+        const float lmv = nolm ? 0.f : col < ncols && col != sp ? s.row_s[col - (col > sp)] : sp_val;
         float v = __fmaf_rn(lambda, lmv, x);  // asr + lambda * lm, one rounding
         if (kAux && col != sp) v = __fmaf_rn(-aux.lam, ilm[j], v);  // - lambda_ilm * ilm (R21)
         if (kMode == NGPULM_CTC && (col == sp || col == pc)) v = x;  // blank raw, repeated token not rescored
@@ -247,26 +262,9 @@ __global__ void __launch_bounds__(256, 1)
   STAMP(7);
   if (kMode == kLoop) {
     if (lane == 0) {
-      const bool ok = bc >= 0 && bc < ncols;
-      tokens_out[row] = ok ? bc : -1;
-      int32_t fr = lp.frame[row], sy = lp.sym[row];
-      if (!ok || bc == sp) {  // blank (or an all-NaN row): next frame
-        ++fr;
-        sy = 0;
-      } else {  // a label: emit it, advance the LM, stay on the frame (up to max_sym symbols)
-        const int32_t tok = bc < sp ? bc : bc - 1;
-        const int32_t e = lp.emit_len[row];
-        if (e < lp.max_len) lp.emit[(size_t)row * lp.max_len + e] = bc;
-        lp.emit_len[row] = e + 1;
-        if (lp.last) lp.last[row] = tok;
-        states[row] = s.row_n[tok];
-        if (++sy >= lp.max_sym) {
-          ++fr;
-          sy = 0;
-        }
-      }
-      lp.frame[row] = fr;
-      lp.sym[row] = sy;
+      const bool lab = bc >= 0 && bc < ncols && bc != sp;
+      loop_epilogue(lp, row, bc, sp, ncols, states, lab && !nolm ? s.row_n[bc < sp ? bc : bc - 1] : 0, dsel,
+                    tokens_out);
     }
     return;
   }
@@ -278,7 +276,7 @@ __global__ void __launch_bounds__(256, 1)
       if (bc == sp) {
         if (kMode == NGPULM_CTC) prev[row] = -1;
       } else if (!(kMode == NGPULM_CTC && bc == pc)) {  // a repeated CTC token: no LM advance
-        states[row] = s.row_n[bc < sp ? bc : bc - 1];
+        if (!nolm) states[row] = s.row_n[bc < sp ? bc : bc - 1];
         if (kMode == NGPULM_CTC) prev[row] = bc;
       }
     }
@@ -318,13 +316,14 @@ __global__ void __launch_bounds__(256, 1)
   const int32_t row = (int32_t)blockIdx.x * R + pair;
   const uint32_t bid = 1 + pair;  // named barrier of the pair (0 is __syncthreads)
   auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bid) : "memory"); };
+  const bool nolm = states == nullptr;  // plain greedy decoding (no LM)
   pdl_trigger();
   if (row >= B) return;
   if (lane == 0) {  // A: root targets -> next-state slots; B: the logits barrier (model data / no inputs: before the wait)
     const uint64_t* bb = role == 0 ? s.bar : lbar;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bb)) : "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (role == 0) {
+    if (role == 0 && !nolm) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(s.bar)),
                    "r"((uint32_t)V * 4u)
                    : "memory");
@@ -332,7 +331,7 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
   float4 rw[8];
-  if (role == 0) {
+  if (role == 0 && !nolm) {
     const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
 #pragma unroll
     for (int j = 0; j < 8; ++j)
@@ -371,14 +370,19 @@ __global__ void __launch_bounds__(256, 1)
         const int32_t rc = warp_argmax_cols(xs);  // stage 1: standard greedy prediction
         if (lane == 0) xch[2] = rc;
       }
+      if (kMode == kLoop && lp.D > 0) {  // TDT: the duration, beside the row build
+        const int32_t d = tdt_duration(lp, row);
+        if (lane == 0) xch[9] = d;
+      }
     }
     pair_sync();  // (1) the row is built (or the row is done)
     if (xch[3]) return;
     fin = __int_as_float(xch[4]);
   } else {
     WLevel lv;
-    int32_t nslots;
-    const Row r = warp_row<kTable>(m, states + row, s, lv, nslots);
+    int32_t nslots = 0;
+    Row r{};
+    if (!nolm) r = warp_row<kTable>(m, states + row, s, lv, nslots);
     if (!on || r.bad) {
       if (lane == 0) {
         tokens_out[row] = -1;
@@ -386,10 +390,11 @@ __global__ void __launch_bounds__(256, 1)
         if (kMode == kLoop && on) lp.frame[row] = lp.len[row];
         xch[3] = 1;
       }
-      mbar_wait(s.bar, 0);
+      if (!nolm) mbar_wait(s.bar, 0);
       pair_sync();
       return;
     }
+    if (!nolm) {
     Window<kW, kPacked> a;
     load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
     {
@@ -411,6 +416,7 @@ __global__ void __launch_bounds__(256, 1)
       write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
       k0 += kW;
       if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
+    }
     }
     fin = r.fin;
     if (lane == 0) {
@@ -440,7 +446,7 @@ __global__ void __launch_bounds__(256, 1)
       const float x = xs[j];
       float v = __int_as_float(0x7fc00000);
       if ((j < kPairSplit) == (role == 0)) {
-        const float lmv = col < ncols && col != sp ? s.row_s[col - (col > sp)] : sp_val;
+        const float lmv = nolm ? 0.f : col < ncols && col != sp ? s.row_s[col - (col > sp)] : sp_val;
         v = __fmaf_rn(lambda, lmv, x);
         if (kAux && col != sp) v = __fmaf_rn(-aux.lam, ilm[j], v);
         if (kMode == NGPULM_CTC && (col == sp || col == pc)) v = x;
@@ -463,26 +469,9 @@ __global__ void __launch_bounds__(256, 1)
   }
   if (kMode == kLoop) {
     if (lane == 0) {
-      const bool ok = bc >= 0 && bc < ncols;
-      tokens_out[row] = ok ? bc : -1;
-      int32_t fr = lp.frame[row], sy = lp.sym[row];
-      if (!ok || bc == sp) {
-        ++fr;
-        sy = 0;
-      } else {
-        const int32_t tok = bc < sp ? bc : bc - 1;
-        const int32_t e = lp.emit_len[row];
-        if (e < lp.max_len) lp.emit[(size_t)row * lp.max_len + e] = bc;
-        lp.emit_len[row] = e + 1;
-        if (lp.last) lp.last[row] = tok;
-        states[row] = s.row_n[tok];
-        if (++sy >= lp.max_sym) {
-          ++fr;
-          sy = 0;
-        }
-      }
-      lp.frame[row] = fr;
-      lp.sym[row] = sy;
+      const bool lab = bc >= 0 && bc < ncols && bc != sp;
+      loop_epilogue(lp, row, bc, sp, ncols, states, lab && !nolm ? s.row_n[bc < sp ? bc : bc - 1] : 0,
+                    lp.D > 0 ? xch[9] : -1, tokens_out);
     }
     return;
   }
@@ -494,7 +483,85 @@ __global__ void __launch_bounds__(256, 1)
       if (bc == sp) {
         if (kMode == NGPULM_CTC) prev[row] = -1;
       } else if (!(kMode == NGPULM_CTC && bc == pc)) {
-        states[row] = s.row_n[bc < sp ? bc : bc - 1];
+        if (!nolm) states[row] = s.row_n[bc < sp ? bc : bc - 1];
+        if (kMode == NGPULM_CTC) prev[row] = bc;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- fused step from precomputed LM rows
+// Overlap mode: in a decode loop the LM query of step t needs
+// only the states left by step t-1, not step t's logits, so the caller issues
+// ngpulm_advance(states) on a second stream while its network computes the
+// logits, and this kernel then makes the mode's decision from the two rows
+// (R13, R14, R19): one warp per row, lane i takes
+// columns i, i+32, ... of the logits and the LM row (coalesced loads, all in
+// flight together), the two-pass warp argmax, and one gather of the winning
+// token's next state. A row whose LM row is marked invalid (next = -1, written
+// by the advance for an out-of-range state) gets token -1 and is untouched.
+template <int kMode>
+__global__ void __launch_bounds__(256)
+    fused_rows_kernel(const float* __restrict__ logits, int64_t row_stride, const float* __restrict__ lm_s,
+                      const int32_t* __restrict__ lm_n, const float* __restrict__ lm_f, int64_t lm_stride, int32_t B,
+                      int32_t V, int32_t* __restrict__ states, int32_t* __restrict__ prev,
+                      const uint8_t* __restrict__ active, float lambda, int32_t sp, int32_t* __restrict__ tokens_out) {
+  constexpr bool kTwo = kMode == NGPULM_RNNT;
+  const int lane = threadIdx.x & 31;
+  const int32_t row = (int32_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), ncols = V + 1;
+  pdl_trigger();
+  pdl_wait();  // logits, LM rows, states and prev all come from preceding kernels
+  if (row >= B) return;
+  if (active && !__ldg(&active[row])) {
+    if (lane == 0) tokens_out[row] = -1;
+    return;
+  }
+  const float* lrow = logits + (size_t)row * row_stride;
+  const float* srow = lm_s + (size_t)row * lm_stride;
+  const int32_t* nrow = lm_n + (size_t)row * lm_stride;
+  const int32_t valid = __ldg(nrow);  // -1: the advance saw an invalid state
+  const int32_t pc = (kMode == NGPULM_CTC) ? __ldg(&prev[row]) : -2;
+  const float sp_val = (kMode == NGPULM_AED) ? __ldg(&lm_f[row]) : 0.f;  // eos <-> final
+  float xs[kMaxColsPerLane], lm[kMaxColsPerLane];
+#pragma unroll
+  for (int j = 0; j < kMaxColsPerLane; ++j) {
+    const int32_t col = lane + 32 * j;
+    xs[j] = __int_as_float(0x7fc00000);  // past the last column: NaN, never taken
+    lm[j] = sp_val;
+    if (col < ncols) {
+      xs[j] = __ldg(lrow + col);
+      if (col != sp) lm[j] = __ldg(srow + (col - (col > sp)));
+    }
+  }
+  if (valid < 0) {
+    if (lane == 0) tokens_out[row] = -1;
+    return;
+  }
+  int32_t bc;
+  const int32_t rc = kTwo ? warp_argmax_cols(xs) : 0;  // stage 1
+  if (kTwo && rc == sp) {
+    bc = sp;
+  } else {
+    float val[kMaxColsPerLane];
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j) {
+      const int32_t col = lane + 32 * j;
+      float v = __fmaf_rn(lambda, lm[j], xs[j]);                    // asr + lambda * lm, one rounding
+      if (kMode == NGPULM_CTC && (col == sp || col == pc)) v = xs[j];  // blank raw, repeated token not rescored
+      if (kTwo && col == sp) v = __int_as_float(0x7fc00000);           // stage 2: non-blank only
+      val[j] = v;
+    }
+    bc = warp_argmax_cols(val);
+  }
+  if (lane == 0) {
+    if (bc < 0 || bc >= ncols) {
+      tokens_out[row] = -1;
+    } else {
+      tokens_out[row] = bc;
+      if (bc == sp) {
+        if (kMode == NGPULM_CTC) prev[row] = -1;
+      } else if (!(kMode == NGPULM_CTC && bc == pc)) {
+        states[row] = __ldg(nrow + (bc < sp ? bc : bc - 1));
         if (kMode == NGPULM_CTC) prev[row] = bc;
       }
     }
@@ -701,10 +768,30 @@ int launch_fused(const DevModel& m, int32_t mode, const float* logits, int64_t r
   }
 }
 
+int launch_fused_rows(int32_t mode, const float* logits, int64_t row_stride, const float* lm_s, const int32_t* lm_n,
+                      const float* lm_f, int64_t lm_stride, int32_t B, int32_t V, int32_t* states, int32_t* prev,
+                      const uint8_t* active, float lambda, int32_t blank, int32_t* tokens_out, void* stream) {
+  if (V > 1024) return (int)cudaErrorNotSupported;
+  const dim3 g((B + 7) / 8), b(256);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (mode) {
+    case NGPULM_CTC:
+      return launch(fused_rows_kernel<NGPULM_CTC>, g, b, 0, st, logits, row_stride, lm_s, lm_n, lm_f, lm_stride, B, V,
+                    states, prev, active, lambda, blank, tokens_out);
+    case NGPULM_RNNT:
+      return launch(fused_rows_kernel<NGPULM_RNNT>, g, b, 0, st, logits, row_stride, lm_s, lm_n, lm_f, lm_stride, B,
+                    V, states, prev, active, lambda, blank, tokens_out);
+    default:
+      return launch(fused_rows_kernel<NGPULM_AED>, g, b, 0, st, logits, row_stride, lm_s, lm_n, lm_f, lm_stride, B, V,
+                    states, prev, active, lambda, blank, tokens_out);
+  }
+}
+
 int launch_transducer_loop(const DevModel& m, const float* logits, int64_t row_stride, int32_t B, int32_t* states,
                            int32_t* frame, int32_t* sym, const int32_t* lengths, int32_t max_sym, float lambda,
                            int32_t blank, const float* aux, int64_t aux_stride, float lambda_ilm,
                            int32_t* tokens_out, int32_t* emit, int32_t* emit_len, int32_t* last, int32_t max_len,
+                           const float* dur, int64_t dur_stride, const int32_t* durations, int32_t D,
                            void* stream) {
   if (m.V % 4 != 0 || m.V > 1024) return (int)cudaErrorNotSupported;
   int R = (B + 147) / 148;
@@ -713,7 +800,8 @@ int launch_transducer_loop(const DevModel& m, const float* logits, int64_t row_s
   const dim3 wg((B + R - 1) / R), wb(32 * R);
   const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
   const AuxRow ax{aux, aux_stride, lambda_ilm};
-  const Loop lp{frame, sym, lengths, emit, emit_len, last, max_sym, max_len};
+  Loop lp{frame, sym, lengths, emit, emit_len, last, max_sym, max_len, dur, dur_stride, D, {}};
+  for (int32_t j = 0; j < D && j < kMaxDur; ++j) lp.durs[j] = durations[j];
   cudaStream_t st = (cudaStream_t)stream;
   if (B <= NGPULM_PAIR_MAX_B) {  // two warps per row
     int Rp = (B + 147) / 148;

@@ -837,7 +837,12 @@ __device__ __forceinline__ int32_t warp_argmax_range(const float (&v)[kMaxColsPe
 // then moves each row's loop state: blank -> next frame; a label -> emitted,
 // LM advance, one more symbol on this frame, and after max_sym symbols the
 // frame advances anyway.
+// Token-and-Duration Transducer (TDT; R25), D > 0:
+// the row also carries D duration logits; the duration is their raw argmax
+// (lowest index on ties, untouched by the LM): a blank advances the frame by
+// max(d, 1), a label by d (d = 0: same frame, up to max_sym labels).
 constexpr int kLoop = 3;
+constexpr int kMaxDur = NGPULM_MAX_DURATIONS;  // (include/ngpulm.h)
 struct Loop {
   int32_t* frame;        // [B] current frame of the row
   int32_t* sym;          // [B] symbols emitted on the current frame
@@ -846,7 +851,62 @@ struct Loop {
   int32_t* emit_len;     // [B] emissions so far (may exceed max_len: truncated)
   int32_t* last;         // [B] last emitted LM token (-1 none), or nullptr
   int32_t max_sym, max_len;
+  const float* dur;      // TDT: row b's duration logits at dur + b * dur_stride (D entries), or nullptr
+  int64_t dur_stride;
+  int32_t D;             // number of durations (0: RNN-T)
+  int32_t durs[kMaxDur]; // frames advanced by duration index j
 };
+
+// TDT duration of a row: the whole warp takes the raw argmax of the D duration
+// logits (NaN never taken, lowest index on ties; an all-NaN row takes index 0)
+// and returns durs[index] to every lane.
+__device__ __forceinline__ int32_t tdt_duration(const Loop& lp, int32_t row) {
+  const int lane = threadIdx.x & 31;
+  float x = -INFINITY;
+  if (lane < lp.D) {
+    x = __ldg(lp.dur + (size_t)row * lp.dur_stride + lane);
+    if (x != x) x = -INFINITY;
+  }
+  const uint32_t kmax = __reduce_max_sync(kFull, fkey(lane < lp.D ? x : -INFINITY));
+  const float M = __uint_as_float((kmax & 0x80000000u) ? (kmax ^ 0x80000000u) : ~kmax);
+  uint32_t idx = __reduce_min_sync(kFull, (lane < lp.D && x == M) ? (uint32_t)lane : 0xffffffffu);
+  if (idx >= (uint32_t)lp.D) idx = 0;
+  int32_t dv = 0;
+#pragma unroll
+  for (int j = 0; j < kMaxDur; ++j)
+    if (lane == j) dv = lp.durs[j];
+  return __shfl_sync(kFull, dv, (int)idx);
+}
+
+// The loop bookkeeping of one row after its decision bc (lane 0; d = the TDT
+// duration or -1 for RNN-T). states == nullptr: no LM state (plain greedy).
+__device__ __forceinline__ void loop_epilogue(const Loop& lp, int32_t row, int32_t bc, int32_t sp, int32_t ncols,
+                                              int32_t* states, int32_t next_state, int32_t d,
+                                              int32_t* tokens_out) {
+  const bool ok = bc >= 0 && bc < ncols;
+  tokens_out[row] = ok ? bc : -1;
+  int32_t fr = lp.frame[row], sy = lp.sym[row];
+  if (!ok || bc == sp) {  // blank (or an all-NaN row): next frame (TDT: max(d, 1) frames)
+    fr += d > 1 ? d : 1;
+    sy = 0;
+  } else {  // a label: emit it, advance the LM, stay on the frame (up to max_sym symbols)
+    const int32_t tok = bc < sp ? bc : bc - 1;
+    const int32_t e = lp.emit_len[row];
+    if (e < lp.max_len) lp.emit[(size_t)row * lp.max_len + e] = bc;
+    lp.emit_len[row] = e + 1;
+    if (lp.last) lp.last[row] = tok;
+    if (states) states[row] = next_state;
+    if (d > 0) {  // TDT: the label's duration moves the frame
+      fr += d;
+      sy = 0;
+    } else if (++sy >= lp.max_sym) {
+      ++fr;
+      sy = 0;
+    }
+  }
+  lp.frame[row] = fr;
+  lp.sym[row] = sy;
+}
 
 // ---------------------------------------------------------------- launch
 // The dynamic shared-memory limit of a kernel is raised once per (device,

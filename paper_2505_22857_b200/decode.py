@@ -38,11 +38,14 @@ class TransducerGreedyDecoder:
 
     def __init__(self, model, joint, B: int, max_frames: int, lam: float = 0.3, max_symbols: int = 10,
                  max_len: int | None = None, blank_id: int | None = None, ilm=None, lam_ilm: float = 0.0,
-                 graph_steps: int = 32, use_graph: bool = True, device=None):
+                 graph_steps: int = 32, use_graph: bool = True, device=None, durations=None, use_lm: bool = True):
         import torch
         self.m, self.joint, self.B = model, joint, B
         self.lam, self.max_symbols, self.blank_id = lam, max_symbols, blank_id
         self.ilm, self.lam_ilm = ilm, lam_ilm
+        # TDT: the joint writes V+1 token and len(durations) duration logits per row
+        self.durations = None if durations is None else [int(d) for d in durations]
+        self.use_lm = use_lm  # False: plain greedy (no LM state), the overhead baseline
         self.graph_steps, self.use_graph = graph_steps, use_graph
         self.max_frames = max_frames
         self.max_len = max_len if max_len is not None else max_frames * max_symbols
@@ -51,7 +54,8 @@ class TransducerGreedyDecoder:
         self.lengths, self.st, self.frame, self.sym, self.elen = z(), z(), z(), z(), z()
         self.last = torch.full((B,), -1, dtype=torch.int32, device=dev)
         self.emit = torch.full((B, max(1, self.max_len)), -1, dtype=torch.int32, device=dev)[:, : self.max_len]
-        self.logits = torch.empty((B, model.V + 1), dtype=torch.float32, device=dev)
+        ncols = model.V + 1 + (len(self.durations) if self.durations else 0)
+        self.logits = torch.empty((B, ncols), dtype=torch.float32, device=dev)
         self.tok = torch.empty(B, dtype=torch.int32, device=dev)
         self.active = torch.zeros((), dtype=torch.bool, device=dev)
         self.stream = torch.cuda.Stream(device=dev)  # captures need a non-default stream
@@ -59,10 +63,11 @@ class TransducerGreedyDecoder:
 
     def _iteration(self):
         self.joint(self.frame, self.elen, self.last, self.logits)
-        self.m.transducer_loop_step(self.logits, self.st, self.frame, self.sym, self.lengths, self.emit, self.elen,
-                                    last_token=self.last, lam=self.lam, blank_id=self.blank_id,
+        self.m.transducer_loop_step(self.logits, self.st if self.use_lm else None, self.frame, self.sym,
+                                    self.lengths, self.emit, self.elen, last_token=self.last,
+                                    lam=self.lam if self.use_lm else 0.0, blank_id=self.blank_id,
                                     max_symbols=self.max_symbols, ilm=self.ilm, lam_ilm=self.lam_ilm,
-                                    tokens_out=self.tok, stream=self.stream)
+                                    tokens_out=self.tok, durations=self.durations, stream=self.stream)
 
     def _body(self):
         import torch
@@ -97,6 +102,7 @@ class TransducerGreedyDecoder:
                     self._body()
             run = self.graph.replay if self.use_graph else self._body
             bound = self.max_frames * (self.max_symbols + 1) + 1  # each iteration advances a frame or emits
+            bound = (bound + self.graph_steps - 1) // self.graph_steps * self.graph_steps
             iters = 0
             while iters < bound:
                 run()
@@ -109,13 +115,15 @@ class TransducerGreedyDecoder:
 
 def transducer_greedy_decode(model, joint, lengths, states=None, lam: float = 0.3, max_symbols: int = 10,
                              max_len: int | None = None, blank_id: int | None = None, ilm=None,
-                             lam_ilm: float = 0.0, graph_steps: int = 32, use_graph: bool = True) -> TransducerResult:
-    """One-shot TransducerGreedyDecoder over lengths [B] int32 CUDA (see the class)."""
+                             lam_ilm: float = 0.0, graph_steps: int = 32, use_graph: bool = True,
+                             durations=None, use_lm: bool = True) -> TransducerResult:
+    """One-shot TransducerGreedyDecoder over lengths [B] int32 CUDA (see the class);
+    durations=[...] decodes a TDT model (the joint writes V+1+len(durations) columns)."""
     B = lengths.numel()
     max_frames = int(lengths.max().item()) if B else 0
     dec = TransducerGreedyDecoder(model, joint, B, max_frames, lam=lam, max_symbols=max_symbols, max_len=max_len,
                                   blank_id=blank_id, ilm=ilm, lam_ilm=lam_ilm, graph_steps=graph_steps,
-                                  use_graph=use_graph, device=lengths.device)
+                                  use_graph=use_graph, device=lengths.device, durations=durations, use_lm=use_lm)
     if B == 0:
         return TransducerResult(dec.emit, dec.elen, dec.st, 0)
     return dec(lengths, states)
