@@ -80,7 +80,7 @@ __device__ __forceinline__ Row build_row_warp(const DevModel& m, const WSlice& s
 
 constexpr int kDecodeMaxRows = 4;  // rows per CTA (2 warps each): 256 threads, up to 255 registers
 
-template <bool kTable, bool kPacked>
+template <bool kTable, bool kPacked, bool kNoLM = false>
 __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
     ctc_decode_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int64_t frame_stride,
                       int32_t B, int32_t T, const int32_t* __restrict__ lengths, int32_t* __restrict__ states,
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
   }
   int32_t len = T;
   if (lengths) len = min(T, max(0, __ldg(&lengths[row])));
-  const bool nolm = states == nullptr;  // plain greedy CTC (no LM)
+  constexpr bool nolm = kNoLM;  // plain greedy CTC (no LM, states == nullptr): its own instantiation
   int32_t st = nolm ? 0 : __ldg(&states[row]);
   const bool bad = st < 0 || st >= m.S;
   const int32_t run = bad ? 0 : len;  // an invalid state decides nothing (token -1 every frame)
@@ -278,6 +278,9 @@ int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride
   const dim3 g((B + R - 1) / R), b(64 * R);
   const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
   cudaStream_t st = (cudaStream_t)stream;
+  if (states == nullptr)
+    return launch(ctc_decode_kernel<true, true, true>, g, b, sm, st, m, logits, row_stride, frame_stride, B, T,
+                  lengths, states, prev, lambda, blank, depth, frames_out, emit_out, emit_len);
 #define NGPULM_DECODE_LAUNCH(TB, P)                                                                                  \
   return launch(ctc_decode_kernel<TB, P>, g, b, sm, st, m, logits, row_stride, frame_stride, B, T, lengths, states, \
                 prev, lambda, blank, depth, frames_out, emit_out, emit_len)

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   }
 }
 
-template <int kMode, bool kTable, bool kPacked, bool kAux>
+template <int kMode, bool kTable, bool kPacked, bool kAux, bool kNoLM = false>
 __global__ void __launch_bounds__(256, 1)
     fused_warp_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int32_t B,
                       int32_t* __restrict__ states, int32_t* __restrict__ prev, const uint8_t* __restrict__ active,
@@ -105,7 +105,10 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* lbar = s.abar;
   float* lbuf = reinterpret_cast<float*>(base + wslice_bytes(V, m.order, 0));
   const int32_t row = (int32_t)blockIdx.x * R + w;
-  const bool nolm = states == nullptr;  // plain greedy decoding (no LM): the baseline of PAPER.md:279
+  // plain greedy decoding without an LM (states == nullptr; the baseline of
+  // PAPER.md:279) is its own instantiation: a runtime flag here costs 4x (the
+  // speculative build no longer overlaps: 3.4 -> 13.8 us at CTC B=256)
+  constexpr bool nolm = kNoLM;
   STAMP(0);
   STAMP(1);
   STAMP(9);
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(256, 1)
 // halved argmax saves).
 constexpr int kPairSplit = 17;
 
-template <int kMode, bool kTable, bool kPacked, bool kAux>
+template <int kMode, bool kTable, bool kPacked, bool kAux, bool kNoLM = false>
 __global__ void __launch_bounds__(256, 1)
     fused_pair_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int32_t B,
                       int32_t* __restrict__ states, int32_t* __restrict__ prev, const uint8_t* __restrict__ active,
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(256, 1)
   const int32_t row = (int32_t)blockIdx.x * R + pair;
   const uint32_t bid = 1 + pair;  // named barrier of the pair (0 is __syncthreads)
   auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bid) : "memory"); };
-  const bool nolm = states == nullptr;  // plain greedy decoding (no LM)
+  constexpr bool nolm = kNoLM;  // plain greedy decoding (no LM)
   pdl_trigger();
   if (row >= B) return;
   if (lane == 0) {  // A: root targets -> next-state slots; B: the logits barrier (model data / no inputs: before the wait)
@@ -712,6 +715,13 @@ int launch_fused_mode(const DevModel& m, const float* logits, int64_t row_stride
                       int32_t* tokens_out, cudaStream_t st) {
   if (m.V % 4 == 0 && m.V <= 1024 && m.adv_kind != NGPULM_ADVANCE_CTA) {
     const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
+    if (states == nullptr) {  // plain greedy (no LM): one warp per row, no row build
+      int R = (B + 147) / 148;
+      R = R < 1 ? 1 : (R > NGPULM_FUSED_MAX_ROWS ? NGPULM_FUSED_MAX_ROWS : R);
+      return launch(fused_warp_kernel<kMode, true, true, false, true>, dim3((B + R - 1) / R), dim3(32 * R),
+                    (size_t)R * fslice_bytes(m.V, m.order), st, m, logits, row_stride, B, states, prev, active,
+                    lambda, blank, aux, Loop{}, tokens_out);
+    }
     if constexpr (kMode == NGPULM_RNNT) if (B <= NGPULM_PAIR_MAX_B) {  // two warps per row (stage 1 beside the row build)
       int R = (B + 147) / 148;
       R = R < 1 ? 1 : (R > 4 ? 4 : R);
@@ -803,6 +813,9 @@ int launch_transducer_loop(const DevModel& m, const float* logits, int64_t row_s
   Loop lp{frame, sym, lengths, emit, emit_len, last, max_sym, max_len, dur, dur_stride, D, {}};
   for (int32_t j = 0; j < D && j < kMaxDur; ++j) lp.durs[j] = durations[j];
   cudaStream_t st = (cudaStream_t)stream;
+  if (states == nullptr)  // plain greedy label looping (no LM)
+    return launch(fused_warp_kernel<kLoop, true, true, false, true>, wg, wb, wsm, st, m, logits, row_stride, B, states,
+                  (int32_t*)nullptr, (const uint8_t*)nullptr, lambda, blank, ax, lp, tokens_out);
   if (B <= NGPULM_PAIR_MAX_B) {  // two warps per row
     int Rp = (B + 147) / 148;
     Rp = Rp < 1 ? 1 : (Rp > 4 ? 4 : Rp);

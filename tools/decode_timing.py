@@ -31,7 +31,8 @@ for skip in (0, 16):
         st = torch.zeros(B, dtype=torch.int32, device="cuda")
         pv = torch.full((B,), -1, dtype=torch.int32, device="cuda")
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        L.ngpulm_debug_phases(np.zeros(16 * B, np.uint64).ctypes.data, 16 * B)  # clear
+        scratch = np.zeros(16 * B, np.uint64)  # (kept alive across the call)
+        L.ngpulm_debug_phases(scratch.ctypes.data, 16 * B)  # clear
         e0.record()
         m.ctc_greedy_decode(x, st, pv, lam=0.3)
         e1.record()
