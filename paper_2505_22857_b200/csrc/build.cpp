@@ -479,6 +479,25 @@ void build_chain_table(const HostModel& m, const std::vector<int32_t>& arc_begin
   }
 }
 
+void build_row_bounds(const HostModel& m, std::vector<float>& ub) {
+  const int32_t S = m.num_states;
+  std::vector<float> maxw((size_t)S, -INFINITY);
+  for (int32_t s = 0; s < S; ++s)
+    for (int32_t a = m.arc_off[s]; a < m.arc_off[s + 1]; ++a) maxw[s] = std::max(maxw[s], m.arc_w[a]);
+  ub.assign((size_t)S, -INFINITY);
+  const int32_t cap = std::max(1, m.order);
+  for (int32_t s = 0; s < S; ++s) {  // the chain of build_chain_table, Algorithm 1 order
+    float acc = 0.0f, u = -INFINITY;
+    int32_t x = s;
+    for (int it = 0; it < cap && x != 0; ++it) {
+      if (m.arc_off[x + 1] > m.arc_off[x]) u = std::max(u, acc + maxw[x]);
+      acc = acc + m.boff_w[x];
+      x = m.boff_to[x];
+    }
+    ub[s] = std::max(u, acc + maxw[0]);  // the root level
+  }
+}
+
 // The context trie's prefix edges (state_of) from the flat arrays alone, for
 // models loaded from NGLM files: state ids are ordered by context length
 // (R6), so walking states in id order, an arc (s, v) whose target has no

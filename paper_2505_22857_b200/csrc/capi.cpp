@@ -72,7 +72,10 @@ int upload(ngpulm_model* m, int device) {
   ngpulm::build_chain_table(h, dbeg, chain, slots);
   const size_t o_q = align256(o_to + A * 4);
   const size_t o_chain = align256(o_q + (pack ? A * 8 : 0));
-  const size_t o_bad = align256(o_chain + chain.size() * 4);
+  std::vector<float> lm_ub;
+  ngpulm::build_row_bounds(h, lm_ub);
+  const size_t o_hi = align256(o_chain + chain.size() * 4);
+  const size_t o_bad = align256(o_hi + S * 4);
   const size_t total = align256(o_bad + 8);
   std::vector<unsigned char> stage(total, 0);
   auto* rec = reinterpret_cast<ngpulm::StateRec*>(stage.data() + o_srec);
@@ -98,6 +101,7 @@ int upload(ngpulm_model* m, int device) {
   }
   std::memcpy(stage.data() + o_fin, h.final_w.data(), S * 4);
   std::memcpy(stage.data() + o_chain, chain.data(), chain.size() * 4);
+  std::memcpy(stage.data() + o_hi, lm_ub.data(), S * 4);
   std::memset(stage.data() + o_bad, 0xff, 8);
 
   DeviceGuard g(device);
@@ -125,6 +129,7 @@ int upload(ngpulm_model* m, int device) {
   m->dm.arc_q = pack ? static_cast<const void*>(base + o_q) : nullptr;
   m->dm.pk_bits = pk_bits;
   m->dm.adv_kind = NGPULM_ADVANCE_AUTO;
+  m->dm.lm_ub = reinterpret_cast<const float*>(base + o_hi);
   // tiny LM (keyword-biasing size): chain table + packed quads <= 96 KiB stay in shared memory
   const size_t chain_bytes = chain.size() * 4, arcq_bytes = pack ? A * 8 : 0;
   const bool tiny = pack && h.V <= 1024 && h.V % 4 == 0 && chain_bytes + arcq_bytes <= ((size_t)96 << 10);

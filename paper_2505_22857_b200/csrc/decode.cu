@@ -1,5 +1,7 @@
 // Whole-utterance greedy CTC decoding with shallow fusion in one launch
 // for sm_100a, and its launcher.
+#include <cfloat>
+
 #include "kcommon.cuh"
 
 namespace ngpulm {
@@ -263,12 +265,451 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
   }
 }
 
+// ---------------------------------------------------------------- bound-pruned persistent CTC decode
+// The same decisions as ctc_decode_kernel (T fused CTC steps, PAPER.md:139;
+// R13, R14, R17, R19) without building the LM row and scanning all V+1
+// columns after every emission. One CTA (2 + kSumWarps warps) per row:
+//  * producer: streams the frames through a TMA ring (as ctc_decode_kernel);
+//  * summary warps (frame t -> warp t % kSumWarps; frame-parallel, LM-free):
+//    the blank column's raw value xb and the two largest raw token values
+//    with their columns and the third value (x1 c1, x2 c2, x3);
+//  * decider: walks the frames in order with the state s, its chain record,
+//    ub(s) (load-time bound: every score of the row of s is <= ub(s)) and the
+//    chain's arcs staged in shared memory by TMA (one bulk copy per level,
+//    slot layout). For lambda >= 0 a token v has fused value
+//    fmaf(lambda, lm, x[v]) <= fmaf(lambda, ub(s), x[v]) (monotone rounding),
+//    so every token outside a candidate set C is below
+//    fmaf(lambda, ub(s), largest raw value outside C).
+//    Level 0: C = {} (the repeated column pc, raw, and the blank, raw, are
+//    exact): the better of them wins if it beats that bound strictly — no LM
+//    value is needed. Level 1: C = {c1, c2}: their exact fused values from the
+//    staged arcs (the highest-order level holding the token wins, Algorithm 1
+//    lines 77-79; else the root level) against the bound with x3. Level 2
+//    (no strict winner): the exact step of ctc_decode_kernel over the full
+//    row, built in shared memory from the staged arcs and kept while the
+//    state stays.
+// Every decision is the full argmax's (tested bit-exact against the oracle
+// and ctc_decode_kernel); plain greedy (states == nullptr) is the summaries'
+// raw argmax.
+#ifndef NGPULM_SUM_WARPS
+#define NGPULM_SUM_WARPS 4
+#endif
+#ifndef NGPULM_DECODE_BOUND
+#define NGPULM_DECODE_BOUND 0
+#endif
+constexpr int kSumWarps = NGPULM_SUM_WARPS;
+constexpr int kStageSlots = 16;  // staged arc slots (32 quads each) per row; beyond: global gathers at level 2
+constexpr int kRing2 = 8;        // frames in flight per row
+
+struct FrameSum {  // per frame, LM-free (32 B)
+  float xb, x1, x2, x3;
+  int32_t c1, c2, pad0, pad1;  // columns of x1, x2 (-1: none)
+};
+
+__host__ __device__ constexpr size_t stage2_bytes(bool packed) { return (size_t)kStageSlots * 32 * (packed ? 32 : 48); }
+// root_w | root_to | cbar | WSlice | full, empty, sfull [kRing2] | sbar | sums [kRing2] | ring [kRing2] | stage
+__host__ __device__ constexpr size_t d2_smem(int32_t V, int32_t order, bool packed) {
+  return 2 * align16((size_t)V * 4) + 16 + wslice_bytes(V, order, 0) + 3 * kRing2 * 8 + 16 +
+         kRing2 * sizeof(FrameSum) + (size_t)kRing2 * lbuf_bytes(V) + stage2_bytes(packed);
+}
+
+__device__ __forceinline__ float unkey(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k ^ 0x80000000u) : ~k);
+}
+// NaN: 0, below every value; -0 and +0 share a key
+__device__ __forceinline__ uint32_t nkey(float v) { return v == v ? fkey(v + 0.0f) : 0u; }
+
+// The two largest values of a row held in registers (lane i: columns i + 32 j;
+// NaN never taken) with their columns (lowest column among equal values; -1:
+// none) and the third value (-inf: none): three rounds of a lane max tree and
+// a warp max, the winning column dropped after each.
+__device__ __forceinline__ void top2(float (&v)[kMaxColsPerLane], float& M1, int32_t& C1, float& M2, int32_t& C2,
+                                     float& M3) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int r = 0; r < 3; ++r) {
+    float t[kMaxColsPerLane];
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j) t[j] = v[j];
+#pragma unroll
+    for (int d = 1; d < kMaxColsPerLane; d *= 2)
+#pragma unroll
+      for (int j = 0; j + d < kMaxColsPerLane; j += 2 * d) t[j] = fmaxf(t[j], t[j + d]);
+    const uint32_t K = __reduce_max_sync(kFull, nkey(t[0]));
+    const float M = K ? unkey(K) : -INFINITY;
+    if (r == 2) { M3 = M; break; }
+    uint32_t cm = 0xffffffffu;
+#pragma unroll
+    for (int j = kMaxColsPerLane - 1; j >= 0; --j) cm = (K && v[j] == M) ? (uint32_t)(lane + 32 * j) : cm;
+    const int32_t C = (int32_t)__reduce_min_sync(kFull, cm);
+    if (r == 0) { M1 = M; C1 = C; } else { M2 = M; C2 = C; }
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j) v[j] = lane + 32 * j == C ? __int_as_float(0x7fc00000) : v[j];
+  }
+}
+
+template <bool kPacked, bool kNoLM>
+__global__ void __launch_bounds__(32 * (2 + kSumWarps), 2)
+    ctc_decode2_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int64_t frame_stride,
+                       int32_t B, int32_t T, const int32_t* __restrict__ lengths, int32_t* __restrict__ states,
+                       int32_t* __restrict__ prev, float lambda, int32_t sp, int32_t* __restrict__ frames_out,
+                       int32_t* __restrict__ emit_out, int32_t* __restrict__ emit_len) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int32_t V = m.V, ncols = V + 1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;  // 0 decider, 1 producer, 2.. summaries
+  const size_t rb = align16((size_t)V * 4);
+  float* root_w = reinterpret_cast<float*>(smem);
+  int32_t* root_to = reinterpret_cast<int32_t*>(smem + rb);
+  uint64_t* cbar = reinterpret_cast<uint64_t*>(smem + 2 * rb);
+  unsigned char* p = smem + 2 * rb + 16;
+  const WSlice s = wcarve(p, V, m.order, 0);
+  p += wslice_bytes(V, m.order, 0);
+  uint64_t* full = reinterpret_cast<uint64_t*>(p);
+  uint64_t* empty = full + kRing2;
+  uint64_t* sfull = empty + kRing2;
+  uint64_t* sbar = sfull + kRing2;
+  p += 3 * kRing2 * 8 + 16;
+  FrameSum* sums = reinterpret_cast<FrameSum*>(p);
+  p += kRing2 * sizeof(FrameSum);
+  float* ring = reinterpret_cast<float*>(p);
+  const size_t lstride = lbuf_bytes(V) / 4;
+  p += (size_t)kRing2 * lbuf_bytes(V);
+  unsigned char* stage = p;
+  constexpr int kSQ = kStageSlots * 32;  // staged quads
+  const int32_t row = (int32_t)blockIdx.x;
+  pdl_trigger();
+  if (threadIdx.x == 0) {  // root level (immutable model data: before the wait) and the barriers
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(cbar)) : "memory");
+    for (int i = 0; i < kRing2; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + i)) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_u32(empty + i)) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(sfull + i)) : "memory");
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(sbar)) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(cbar)), "r"((uint32_t)V * 8u)
+                 : "memory");
+    bulk_g2s(root_w, m.arc_w, (uint32_t)V * 4u, cbar);
+    bulk_g2s(root_to, m.arc_to, (uint32_t)V * 4u, cbar);
+  }
+  __syncthreads();
+  pdl_wait();
+  int32_t len = T;
+  if (lengths) len = min(T, max(0, __ldg(&lengths[row])));
+  int32_t st = kNoLM ? 0 : __ldg(&states[row]);
+  const bool bad = st < 0 || st >= m.S;
+  const int32_t run = bad ? 0 : len;
+  const float* lrow0 = logits + (size_t)row * row_stride;
+  auto frame_buf = [&](int32_t t) {  // column c of frame t at [c]
+    const float* lrow = lrow0 + (size_t)t * frame_stride;
+    return ring + (size_t)(t % kRing2) * lstride + (reinterpret_cast<uintptr_t>(lrow) & 15) / 4;
+  };
+  if (wid == 1) {  // ---- producer
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    for (int32_t t = 0; t < run; ++t) {
+      const int32_t slot = t % kRing2;
+      if (t >= kRing2) mbar_wait(empty + slot, (uint32_t)(t / kRing2 - 1) & 1u);
+      issue_frame(lrow0 + (size_t)t * frame_stride, ncols, ring + (size_t)slot * lstride, full + slot, pol);
+    }
+    return;
+  }
+  mbar_wait(cbar, 0);
+  if (wid >= 2) {  // ---- summary warps
+    for (int32_t t = wid - 2; t < run; t += kSumWarps) {
+      const int32_t slot = t % kRing2;
+      mbar_wait(full + slot, (uint32_t)(t / kRing2) & 1u);
+      const float* fb = frame_buf(t);
+      float v[kMaxColsPerLane];
+#pragma unroll
+      for (int j = 0; j < kMaxColsPerLane; ++j) {
+        const int32_t col = lane + 32 * j;
+        v[j] = (col < ncols && col != sp) ? fb[col] : __int_as_float(0x7fc00000);
+      }
+      float x1, x2, x3;
+      int32_t c1, c2;
+      top2(v, x1, c1, x2, c2, x3);
+      if (lane == 0) {
+        float4* d4 = reinterpret_cast<float4*>(sums + slot);
+        d4[0] = make_float4(fb[sp], x1, x2, x3);
+        d4[1] = make_float4(__int_as_float(c1), __int_as_float(c2), 0.f, 0.f);
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(sfull + slot)) : "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + slot)) : "memory");
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  // ---- decider
+  int32_t pc = __ldg(&prev[row]);
+  int32_t* fout = frames_out ? frames_out + (size_t)row * T : nullptr;
+  int32_t* eout = emit_out ? emit_out + (size_t)row * T : nullptr;
+  if (bad && len > 0 && lane == 0) atomicMin(m.bad_row, (unsigned long long)row);
+  WLevel lv;
+  int32_t nslots = 0, nlev = 0, row_state = -1;
+  float acc_root = 0.f, ub = 0.f;
+  bool staged = false, spend = false;
+  uint32_t nst = 0;  // stagings issued
+  auto stage_wait = [&]() {
+    if (spend) { mbar_wait(sbar, (nst - 1u) & 1u); spend = false; }
+  };
+#ifdef NGPULM_PHASE_TIMING
+  // debug build: per row 0 summary waits, 1 level 0, 2 lookups (incl. staging wait), 3 staging wait,
+  // 4 level-2 builds, 5 level-2 argmax, 6 state loads, 7 output; counts 8 level0, 9 level1, 10 level2,
+  // 11 builds, 12 state loads
+  long long ck[13] = {0};
+  long long tk0 = clock64(), tk1;
+#define D2STAMP(i) do { tk1 = clock64(); ck[i] += tk1 - tk0; tk0 = tk1; } while (0)
+#define D2COUNT(i) do { ck[i] += 1; } while (0)
+#else
+#define D2STAMP(i) do { } while (0)
+#define D2COUNT(i) do { } while (0)
+#endif
+  const bool fast = !kNoLM && lambda >= 0.f && lambda <= FLT_MAX;
+  bool need_state = !kNoLM && run > 0;
+  int32_t nemit = 0;
+  for (int32_t t = 0; t < run; ++t) {
+    if (need_state) {  // the decider's view of st: chain record, ub(st), arcs staged by TMA
+      need_state = false;
+      float uv = 0.f;
+      const Row r = warp_row_src<true>(m, ValState{st}, s, lv, nslots, [&] {
+        if (lane == 0) uv = __ldg(m.lm_ub + st);
+      });
+      nlev = r.nlev;
+      acc_root = r.acc_root;
+      ub = __shfl_sync(kFull, uv, 0);
+      staged = nslots <= kStageSlots;
+      if (staged) {
+        stage_wait();        // no copy for the previous state still landing
+        proxy_fence_warp();  // the staging area's generic reads before the async overwrite
+        const int32_t nq = (lane >= 1 && lane <= nlev) ? (lv.info & 0xffff) : 0;
+        const uint32_t bytes = __reduce_add_sync(kFull, (uint32_t)nq * (kPacked ? 32u : 48u));
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(sbar)), "r"(bytes)
+                       : "memory");
+        __syncwarp();
+        if (nq > 0) {
+          const size_t q0 = (size_t)(lv.info >> 16) * 32;  // the level's first slot
+          if (kPacked) {
+            bulk_g2s(stage + q0 * 32, static_cast<const unsigned char*>(m.arc_q) + (size_t)lv.qbase * 32,
+                     (uint32_t)nq * 32u, sbar);
+          } else {
+            bulk_g2s(stage + q0 * 16, m.arc_tok + (size_t)lv.qbase * 4, (uint32_t)nq * 16u, sbar);
+            bulk_g2s(stage + (kSQ + q0) * 16, m.arc_w + (size_t)lv.qbase * 4, (uint32_t)nq * 16u, sbar);
+            bulk_g2s(stage + (2 * kSQ + q0) * 16, m.arc_to + (size_t)lv.qbase * 4, (uint32_t)nq * 16u, sbar);
+          }
+        }
+        ++nst;
+        spend = true;
+      }
+      D2COUNT(12);
+      D2STAMP(6);
+    }
+    const int32_t slot = t % kRing2;
+    const uint32_t ph = (uint32_t)(t / kRing2) & 1u;
+    mbar_wait(sfull + slot, ph);
+    mbar_wait(full + slot, ph);  // (already complete: the summary warp saw it) the frame's bytes for this warp
+    D2STAMP(0);
+    const float* fb = frame_buf(t);
+    const float4 s0 = reinterpret_cast<const float4*>(sums + slot)[0];
+    const int4 s1 = reinterpret_cast<const int4*>(sums + slot)[1];
+    float bv = -INFINITY;  // the best exactly valued (value, column) so far (R14 order)
+    int32_t bc = INT_MAX, ns = st;
+    bool got = false;
+    if (kNoLM) {  // plain greedy: every column raw
+      if (better(s0.x, sp, bv, bc)) { bv = s0.x; bc = sp; }
+      if (s1.x >= 0 && better(s0.y, s1.x, bv, bc)) { bv = s0.y; bc = s1.x; }
+      got = true;
+    } else if (fast) {
+      if (better(s0.x, sp, bv, bc)) { bv = s0.x; bc = sp; }  // blank: fmaf(lambda, 0, x) == x
+      if (pc >= 0) {                                          // the repeated column: raw (R17)
+        const float xp = fb[pc];
+        if (better(xp, pc, bv, bc)) { bv = xp; bc = pc; }
+      }
+      if (bv > __fmaf_rn(lambda, ub, s1.x != pc ? s0.y : s0.z)) {
+        got = true;  // level 0
+        D2COUNT(8);
+        D2STAMP(1);
+      } else if (staged) {
+        D2STAMP(1);
+        // level 1: the exact fused values of c1, c2 (pc excluded: its value is raw)
+        const int32_t ca = s1.x == pc ? -1 : s1.x, cb = (s1.y == pc || s1.y == s1.x) ? -1 : s1.y;
+        const int32_t va = ca < 0 ? -1 : ca - (ca > sp), vb = cb < 0 ? -1 : cb - (cb > sp);
+        stage_wait();
+        D2STAMP(3);
+        const uint32_t tmask = kPacked ? (1u << m.pk_bits) - 1u : 0xffffffffu;
+        uint32_t ka = 0u, kb = 0u;  // the last (highest-order) hit: (slot << 7 | lane << 2 | j) + 1
+#pragma unroll 2
+        for (int32_t k = 0; k < nslots; ++k) {
+          const int32_t L = nlev - 1 - __popc(__ballot_sync(kFull, lv.eslot <= k));
+          const int32_t info = __shfl_sync(kFull, lv.info, L + 1);
+          if ((k - (info >> 16)) * 32 + lane < (info & 0xffff)) {
+            const int4 q = reinterpret_cast<const int4*>(stage)[kPacked ? 2 * (k * 32 + lane) : k * 32 + lane];
+            const uint32_t tk[4] = {(uint32_t)q.x & tmask, (uint32_t)q.y & tmask, (uint32_t)q.z & tmask,
+                                    (uint32_t)q.w & tmask};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t key = (uint32_t)((k << 7) | (lane << 2) | j) + 1u;
+              if (tk[j] == (uint32_t)va) ka = key;
+              if (tk[j] == (uint32_t)vb) kb = key;
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int32_t col = c ? cb : ca, vt = c ? vb : va;
+          const uint32_t kk = __reduce_max_sync(kFull, c ? kb : ka);
+          if (col < 0) continue;
+          float lmv;
+          int32_t nxv;
+          if (kk) {
+            const uint32_t pos = kk - 1u;
+            const int32_t k = (int32_t)(pos >> 7), qi = k * 32 + (int32_t)((pos >> 2) & 31u), j = (int32_t)(pos & 3u);
+            const int32_t L = nlev - 1 - __popc(__ballot_sync(kFull, lv.eslot <= k));
+            const float acc = __shfl_sync(kFull, lv.acc, L + 1);
+            float w;
+            if (kPacked) {
+              nxv = (int32_t)(reinterpret_cast<const uint32_t*>(stage)[qi * 8 + j] >> m.pk_bits);
+              w = reinterpret_cast<const float*>(stage)[qi * 8 + 4 + j];
+            } else {
+              w = reinterpret_cast<const float*>(stage + (size_t)kSQ * 16)[qi * 4 + j];
+              nxv = reinterpret_cast<const int32_t*>(stage + (size_t)2 * kSQ * 16)[qi * 4 + j];
+            }
+            lmv = __fadd_rn(acc, w);  // acc_boff + arc weight (Alg. 1 line 74)
+          } else {
+            lmv = __fadd_rn(acc_root, root_w[vt]);  // the root level
+            nxv = root_to[vt];
+          }
+          const float fv = __fmaf_rn(lambda, lmv, fb[col]);
+          if (better(fv, col, bv, bc)) { bv = fv; bc = col; ns = nxv; }
+        }
+        if (bv > __fmaf_rn(lambda, ub, s0.w)) { got = true; D2COUNT(9); }  // level 1
+        D2STAMP(2);
+      }
+    }
+    if (!got) {  // level 2: the exact step over the full row (ctc_decode_kernel's frame)
+      D2COUNT(10);
+      if (row_state != st) {
+        if (kPacked && staged) {  // the row from the staged arcs: root level, then the levels in slot order
+          stage_wait();
+          {
+            const float4* w4 = reinterpret_cast<const float4*>(root_w);
+            const int4* t4 = reinterpret_cast<const int4*>(root_to);
+            float4* s4 = reinterpret_cast<float4*>(s.row_s);
+            int4* n4 = reinterpret_cast<int4*>(s.row_n);
+            for (int32_t q = lane; q < V / 4; q += 32) {
+              float4 y = w4[q];
+              y.x = __fadd_rn(acc_root, y.x);
+              y.y = __fadd_rn(acc_root, y.y);
+              y.z = __fadd_rn(acc_root, y.z);
+              y.w = __fadd_rn(acc_root, y.w);
+              s4[q] = y;
+              n4[q] = t4[q];
+            }
+          }
+          __syncwarp();
+          const uint32_t tmask = (1u << m.pk_bits) - 1u;
+#pragma unroll 1
+          for (int32_t k = 0; k < nslots; ++k) {  // slot order = level order, lowest order first (Alg. 1 lines 77-79)
+            const int32_t L = nlev - 1 - __popc(__ballot_sync(kFull, lv.eslot <= k));
+            const int32_t info = __shfl_sync(kFull, lv.info, L + 1);
+            const float acc = __shfl_sync(kFull, lv.acc, L + 1);
+            if ((k - (info >> 16)) * 32 + lane < (info & 0xffff)) {
+              const int4 q = reinterpret_cast<const int4*>(stage)[2 * (k * 32 + lane)];
+              const float4 w = reinterpret_cast<const float4*>(stage)[2 * (k * 32 + lane) + 1];
+              const int32_t qq[4] = {q.x, q.y, q.z, q.w};
+              const float ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t x = (uint32_t)qq[j];
+                s.row_s[x & tmask] = __fadd_rn(acc, ww[j]);
+                s.row_n[x & tmask] = (int32_t)(x >> m.pk_bits);
+              }
+            }
+            __syncwarp();
+          }
+          __syncwarp();
+        } else {
+          build_row_warp<true, kPacked>(m, s, root_w, root_to, st);
+        }
+        row_state = st;
+        D2COUNT(11);
+      }
+      D2STAMP(4);
+      float val[kMaxColsPerLane];
+#pragma unroll
+      for (int j = 0; j < kMaxColsPerLane; ++j) {
+        const int32_t col = lane + 32 * j;
+        float x = __int_as_float(0x7fc00000);  // past the last column: NaN, never selected
+        float lmv = 0.f;                        // blank: 0
+        if (col < ncols) {
+          x = fb[col];
+          if (col != sp) lmv = s.row_s[col - (col > sp)];
+        }
+        val[j] = col == pc ? x : __fmaf_rn(lambda, lmv, x);
+      }
+      bc = warp_argmax_cols(val);
+      if (bc >= 0 && bc < ncols && bc != sp && bc != pc) ns = s.row_n[bc < sp ? bc : bc - 1];
+      D2STAMP(5);
+    }
+    int32_t tok = -1;
+    if (bc >= 0 && bc < ncols) {
+      tok = bc;
+      if (bc == sp) {
+        pc = -1;
+      } else if (bc != pc) {  // an emission: LM advance (a repeat of prev is collapsed)
+        if (lane == 0 && eout) eout[nemit] = bc;
+        ++nemit;
+        pc = bc;
+        if (!kNoLM && ns != st) { st = ns; need_state = true; }
+      }
+    }
+    if (lane == 0 && fout) fout[t] = tok;
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + slot)) : "memory");
+    D2STAMP(7);
+  }
+#ifdef NGPULM_PHASE_TIMING
+  if (lane == 0 && row < 16384)
+    for (int i = 0; i < 13; ++i) g_phase[row * 16 + i] = (unsigned long long)ck[i];
+#endif
+#undef D2STAMP
+#undef D2COUNT
+  stage_wait();  // no bulk copy in flight at exit
+  if (fout)
+    for (int32_t t = run + lane; t < T; t += 32) fout[t] = -1;
+  if (lane == 0) {
+    if (!kNoLM) states[row] = st;
+    prev[row] = pc;
+    if (emit_len) emit_len[row] = nemit;
+  }
+}
+
 }  // namespace
 
 int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride, int64_t frame_stride, int32_t B,
                       int32_t T, const int32_t* lengths, int32_t* states, int32_t* prev, float lambda, int32_t blank,
                       int32_t* frames_out, int32_t* emit_out, int32_t* emit_len, void* stream) {
   if (m.V % 4 != 0 || m.V > 1024) return (int)cudaErrorNotSupported;
+  if (B <= 0) return 0;
+  const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  // plain greedy (no LM): the summary warps' raw argmax, frame-parallel. With an LM the default is
+  // ctc_decode_kernel; the bound-pruned variant (NGPULM_DECODE_BOUND=1 builds) is exact too but its
+  // single decider warp measured slower (configs[2]: 1.15 vs 0.69 ms).
+  if (states == nullptr || (NGPULM_DECODE_BOUND && table)) {
+    const size_t sm = d2_smem(m.V, m.order, pk);
+    const dim3 g(B), b(32 * (2 + kSumWarps));
+#define NGPULM_DECODE2(P, NOLM)                                                                                    \
+  return launch(ctc_decode2_kernel<P, NOLM>, g, b, sm, st, m, logits, row_stride, frame_stride, B, T, lengths,     \
+                states, prev, lambda, blank, frames_out, emit_out, emit_len)
+    if (states == nullptr) NGPULM_DECODE2(true, true);
+#if NGPULM_DECODE_BOUND
+    if (pk) NGPULM_DECODE2(true, false);
+    NGPULM_DECODE2(false, false);
+#endif
+#undef NGPULM_DECODE2
+  }
   int R = (B + 147) / 148;
   R = R < 1 ? 1 : (R > kDecodeMaxRows ? kDecodeMaxRows : R);
   int depth = kRingMax;
@@ -276,11 +717,6 @@ int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride
   while (R > 1 && dcta_smem(m.V, m.order, R, depth) > 227 * 1024) --R;
   const size_t sm = dcta_smem(m.V, m.order, R, depth);
   const dim3 g((B + R - 1) / R), b(64 * R);
-  const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (states == nullptr)
-    return launch(ctc_decode_kernel<true, true, true>, g, b, sm, st, m, logits, row_stride, frame_stride, B, T,
-                  lengths, states, prev, lambda, blank, depth, frames_out, emit_out, emit_len);
 #define NGPULM_DECODE_LAUNCH(TB, P)                                                                                  \
   return launch(ctc_decode_kernel<TB, P>, g, b, sm, st, m, logits, row_stride, frame_stride, B, T, lengths, states, \
                 prev, lambda, blank, depth, frames_out, emit_out, emit_len)

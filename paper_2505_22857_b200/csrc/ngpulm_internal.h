@@ -68,6 +68,13 @@ bool packable(const HostModel& m);
 void build_chain_table(const HostModel& m, const std::vector<int32_t>& arc_begin, std::vector<int32_t>& out,
                        int32_t& slots);
 
+// Load-time bound for the bound-pruned CTC decode: per state s,
+// ub[s] = max over the levels L of its back-off chain (root included) of
+// fadd(acc_boff_L, max arc weight of level L), in float with the kernels'
+// rounding (fadd is monotone), so ub[s] >= every score of the row of s
+// (Algorithm 1 takes each token's score from one of these levels).
+void build_row_bounds(const HostModel& m, std::vector<float>& ub);
+
 // Device-side view passed to kernels by value.
 struct DevModel {
   const StateRec* srec;
@@ -87,6 +94,7 @@ struct DevModel {
   // tiny LMs: bytes of the chain table and of the packed arc quads, both
   // staged into shared memory by the advance kernel (0: not a tiny LM)
   int32_t tiny_chain_bytes, tiny_arcq_bytes;
+  const float* lm_ub;  // [S] build_row_bounds
 };
 
 // Kernel launchers (advance.cu, fused.cu, decode.cu). Return cudaError_t as int.
