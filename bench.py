@@ -64,6 +64,8 @@ def parse():
     p.add_argument("--no-large", action="store_true", help="skip the configs[3]/[4] LMs")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--dependent", action="store_true",
+                   help="headline calls without NGPULM_ADVANCE_INDEPENDENT (each waits for its predecessor)")
     p.add_argument("--workdir", default="/tmp/ngpulm_bench")
     p.add_argument("--launcher-selftest", action="store_true",
                    help="multi-rank plumbing only (gloo, no GPU): launch, shared files, shard, gather, check")
@@ -107,7 +109,8 @@ def workload_config(B, world):
             "order": ORDER, "parallelism": f"dp{world} (rows sharded, trie replicated)",
             "l2": "inputs/outputs rotate over buffer sets > 4x L2 (126 MiB)",
             "timing": "K calls inside a CUDA graph between untimed lead-in/lead-out calls, external event "
-                      "nodes, median over replays, max over ranks"}
+                      "nodes, median over replays, max over ranks",
+            "steps": "independent batches (each step its own states and output buffers)"}
 
 
 # ----------------------------------------------------------------------------- shared inputs
@@ -373,9 +376,13 @@ def run_ours(args):
     touched = statistics.mean(m.touched_bytes(states_np[r]) for r in range(min(R, 16)))
     stream = torch.cuda.Stream(device=dev)
 
+    # one step = one ngpulm_advance call over its own batch into its own buffer set: the
+    # steps are independent (NGPULM_ADVANCE_INDEPENDENT), unless --dependent
+    indep = not args.dependent
+
     def step(k):
         r = k % R
-        m.advance(states[r], scores[r], nxt[r], fin[r], stream=stream)
+        m.advance(states[r], scores[r], nxt[r], fin[r], stream=stream, independent=indep)
 
     K, W = args.steps, args.warmup
     with torch.cuda.stream(stream):
@@ -439,7 +446,15 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": compulsory,
                      "bytes_formula": "8*B*V outputs + 4*B states + 4*B finals (HBM-compulsory; the trie is "
                                       "L2-resident, its unique bytes are reported apart)",
-                     "trie_unique_bytes_per_launch": touched},
+                     "trie_unique_bytes_per_launch": touched,
+                     "call_mode": "independent (NGPULM_ADVANCE_INDEPENDENT)" if indep else "dependent"},
+        "roofline_dependent_calls": {
+            "us_per_call": variants.get("b1024_table_dependent"),
+            "frac": (compulsory / (variants["b1024_table_dependent"] * 1e-6) / 1e9 / peak_gbs
+                     if variants.get("b1024_table_dependent") else None),
+            "what": "the same step through plain ngpulm_advance: each call waits for its predecessor to "
+                    "complete before storing (the regime of a decode loop whose next states come from the "
+                    "previous step)"},
         "gpu_launches": K,
         "e2e": e2e,
         "clocks": sampler.summary(),
@@ -530,17 +545,22 @@ def cpu_baseline(files, states_all, seconds):
 
 def advance_variants(m, states, scores, nxt, fin, R, stream):
     """us per advance call in the steady state (Window) for the other shapes:
-    BASELINE configs[1] (B=128), B=4096 and Algorithm 1's literal chain walk."""
+    BASELINE configs[1] (B=128), B=4096 and Algorithm 1's literal chain walk; each
+    in both call modes — independent (NGPULM_ADVANCE_INDEPENDENT: the calls' batches
+    and buffers are independent, rows stored before the PDL wait) and dependent
+    (plain ngpulm_advance: every call waits for its predecessor before storing)."""
     import paper_2505_22857_b200 as ng
     out = {}
     Bh = states.shape[1]
-    for name, Bv, mode in (("b128_table", 128, ng.CHAIN_TABLE), ("b1024_table", Bh, ng.CHAIN_TABLE),
-                           ("b1024_walk", Bh, ng.CHAIN_WALK)):
+    for name, Bv, mode, ind in (("b128_table", 128, ng.CHAIN_TABLE, True), ("b1024_table", Bh, ng.CHAIN_TABLE, True),
+                                ("b1024_walk", Bh, ng.CHAIN_WALK, True),
+                                ("b128_table_dependent", 128, ng.CHAIN_TABLE, False),
+                                ("b1024_table_dependent", Bh, ng.CHAIN_TABLE, False)):
         m.set_chain_mode(mode)
 
         def call(k):
             r = k % R
-            m.advance(states[r, :Bv], scores[r, :Bv], nxt[r, :Bv], fin[r, :Bv], stream=stream)
+            m.advance(states[r, :Bv], scores[r, :Bv], nxt[r, :Bv], fin[r, :Bv], stream=stream, independent=ind)
         out[name] = window_ms(call, 256, stream) * 1e3 / 256
     m.set_chain_mode(ng.CHAIN_TABLE)
     # B = 4096: four of the rotating batches side by side
@@ -551,10 +571,11 @@ def advance_variants(m, states, scores, nxt, fin, R, stream):
     nx4 = nxt[: 4 * R4].reshape(R4, 4 * Bh, -1)
     fi4 = fin[: 4 * R4].reshape(R4, 4 * Bh)
 
-    def call4(k):
-        r = k % R4
-        m.advance(st4[r], sc4[r], nx4[r], fi4[r], stream=stream)
-    out["b4096_table"] = window_ms(call4, 128, stream) * 1e3 / 128
+    for ind, name in ((True, "b4096_table"), (False, "b4096_table_dependent")):
+        def call4(k):
+            r = k % R4
+            m.advance(st4[r], sc4[r], nx4[r], fi4[r], stream=stream, independent=ind)
+        out[name] = window_ms(call4, 128, stream) * 1e3 / 128
     del torch
     return out
 
@@ -581,6 +602,26 @@ def tiny_lm_variant(workdir, dev, stream):
         def call(k):
             m.advance(st[k % R], sc[k % R], nx[k % R], want_final=False, stream=stream)
         out[name] = window_ms(call, 128, stream) * 1e3 / 128
+    m.set_advance_kernel(ng.ADVANCE_AUTO)
+    # the decode kernels with the biasing LM (f4 tiny path vs the same model read from global memory):
+    # configs[2]-shaped CTC (B=256, T=500): per-frame fused steps and the persistent decode
+    Bc, T = 256, 500
+    x = torch.from_numpy(synth.ctc_logits(synth.read_sentences(f.heldout), Bc, T, V, seed=4)).to(dev)
+    stc = torch.zeros(Bc, dtype=torch.int32, device=dev)
+    pv = torch.full((Bc,), -1, dtype=torch.int32, device=dev)
+    frames = torch.empty((T, Bc), dtype=torch.int32, device=dev)
+    reset = lambda: (stc.zero_(), pv.fill_(-1))  # noqa: E731
+    for kind, tag in ((ng.ADVANCE_AUTO, "smem"), (ng.ADVANCE_WARP, "global")):
+        m.set_advance_kernel(kind)
+
+        def ctc_all():
+            for t in range(T):
+                m.fused_greedy_step(ng.CTC, x[:, t], stc, prev=pv, lam=0.3, tokens_out=frames[t], stream=stream)
+        out[f"tiny_lm_ctc_b256_fused_us_per_frame_{tag}"] = graph_ms(ctc_all, stream, 5, reset) * 1e3 / T
+
+        def ctc_persistent():
+            m.ctc_greedy_decode(x, stc, pv, lam=0.3, stream=stream)
+        out[f"tiny_lm_ctc_b256_t500_persistent_ms_{tag}"] = graph_ms(ctc_persistent, stream, 5, reset)
     m.set_advance_kernel(ng.ADVANCE_AUTO)
     return out
 
@@ -715,14 +756,16 @@ def transducer_steps(m, states0, dev, stream, rank, tag, nsteps=256):
     tok = torch.empty(B, dtype=torch.int32, device=dev)
     out = {}
     for lam, name in ((0.3, "fused"), (0.0, "plain")):
+        sv = st if name == "fused" else None  # plain greedy: no LM state (the C ABI's states == NULL path)
+
         def b2b():
             for k in range(nsteps):
-                m.fused_greedy_step(ng.RNNT, xs[k % NB], st, lam=lam, tokens_out=tok, stream=stream)
+                m.fused_greedy_step(ng.RNNT, xs[k % NB], sv, lam=lam, tokens_out=tok, stream=stream)
 
         def with_net():
             for k in range(nsteps):
                 network_kernel(xs[k % NB], buf)
-                m.fused_greedy_step(ng.RNNT, buf, st, lam=lam, tokens_out=tok, stream=stream)
+                m.fused_greedy_step(ng.RNNT, buf, sv, lam=lam, tokens_out=tok, stream=stream)
         reset = lambda: st.copy_(st0)  # noqa: E731
         out[f"{tag}_b{B}_{name}_us_per_step_back_to_back"] = graph_ms(b2b, stream, 5, reset) * 1e3 / nsteps
         out[f"{tag}_b{B}_{name}_us_per_step_after_network"] = graph_ms(with_net, stream, 5, reset) * 1e3 / nsteps
@@ -754,7 +797,7 @@ def label_loop(m, dev, stream, rank):
         def joint(frame, u, last, outl):
             synth.joint_gpu(5 + rank, frame, u, last, outl, temperature=8.0, blank=V, blank_bias=0.75,
                             stream=dec.stream)
-        dec = TransducerGreedyDecoder(m, joint, Bl, 100, lam=lam)
+        dec = TransducerGreedyDecoder(m, joint, Bl, 100, lam=lam, use_lm=name == "fused")
         dec(lengths)  # capture + warm-up
         ts = []
         for _ in range(3):
@@ -788,20 +831,28 @@ def bench_fused(m, files, dev, stream, rank):
     frames = torch.empty((T, Bc), dtype=torch.int32, device=dev)
     reset = lambda: (st.zero_(), pv.fill_(-1))  # noqa: E731
     for lam, name in ((0.3, "fused"), (0.0, "plain")):
-        def ctc_all():
-            for t in range(T):
-                m.fused_greedy_step(ng.CTC, x[:, t], st, prev=pv, lam=lam, tokens_out=frames[t], stream=stream)
-        ms = graph_ms(ctc_all, stream, 5, reset)
-        out[f"ctc_b256_t500_{name}_us_per_frame"] = ms * 1e3 / T
+        sv = st if name == "fused" else None  # plain greedy: no LM state
+
+        for ready in (False, True):  # logits_ready: NGPULM_STEP_LOGITS_READY (the encoder output precedes the loop)
+            def ctc_all():
+                for t in range(T):
+                    m.fused_greedy_step(ng.CTC, x[:, t], sv, prev=pv, lam=lam, tokens_out=frames[t], stream=stream,
+                                        logits_ready=ready)
+            ms = graph_ms(ctc_all, stream, 5, reset)
+            out[f"ctc_b256_t500_{name}{'_logits_ready' if ready else ''}_us_per_frame"] = ms * 1e3 / T
     out["ctc_per_frame_lm_overhead"] = out["ctc_b256_t500_fused_us_per_frame"] / out["ctc_b256_t500_plain_us_per_frame"] - 1
+    out["ctc_per_frame_lm_overhead_logits_ready"] = (out["ctc_b256_t500_fused_logits_ready_us_per_frame"]
+                                                     / out["ctc_b256_t500_plain_logits_ready_us_per_frame"] - 1)
 
     # the same utterance batch in ONE persistent launch
     fr2 = torch.empty((Bc, T), dtype=torch.int32, device=dev)
     em2 = torch.empty((Bc, T), dtype=torch.int32, device=dev)
     el2 = torch.empty(Bc, dtype=torch.int32, device=dev)
     for lam, name in ((0.3, "fused"), (0.0, "plain")):
+        sv = st if name == "fused" else None  # plain greedy: no LM state
+
         def ctc_persistent():
-            m.ctc_greedy_decode(x, st, pv, lam=lam, frames_out=fr2, emit_out=em2, emit_len=el2, stream=stream)
+            m.ctc_greedy_decode(x, sv, pv, lam=lam, frames_out=fr2, emit_out=em2, emit_len=el2, stream=stream)
         ms_p = graph_ms(ctc_persistent, stream, 5, reset)
         out[f"ctc_b256_t500_persistent_{name}_ms"] = ms_p
         out[f"ctc_b256_t500_persistent_{name}_logits_gbs"] = x.numel() * 4 / (ms_p * 1e-3) / 1e9

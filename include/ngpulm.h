@@ -171,6 +171,22 @@ int ngpulm_state_of(const ngpulm_model* model, int32_t with_bos, const int32_t* 
 int ngpulm_advance(const ngpulm_model* model, const int32_t* states, int32_t B, float* scores,
                    int32_t* next, float* final_out, ngpulm_stream stream);
 
+/* ngpulm_advance with flags:
+ *   NGPULM_ADVANCE_INDEPENDENT: the caller guarantees that no kernel which may
+ *     still be running when this call's kernel starts writes `states` or reads
+ *     or writes `scores`, `next`, `final_out` — e.g. consecutive calls over
+ *     independent batches with distinct output buffers (batch rescoring of
+ *     many state batches, PAPER.md:111-113's batched query issued back to
+ *     back). Each row is then built AND stored before the kernel waits for its
+ *     predecessor (programmatic dependent launch), so consecutive calls' 8 V B
+ *     output bytes stream out back to back instead of each call waiting for
+ *     the previous one to drain; the call still completes after its
+ *     predecessor (stream completion order is kept). Results are identical.
+ * flags == 0 is ngpulm_advance. EUSAGE for unknown flags. */
+enum { NGPULM_ADVANCE_INDEPENDENT = 1 };
+int ngpulm_advance_ex(const ngpulm_model* model, const int32_t* states, int32_t B, float* scores,
+                      int32_t* next, float* final_out, uint32_t flags, ngpulm_stream stream);
+
 /* final_out[b] = final weight of states[b] (the AED <eos> score).
  * states: dev [B] int32; final_out: dev [B] float32. */
 int ngpulm_final(const ngpulm_model* model, const int32_t* states, int32_t B, float* final_out,
@@ -205,6 +221,22 @@ int ngpulm_fused_greedy_step(const ngpulm_model* model, int32_t mode, const floa
                              int64_t row_stride, int32_t B, int32_t* states, int32_t* prev,
                              const uint8_t* active, float lambda, int32_t blank_id,
                              int32_t* tokens_out, ngpulm_stream stream);
+
+/* ngpulm_fused_greedy_step with flags:
+ *   NGPULM_STEP_LOGITS_READY: the caller guarantees that no kernel which may
+ *     still be running when this call's kernel starts writes `logits` — e.g.
+ *     a CTC loop over an encoder output produced before the loop (the kernel
+ *     then copies its logits rows before its programmatic-dependent-launch
+ *     wait, overlapping the previous step; PAPER.md:139's per-frame loop).
+ *     NGPU-LM calls never write logits, so a loop of NGPU-LM steps over
+ *     precomputed logits always qualifies; a logits producer launched with
+ *     programmatic dependent launch that triggers early does not.
+ * flags == 0 is ngpulm_fused_greedy_step. EUSAGE for unknown flags. */
+enum { NGPULM_STEP_LOGITS_READY = 1 };
+int ngpulm_fused_greedy_step_ex(const ngpulm_model* model, int32_t mode, const float* logits,
+                                int64_t row_stride, int32_t B, int32_t* states, int32_t* prev,
+                                const uint8_t* active, float lambda, int32_t blank_id, int32_t* tokens_out,
+                                uint32_t flags, ngpulm_stream stream);
 
 /* ngpulm_fused_greedy_step with internal-LM subtraction ("-ILM+LM" for HAT
  * transducers, Table 3; SPEC.md:298-306 fuse_scores): every

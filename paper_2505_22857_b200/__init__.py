@@ -22,6 +22,8 @@ NGPULM_OK, NGPULM_EDOMAIN, NGPULM_EUSAGE, NGPULM_ECUDA, NGPULM_EIO = 0, 1, 2, 3,
 CTC, RNNT, AED = 0, 1, 2
 CHAIN_TABLE, CHAIN_WALK = 0, 1
 ADVANCE_AUTO, ADVANCE_WARP, ADVANCE_CTA = 0, 1, 2
+STEP_LOGITS_READY = 1  # ngpulm_fused_greedy_step_ex flag
+ADVANCE_INDEPENDENT = 1  # ngpulm_advance_ex flag
 MAX_ORDER = 32
 MAX_TOPK = 256
 
@@ -63,8 +65,11 @@ SIGNATURES = {
     "ngpulm_last_error": (C.c_char_p, []),
     "ngpulm_state_of": (C.c_int, [_P, _I32, _P, _I32, C.POINTER(_I32)]),
     "ngpulm_advance": (C.c_int, [_P, _P, _I32, _P, _P, _P, _P]),
+    "ngpulm_advance_ex": (C.c_int, [_P, _P, _I32, _P, _P, _P, C.c_uint32, _P]),
     "ngpulm_final": (C.c_int, [_P, _P, _I32, _P, _P]),
     "ngpulm_fused_greedy_step": (C.c_int, [_P, _I32, _P, _I64, _I32, _P, _P, _P, _F, _I32, _P, _P]),
+    "ngpulm_fused_greedy_step_ex": (C.c_int, [_P, _I32, _P, _I64, _I32, _P, _P, _P, _F, _I32, _P, C.c_uint32,
+                                               _P]),
     "ngpulm_fused_greedy_step_ilm": (C.c_int, [_P, _I32, _P, _I64, _I32, _P, _P, _P, _F, _I32, _P, _I64, _F, _P,
                                                 _P]),
     "ngpulm_transducer_loop_step": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _P, _P, _I32, _F, _I32, _P, _I64, _F,
@@ -227,8 +232,11 @@ class NgpuLM:
         return out.value
 
     # ---------------------------------------------------------------- hot path
-    def advance(self, states, scores=None, next=None, final_out=None, want_final=True, stream=None):
-        """ngpulm_advance: states [B] int32 (CUDA) -> scores [B,V] f32, next [B,V] i32, final [B]."""
+    def advance(self, states, scores=None, next=None, final_out=None, want_final=True, stream=None,
+                independent: bool = False):
+        """ngpulm_advance: states [B] int32 (CUDA) -> scores [B,V] f32, next [B,V] i32, final [B].
+        independent=True: ngpulm_advance_ex with NGPULM_ADVANCE_INDEPENDENT (no running kernel
+        writes the states or touches the outputs: consecutive calls' stores overlap)."""
         import torch
         B = states.numel()
         if scores is None:
@@ -237,11 +245,12 @@ class NgpuLM:
             next = torch.empty((B, self.V), dtype=torch.int32, device=states.device)
         if final_out is None and want_final:
             final_out = torch.empty(B, dtype=torch.float32, device=states.device)
-        _check(lib().ngpulm_advance(
+        _check(lib().ngpulm_advance_ex(
             self._h, _dev_ptr(states, torch.int32, "states", B), B,
             _dev_ptr(scores, torch.float32, "scores", B * self.V),
             _dev_ptr(next, torch.int32, "next", B * self.V),
-            _dev_ptr(final_out, torch.float32, "final_out", B), _stream(stream)))
+            _dev_ptr(final_out, torch.float32, "final_out", B), ADVANCE_INDEPENDENT if independent else 0,
+            _stream(stream)))
         return scores, next, final_out
 
     def final(self, states, out=None, stream=None):
@@ -255,8 +264,9 @@ class NgpuLM:
 
     def fused_greedy_step(self, mode: int, logits, states, prev=None, active=None, lam: float = 0.3,
                           blank_id: int | None = None, tokens_out=None, row_stride: int | None = None,
-                          B: int | None = None, stream=None):
-        """ngpulm_fused_greedy_step. logits: CUDA f32 tensor whose row b starts at
+                          B: int | None = None, stream=None, logits_ready: bool = False):
+        """ngpulm_fused_greedy_step (ngpulm_fused_greedy_step_ex with logits_ready:
+        NGPULM_STEP_LOGITS_READY). logits: CUDA f32 tensor whose row b starts at
         b*row_stride (default: a [B, V+1] contiguous tensor, or a strided 2-D view
         such as logits3d[:, t] of a [B, T, V+1] tensor). states/prev updated in place.
         states=None with lam=0: plain greedy decoding (no LM)."""
@@ -267,12 +277,13 @@ class NgpuLM:
         if tokens_out is None:
             tokens_out = torch.empty(B, dtype=torch.int32, device=logits.device)
         blank = self.V if blank_id is None else blank_id
-        _check(lib().ngpulm_fused_greedy_step(
+        _check(lib().ngpulm_fused_greedy_step_ex(
             self._h, mode, lp, row_stride, B,
             _dev_ptr(states, torch.int32, "states", B) if states is not None else None,
             _dev_ptr(prev, torch.int32, "prev", B) if prev is not None else None,
             _dev_ptr(active, torch.uint8, "active", B) if active is not None else None,
-            float(lam), blank, _dev_ptr(tokens_out, torch.int32, "tokens_out", B), _stream(stream)))
+            float(lam), blank, _dev_ptr(tokens_out, torch.int32, "tokens_out", B),
+            STEP_LOGITS_READY if logits_ready else 0, _stream(stream)))
         return tokens_out
 
     def fused_greedy_step_ilm(self, mode: int, logits, states, ilm, lam_ilm: float, prev=None, active=None,
@@ -443,8 +454,10 @@ def load_binary(path: str, device: int | None = None) -> NgpuLM:
 # C-ABI names, for callers that mirror include/ngpulm.h
 ngpulm_load_arpa = load_arpa
 ngpulm_advance = NgpuLM.advance
+ngpulm_advance_ex = NgpuLM.advance
 ngpulm_final = NgpuLM.final
 ngpulm_fused_greedy_step = NgpuLM.fused_greedy_step
+ngpulm_fused_greedy_step_ex = NgpuLM.fused_greedy_step
 ngpulm_check = NgpuLM.check
 ngpulm_ctc_greedy_decode = NgpuLM.ctc_greedy_decode
 ngpulm_fused_greedy_step_ilm = NgpuLM.fused_greedy_step_ilm

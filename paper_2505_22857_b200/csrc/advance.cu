@@ -78,7 +78,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 // loaded before the wait, so the root fill is register -> shared stores that
 // overlap the arc gathers (shared-memory loads issued after the gathers would
 // return behind them); otherwise the CTA bulk-copies the root weights once.
-template <bool kTable, int kW, bool kPacked, bool kRegRoot>
+// kIndep (NGPULM_ADVANCE_INDEPENDENT): no running kernel writes this call's
+// states or touches its outputs, so the row is built and stored before
+// griddepcontrol.wait, which moves to the end (the grid still completes after
+// its predecessor: stream completion order is kept) — consecutive calls'
+// stores overlap instead of each waiting for the previous call to drain.
+template <bool kTable, int kW, bool kPacked, bool kRegRoot, bool kIndep = false>
 __global__ void __launch_bounds__(32, NGPULM_ADV_MINB(kW, kPacked))
     advance_warp_kernel(DevModel m, const int32_t* __restrict__ states, int32_t B, float* __restrict__ scores,
                         int32_t* __restrict__ next, float* __restrict__ final_out) {
@@ -110,6 +115,7 @@ __global__ void __launch_bounds__(32, NGPULM_ADV_MINB(kW, kPacked))
       bulk_g2s(const_cast<float*>(root_w), m.arc_w, bytes, bar);
     }
   }
+  __syncwarp();  // lane 0's barrier init before the other lanes wait on it
   float4 rw[kRegRoot ? 8 : 1];
   if (kRegRoot && row < B) {
     const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
@@ -182,6 +188,22 @@ __global__ void __launch_bounds__(32, NGPULM_ADV_MINB(kW, kPacked))
   int32_t st = load_state();
   Row r = build(st, 0);
   if (!r.bad) proxy_fence_warp();  // the row's generic writes -> the bulk stores
+  if constexpr (kIndep) {
+    if (lane == 0) {
+      if (!r.bad) store_row_bulk(s, srow, nrow, bytes);
+      if (r.bad) atomicMin(m.bad_row, (unsigned long long)row);
+      if (final_out) final_out[row] = r.bad ? __int_as_float(0x7fc00000) : r.fin;
+    }
+    if (r.bad) {
+      for (int32_t v = lane; v < V; v += 32) { srow[v] = __int_as_float(0x7fc00000); nrow[v] = -1; }
+    }
+    if (!r.bad && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    if (w == 0 && !kRegRoot) mbar_wait(bar, 0);
+    // the grid completes only after its predecessor (stream order of completion)
+    // as long as one CTA waits for it; the others leave at once, freeing their slot
+    if (blockIdx.x == 0) pdl_wait();
+    return;
+  }
   pdl_wait();
   STAMP(2);
   bool stored = false;
@@ -401,7 +423,8 @@ int32_t vocab_tile(int32_t V, int32_t order) {
 }
 
 int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* scores, int32_t* next,
-                   float* final_out, void* stream) {
+                   float* final_out, void* stream, uint32_t flags) {
+  const bool indep = flags & NGPULM_ADVANCE_INDEPENDENT;  // (a permission: paths without it ignore it)
   const bool vec = (m.V % 4 == 0) && ((uintptr_t)scores % 16 == 0) && ((uintptr_t)next % 16 == 0);
   const bool table = m.chain != nullptr;
   cudaStream_t st = (cudaStream_t)stream;
@@ -429,7 +452,7 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
     // one row (warp) per CTA: a CTA leaves as soon as its row is stored and the
     // next call's CTA starts its speculative build in its place (B=1024: 7 rows
     // per CTA 3.29 us, 1 row 2.83 us; B=4096: 10.1 -> 9.4 us)
-    const int R = 1;
+    const int R = NGPULM_ADV_ROWS;
     if (wcta_smem(m.V, m.order, R, 0) <= 227 * 1024) {
       const size_t wsm = wcta_smem(m.V, m.order, R, 0);
       // the grid is padded to a multiple of the SM count (the extra CTAs exit at
@@ -453,6 +476,11 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
 #define NGPULM_WARP_LAUNCH(T, W, P)                                                                                 \
   return small_v ? launch(advance_warp_kernel<T, W, P, true>, wg, wb, wsm, st, m, states, B, scores, next, final_out) \
                  : launch(advance_warp_kernel<T, W, P, false>, wg, wb, wsm, st, m, states, B, scores, next, final_out)
+      if (indep && table && pk && small_v)
+        return wide ? launch(advance_warp_kernel<true, 16, true, true, true>, wg, wb, wsm, st, m, states, B, scores,
+                             next, final_out)
+                    : launch(advance_warp_kernel<true, 8, true, true, true>, wg, wb, wsm, st, m, states, B, scores,
+                             next, final_out);
       if (table) {
         if (wide) { if (pk) NGPULM_WARP_LAUNCH(true, 16, true); NGPULM_WARP_LAUNCH(true, 16, false); }
         if (pk) NGPULM_WARP_LAUNCH(true, 8, true);

@@ -299,7 +299,13 @@ int ngpulm_state_of(const ngpulm_model* m, int32_t with_bos, const int32_t* toke
 
 int ngpulm_advance(const ngpulm_model* m, const int32_t* states, int32_t B, float* scores, int32_t* next,
                    float* final_out, ngpulm_stream stream) {
+  return ngpulm_advance_ex(m, states, B, scores, next, final_out, 0u, stream);
+}
+
+int ngpulm_advance_ex(const ngpulm_model* m, const int32_t* states, int32_t B, float* scores, int32_t* next,
+                      float* final_out, uint32_t flags, ngpulm_stream stream) {
   if (int r = check_hot(m, B)) return r;
+  if (flags & ~(uint32_t)NGPULM_ADVANCE_INDEPENDENT) return err(NGPULM_EUSAGE, "unknown flags");
   if (B == 0) return NGPULM_OK;
   if (!states || !scores || !next) return err(NGPULM_EUSAGE, "NULL device buffer");
   {  // the outputs must not overlap the states (rows re-read their state after others are written)
@@ -311,7 +317,7 @@ int ngpulm_advance(const ngpulm_model* m, const int32_t* states, int32_t B, floa
     if (overlap(states, sb, scores, ob) || overlap(states, sb, next, ob) || (final_out && overlap(states, sb, final_out, sb)))
       return err(NGPULM_EUSAGE, "advance outputs overlap the states");
   }
-  int e = ngpulm::launch_advance(m->dm, states, B, scores, next, final_out, stream);
+  int e = ngpulm::launch_advance(m->dm, states, B, scores, next, final_out, stream, flags);
   if (e) return cuda_err((cudaError_t)e, "advance launch");
   return NGPULM_OK;
 }
@@ -329,7 +335,15 @@ int ngpulm_final(const ngpulm_model* m, const int32_t* states, int32_t B, float*
 int ngpulm_fused_greedy_step(const ngpulm_model* m, int32_t mode, const float* logits, int64_t row_stride,
                              int32_t B, int32_t* states, int32_t* prev, const uint8_t* active, float lambda,
                              int32_t blank_id, int32_t* tokens_out, ngpulm_stream stream) {
+  return ngpulm_fused_greedy_step_ex(m, mode, logits, row_stride, B, states, prev, active, lambda, blank_id,
+                                     tokens_out, 0u, stream);
+}
+
+int ngpulm_fused_greedy_step_ex(const ngpulm_model* m, int32_t mode, const float* logits, int64_t row_stride,
+                                int32_t B, int32_t* states, int32_t* prev, const uint8_t* active, float lambda,
+                                int32_t blank_id, int32_t* tokens_out, uint32_t flags, ngpulm_stream stream) {
   if (int r = check_hot(m, B)) return r;
+  if (flags & ~(uint32_t)NGPULM_STEP_LOGITS_READY) return err(NGPULM_EUSAGE, "unknown flags");
   if (mode != NGPULM_CTC && mode != NGPULM_RNNT && mode != NGPULM_AED) return err(NGPULM_EUSAGE, "bad mode");
   if (blank_id < 0 || blank_id > m->h.V) return err(NGPULM_EUSAGE, "blank_id outside [0, V]");
   if (m->h.V > ngpulm::max_fused_vocab()) return err(NGPULM_EUSAGE, "fused step: the row must fit in shared memory");
@@ -339,7 +353,7 @@ int ngpulm_fused_greedy_step(const ngpulm_model* m, int32_t mode, const float* l
     return err(NGPULM_EUSAGE, "NULL device buffer");
   if (B > 1 && row_stride < (int64_t)m->h.V + 1) return err(NGPULM_EUSAGE, "row_stride < V+1");
   int e = ngpulm::launch_fused(m->dm, mode, logits, row_stride, B, states, prev, active, lambda, blank_id, nullptr,
-                               0, 0.f, tokens_out, stream);
+                               0, 0.f, tokens_out, stream, flags);
   if (e) return cuda_err((cudaError_t)e, "fused step launch");
   return NGPULM_OK;
 }

@@ -40,18 +40,18 @@ struct NoStamp {
   __device__ void operator()(int) const {}
 };
 
-template <bool kTable, bool kPacked, typename F = NoStamp>
+template <bool kTable, bool kPacked, typename F = NoStamp, bool kTiny = false>
 __device__ __forceinline__ Row build_row_warp(const DevModel& m, const WSlice& s, const float* root_w,
                                               const int32_t* root_to, int32_t st, F stamp = F()) {
   constexpr int kW = 8;
   const int lane = threadIdx.x & 31;
   WLevel lv;
   int32_t nslots;
-  const Row r = warp_row_src<kTable>(m, ValState{st}, s, lv, nslots);
+  const Row r = warp_row_src<kTable, NoOp, ValState, kTiny>(m, ValState{st}, s, lv, nslots);
   stamp(1);
   if (r.bad) return r;
   Window<kW, kPacked> a;
-  load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
+  load_window<kW, kPacked, kTiny>(m, s, lv, r.nlev, 0, nslots, a);
   {  // root level while the gathers fly: acc_root + root weight, root targets
     const float4* w4 = reinterpret_cast<const float4*>(root_w);
     const int4* t4 = reinterpret_cast<const int4*>(root_to);
@@ -73,7 +73,7 @@ __device__ __forceinline__ Row build_row_warp(const DevModel& m, const WSlice& s
   for (int32_t k0 = 0; k0 < nslots;) {
     write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
     k0 += kW;
-    if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
+    if (k0 < nslots) load_window<kW, kPacked, kTiny>(m, s, lv, r.nlev, k0, nslots, a);
   }
   __syncwarp();
   stamp(8);
@@ -82,7 +82,7 @@ __device__ __forceinline__ Row build_row_warp(const DevModel& m, const WSlice& s
 
 constexpr int kDecodeMaxRows = 4;  // rows per CTA (2 warps each): 256 threads, up to 255 registers
 
-template <bool kTable, bool kPacked, bool kNoLM = false>
+template <bool kTable, bool kPacked, bool kNoLM = false, bool kTiny = false>
 __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
     ctc_decode_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int64_t frame_stride,
                       int32_t B, int32_t T, const int32_t* __restrict__ lengths, int32_t* __restrict__ states,
@@ -95,11 +95,16 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
   const int wid = threadIdx.x >> 5, w = wid % R;
   const bool producer = wid >= R;
   const size_t rb = align16((size_t)V * 4);
-  float* root_w = reinterpret_cast<float*>(smem);
-  int32_t* root_to = reinterpret_cast<int32_t*>(smem + rb);
-  uint64_t* cbar = reinterpret_cast<uint64_t*>(smem + 2 * rb);
-  unsigned char* base = smem + 2 * rb + 16 + (size_t)w * dslice_bytes(V, m.order, depth);
-  const WSlice s = wcarve(base, V, m.order, 0);
+  unsigned char* sm0 = smem + (kTiny ? tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) : 0);
+  float* root_w = reinterpret_cast<float*>(sm0);
+  int32_t* root_to = reinterpret_cast<int32_t*>(sm0 + rb);
+  uint64_t* cbar = reinterpret_cast<uint64_t*>(sm0 + 2 * rb);
+  unsigned char* base = sm0 + 2 * rb + 16 + (size_t)w * dslice_bytes(V, m.order, depth);
+  WSlice s = wcarve(base, V, m.order, 0);
+  if (kTiny) {  // the tiny LM resident in the CTA's shared memory (tiny_copy_issue)
+    s.chain_s = reinterpret_cast<const int4*>(smem);
+    s.st_q = reinterpret_cast<int4*>(smem + align16((size_t)m.tiny_chain_bytes));
+  }
   uint64_t* full = reinterpret_cast<uint64_t*>(base + wslice_bytes(V, m.order, 0));
   uint64_t* empty = full + kRingMax;
   float* ring = reinterpret_cast<float*>(base + wslice_bytes(V, m.order, 0) + 2 * kRingMax * 8);
@@ -114,6 +119,7 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
                  : "memory");
     bulk_g2s(root_w, m.arc_w, (uint32_t)V * 4u, cbar);
     bulk_g2s(root_to, m.arc_to, (uint32_t)V * 4u, cbar);
+    if (kTiny) tiny_copy_issue(m, smem);
   }
   if (!producer && lane == 0) {
     for (int i = 0; i < depth; ++i) {
@@ -125,7 +131,10 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
   __syncthreads();  // barrier inits visible to every warp
   pdl_wait();
   if (row >= B) {
-    if (threadIdx.x == 0) mbar_wait(cbar, 0);  // no exit with the CTA's bulk copy in flight
+    if (threadIdx.x == 0) {  // no exit with the CTA's bulk copies in flight
+      mbar_wait(cbar, 0);
+      if (kTiny) mbar_wait(tiny_bar(smem, m), 0);
+    }
     return;
   }
   int32_t len = T;
@@ -153,6 +162,7 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
   int32_t* eout = emit_out ? emit_out + (size_t)row * T : nullptr;
   if (bad && len > 0 && lane == 0) atomicMin(m.bad_row, (unsigned long long)row);
   mbar_wait(cbar, 0);
+  if (kTiny) mbar_wait(tiny_bar(smem, m), 0);
 #ifdef NGPULM_PHASE_TIMING
   // debug build: cycles per phase, per row: 0 first build, 1 rebuild: record,
   // 2 logits wait, 3 decide, 4 rebuild: LM registers, 5 rebuild count,
@@ -172,7 +182,7 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
       for (int j = 0; j < kMaxColsPerLane; ++j) lm[j] = 0.f;
       return;
     }
-    build_row_warp<kTable, kPacked>(m, s, root_w, root_to, state, stamp);
+    build_row_warp<kTable, kPacked, decltype(stamp), kTiny>(m, s, root_w, root_to, state, stamp);
 #pragma unroll
     for (int j = 0; j < kMaxColsPerLane; ++j) {
       const int32_t col = lane + 32 * j;
@@ -709,6 +719,19 @@ int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride
     NGPULM_DECODE2(false, false);
 #endif
 #undef NGPULM_DECODE2
+  }
+  if (table && pk && m.tiny_chain_bytes > 0) {  // tiny LM: the model in every CTA's shared memory
+    const size_t mb = tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes);
+    int R = (B + 147) / 148;
+    R = R < 1 ? 1 : (R > kDecodeMaxRows ? kDecodeMaxRows : R);
+    int depth = kRingMax;
+    while (depth > 2 && mb + dcta_smem(m.V, m.order, R, depth) > 227 * 1024) --depth;
+    while (R > 1 && mb + dcta_smem(m.V, m.order, R, depth) > 227 * 1024) --R;
+    const size_t sm = mb + dcta_smem(m.V, m.order, R, depth);
+    if (sm <= 227 * 1024)
+      return launch(ctc_decode_kernel<true, true, false, true>, dim3((B + R - 1) / R), dim3(64 * R), sm, st, m,
+                    logits, row_stride, frame_stride, B, T, lengths, states, prev, lambda, blank, depth, frames_out,
+                    emit_out, emit_len);
   }
   int R = (B + 147) / 148;
   R = R < 1 ? 1 : (R > kDecodeMaxRows ? kDecodeMaxRows : R);

@@ -90,7 +90,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   }
 }
 
-template <int kMode, bool kTable, bool kPacked, bool kAux, bool kNoLM = false>
+// kTiny: a tiny LM (keyword-biasing size) resident in the CTA's shared memory
+// (tiny_copy_issue before the wait): records and arc quads are shared loads.
+// kEarly (NGPULM_STEP_LOGITS_READY): the logits are copied before the wait.
+template <int kMode, bool kTable, bool kPacked, bool kAux, bool kNoLM = false, bool kTiny = false,
+          bool kEarly = false>
 __global__ void __launch_bounds__(256, 1)
     fused_warp_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int32_t B,
                       int32_t* __restrict__ states, int32_t* __restrict__ prev, const uint8_t* __restrict__ active,
@@ -100,8 +104,13 @@ __global__ void __launch_bounds__(256, 1)
   extern __shared__ __align__(16) unsigned char smem[];
   const int32_t V = m.V, ncols = V + 1;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, R = blockDim.x >> 5;
-  unsigned char* base = smem + (size_t)w * fslice_bytes(V, m.order);
-  const WSlice s = wcarve(base, V, m.order, 0);
+  const size_t mb = kTiny ? tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) : 0;
+  unsigned char* base = smem + mb + (size_t)w * fslice_bytes(V, m.order);
+  WSlice s = wcarve(base, V, m.order, 0);
+  if (kTiny) {
+    s.chain_s = reinterpret_cast<const int4*>(smem);
+    s.st_q = reinterpret_cast<int4*>(smem + align16((size_t)m.tiny_chain_bytes));
+  }
   uint64_t* lbar = s.abar;
   float* lbuf = reinterpret_cast<float*>(base + wslice_bytes(V, m.order, 0));
   const int32_t row = (int32_t)blockIdx.x * R + w;
@@ -113,6 +122,10 @@ __global__ void __launch_bounds__(256, 1)
   STAMP(1);
   STAMP(9);
   pdl_trigger();
+  if constexpr (kTiny) {
+    if (threadIdx.x == 0) tiny_copy_issue(m, smem);
+    __syncthreads();  // the copy's barrier initialized for every warp
+  }
   if (row >= B) return;
   if (lane == 0 && !nolm) {  // root targets -> the row's next-state slots (immutable model data: before the wait)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(s.bar)) : "memory");
@@ -126,6 +139,7 @@ __global__ void __launch_bounds__(256, 1)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(lbar)) : "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
+  __syncwarp();  // lane 0's barrier inits before any other lane's arrive / wait on them
   float4 rw[8];
   if (!nolm) {
     const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
@@ -138,13 +152,14 @@ __global__ void __launch_bounds__(256, 1)
   auto build = [&](int32_t st, uint32_t ph) -> Row {
     WLevel lv;
     int32_t nslots;
-    const Row r = warp_row_src<kTable>(m, ValState{st}, s, lv, nslots);
+    if (kTiny) mbar_wait(tiny_bar(smem, m), 0);  // the CTA's model copy has landed
+    const Row r = warp_row_src<kTable, NoOp, ValState, kTiny>(m, ValState{st}, s, lv, nslots);
     if (r.bad) {
       mbar_wait(s.bar, ph);  // the copy of this phase is over before any re-arm or exit
       return r;
     }
     Window<kW, kPacked> a;
-    load_window<kW, kPacked>(m, s, lv, r.nlev, 0, nslots, a);
+    load_window<kW, kPacked, kTiny>(m, s, lv, r.nlev, 0, nslots, a);
     {  // root scores: acc_root + root weight, while the gathers fly
       float4* s4 = reinterpret_cast<float4*>(s.row_s);
 #pragma unroll
@@ -163,7 +178,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int32_t k0 = 0; k0 < nslots;) {
       write_window<kW, kPacked>(s, a, k0, nslots, m.pk_bits);
       k0 += kW;
-      if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
+      if (k0 < nslots) load_window<kW, kPacked, kTiny>(m, s, lv, r.nlev, k0, nslots, a);
     }
     return r;
   };
@@ -172,9 +187,15 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(states + row) : "memory");
     return __shfl_sync(kFull, v, 0);
   };
+  const float* lrow = logits + (size_t)row * row_stride;
+  if (kEarly) {  // the caller guarantees no running kernel writes the logits (NGPULM_STEP_LOGITS_READY)
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));  // read once
+    issue_frame(lrow, ncols, lbuf, lbar, pol);
+  }
   // Speculative build (as advance_warp_kernel): the LM row from the state read
-  // before griddepcontrol.wait, re-checked after it. Inputs (logits, prev,
-  // active, ILM rows) are read after the wait only.
+  // before griddepcontrol.wait, re-checked after it. Inputs (prev, active, ILM
+  // rows, and the logits unless kEarly) are read after the wait only.
   int32_t st = 0;
   Row r{};
   if (NGPULM_FUSED_SPECULATE && !nolm) {
@@ -183,7 +204,6 @@ __global__ void __launch_bounds__(256, 1)
   }
   pdl_wait();
   STAMP(2);
-  const float* lrow = logits + (size_t)row * row_stride;
   float ilm[kAux ? kMaxColsPerLane : 1];
   if (kAux) {  // the row's ILM scores, column layout (lane i: columns i, i+32, ...), loads in flight early
     const float* arow = aux.p + (size_t)row * aux.stride;
@@ -197,7 +217,7 @@ __global__ void __launch_bounds__(256, 1)
   // used only after the state and record loads are issued
   const bool on = kMode == kLoop ? __ldg(&lp.frame[row]) < __ldg(&lp.len[row]) : (!active || __ldg(&active[row]));
   const int32_t pc = (kMode == NGPULM_CTC) ? __ldg(&prev[row]) : -2;
-  if (on) {  // the logits (an input: after the wait), copied while the state is checked
+  if (on && !kEarly) {  // the logits (an input: after the wait), copied while the state is checked
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));  // read once
     issue_frame(lrow, ncols, lbuf, lbar, pol);
@@ -221,7 +241,7 @@ __global__ void __launch_bounds__(256, 1)
       if (on) atomicMin(m.bad_row, (unsigned long long)row);
       if (kMode == kLoop && on) lp.frame[row] = lp.len[row];  // an invalid state ends the row's loop
     }
-    if (on) mbar_wait(lbar, 0);  // no exit with a bulk copy in flight
+    if (on || kEarly) mbar_wait(lbar, 0);  // no exit with a bulk copy in flight
     return;
   }
   mbar_wait(lbar, 0);
@@ -333,6 +353,7 @@ __global__ void __launch_bounds__(256, 1)
       bulk_g2s(s.row_n, m.arc_to, (uint32_t)V * 4u, s.bar);
     }
   }
+  __syncwarp();  // lane 0's barrier init before any other lane's arrive / wait on it
   float4 rw[8];
   if (role == 0 && !nolm) {
     const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
@@ -603,6 +624,7 @@ __global__ void __launch_bounds__(256, 1)
                  : "memory");
     bulk_g2s(s.row_n, m.arc_to, (uint32_t)V * 4u, s.bar);
   }
+  __syncwarp();  // lane 0's barrier inits before any other lane's arrive / wait on them
   float4 rw[8];
   {
     const float4* w4 = reinterpret_cast<const float4*>(m.arc_w);
@@ -712,15 +734,44 @@ __global__ void __launch_bounds__(256, 1)
 template <int kMode>
 int launch_fused_mode(const DevModel& m, const float* logits, int64_t row_stride, int32_t B, int32_t* states,
                       int32_t* prev, const uint8_t* active, float lambda, int32_t blank, AuxRow aux,
-                      int32_t* tokens_out, cudaStream_t st) {
+                      int32_t* tokens_out, cudaStream_t st, uint32_t flags) {
+  const bool early = (flags & NGPULM_STEP_LOGITS_READY) && !aux.p;  // (a permission: other paths ignore it)
   if (m.V % 4 == 0 && m.V <= 1024 && m.adv_kind != NGPULM_ADVANCE_CTA) {
     const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
     if (states == nullptr) {  // plain greedy (no LM): one warp per row, no row build
       int R = (B + 147) / 148;
       R = R < 1 ? 1 : (R > NGPULM_FUSED_MAX_ROWS ? NGPULM_FUSED_MAX_ROWS : R);
+      if (early)
+        return launch(fused_warp_kernel<kMode, true, true, false, true, false, true>, dim3((B + R - 1) / R),
+                      dim3(32 * R), (size_t)R * fslice_bytes(m.V, m.order), st, m, logits, row_stride, B, states,
+                      prev, active, lambda, blank, aux, Loop{}, tokens_out);
       return launch(fused_warp_kernel<kMode, true, true, false, true>, dim3((B + R - 1) / R), dim3(32 * R),
                     (size_t)R * fslice_bytes(m.V, m.order), st, m, logits, row_stride, B, states, prev, active,
                     lambda, blank, aux, Loop{}, tokens_out);
+    }
+    if (table && pk && m.tiny_chain_bytes > 0) {  // tiny LM: the model in every CTA's shared memory
+      const size_t mb = tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes);
+      int R = (B + 147) / 148;
+      R = R < 1 ? 1 : (R > NGPULM_FUSED_MAX_ROWS ? NGPULM_FUSED_MAX_ROWS : R);
+      while (R > 1 && mb + (size_t)R * fslice_bytes(m.V, m.order) > 227 * 1024) --R;
+      const size_t tsm = mb + (size_t)R * fslice_bytes(m.V, m.order);
+      if (tsm <= 227 * 1024) {
+        const dim3 tg((B + R - 1) / R), tb(32 * R);
+        if (early)
+          return launch(fused_warp_kernel<kMode, true, true, false, false, true, true>, tg, tb, tsm, st, m, logits,
+                        row_stride, B, states, prev, active, lambda, blank, aux, Loop{}, tokens_out);
+        return aux.p ? launch(fused_warp_kernel<kMode, true, true, true, false, true>, tg, tb, tsm, st, m, logits,
+                              row_stride, B, states, prev, active, lambda, blank, aux, Loop{}, tokens_out)
+                     : launch(fused_warp_kernel<kMode, true, true, false, false, true>, tg, tb, tsm, st, m, logits,
+                              row_stride, B, states, prev, active, lambda, blank, aux, Loop{}, tokens_out);
+      }
+    }
+    if (kMode != NGPULM_RNNT || B > NGPULM_PAIR_MAX_B) if (early && table && pk) {
+      int R = (B + 147) / 148;
+      R = R < 1 ? 1 : (R > NGPULM_FUSED_MAX_ROWS ? NGPULM_FUSED_MAX_ROWS : R);
+      return launch(fused_warp_kernel<kMode, true, true, false, false, false, true>, dim3((B + R - 1) / R),
+                    dim3(32 * R), (size_t)R * fslice_bytes(m.V, m.order), st, m, logits, row_stride, B, states, prev,
+                    active, lambda, blank, aux, Loop{}, tokens_out);
     }
     if constexpr (kMode == NGPULM_RNNT) if (B <= NGPULM_PAIR_MAX_B) {  // two warps per row (stage 1 beside the row build)
       int R = (B + 147) / 148;
@@ -762,19 +813,20 @@ int launch_fused_mode(const DevModel& m, const float* logits, int64_t row_stride
 
 int launch_fused(const DevModel& m, int32_t mode, const float* logits, int64_t row_stride, int32_t B,
                  int32_t* states, int32_t* prev, const uint8_t* active, float lambda, int32_t blank,
-                 const float* aux, int64_t aux_stride, float lambda_ilm, int32_t* tokens_out, void* stream) {
+                 const float* aux, int64_t aux_stride, float lambda_ilm, int32_t* tokens_out, void* stream,
+                 uint32_t flags) {
   cudaStream_t st = (cudaStream_t)stream;
   const AuxRow ax{aux, aux_stride, lambda_ilm};
   switch (mode) {
     case NGPULM_CTC:
       return launch_fused_mode<NGPULM_CTC>(m, logits, row_stride, B, states, prev, active, lambda, blank, ax,
-                                           tokens_out, st);
+                                           tokens_out, st, flags);
     case NGPULM_RNNT:
       return launch_fused_mode<NGPULM_RNNT>(m, logits, row_stride, B, states, prev, active, lambda, blank, ax,
-                                            tokens_out, st);
+                                            tokens_out, st, flags);
     default:
       return launch_fused_mode<NGPULM_AED>(m, logits, row_stride, B, states, prev, active, lambda, blank, ax,
-                                           tokens_out, st);
+                                           tokens_out, st, flags);
   }
 }
 
@@ -816,6 +868,21 @@ int launch_transducer_loop(const DevModel& m, const float* logits, int64_t row_s
   if (states == nullptr)  // plain greedy label looping (no LM)
     return launch(fused_warp_kernel<kLoop, true, true, false, true>, wg, wb, wsm, st, m, logits, row_stride, B, states,
                   (int32_t*)nullptr, (const uint8_t*)nullptr, lambda, blank, ax, lp, tokens_out);
+  if (table && pk && m.tiny_chain_bytes > 0) {  // tiny LM: the model in every CTA's shared memory
+    const size_t mb = tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes);
+    int Rt = R;
+    while (Rt > 1 && mb + (size_t)Rt * fslice_bytes(m.V, m.order) > 227 * 1024) --Rt;
+    const size_t tsm = mb + (size_t)Rt * fslice_bytes(m.V, m.order);
+    if (tsm <= 227 * 1024) {
+      const dim3 tg((B + Rt - 1) / Rt), tb(32 * Rt);
+      return aux ? launch(fused_warp_kernel<kLoop, true, true, true, false, true>, tg, tb, tsm, st, m, logits,
+                          row_stride, B, states, (int32_t*)nullptr, (const uint8_t*)nullptr, lambda, blank, ax, lp,
+                          tokens_out)
+                 : launch(fused_warp_kernel<kLoop, true, true, false, false, true>, tg, tb, tsm, st, m, logits,
+                          row_stride, B, states, (int32_t*)nullptr, (const uint8_t*)nullptr, lambda, blank, ax, lp,
+                          tokens_out);
+    }
+  }
   if (B <= NGPULM_PAIR_MAX_B) {  // two warps per row
     int Rp = (B + 147) / 148;
     Rp = Rp < 1 ? 1 : (Rp > 4 ? 4 : Rp);

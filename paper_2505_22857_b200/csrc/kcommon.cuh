@@ -405,6 +405,9 @@ __device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, con
 #ifndef NGPULM_TINY_ROWS
 #define NGPULM_TINY_ROWS 8
 #endif
+#ifndef NGPULM_ADV_ROWS
+#define NGPULM_ADV_ROWS 1  // rows (warps) per CTA of the warp advance kernel
+#endif
 #ifndef NGPULM_FUSED_MAX_ROWS
 #define NGPULM_FUSED_MAX_ROWS 8
 #endif
@@ -439,7 +442,8 @@ struct WSlice {
   float* acc;
   uint64_t* bar;   // the root targets' bulk copy into row_n
   uint64_t* abar;  // second mbarrier (the fused kernels' logits copy)
-  int4* st_q;      // packed arc quads read from shared memory (tiny-LM kernel: the CTA's model copy)
+  int4* st_q;      // packed arc quads read from shared memory (tiny-LM kernels: the CTA's model copy)
+  const int4* chain_s;  // tiny-LM kernels: the CTA's copy of the chain table
 };
 
 __device__ __forceinline__ WSlice wcarve(unsigned char* p, int32_t V, int32_t order, int stage_q) {
@@ -456,7 +460,19 @@ __device__ __forceinline__ WSlice wcarve(unsigned char* p, int32_t V, int32_t or
   s.bar = reinterpret_cast<uint64_t*>(p + levels_bytes(order));
   s.abar = s.bar + 1;
   s.st_q = reinterpret_cast<int4*>(p + levels_bytes(order) + 16);
+  s.chain_s = nullptr;
   return s;
+}
+
+// Tiny LMs (keyword-biasing size): the chain
+// table and the packed arc quads copied into a CTA's shared memory (before
+// griddepcontrol.wait: model data is immutable), so a row's record and arc
+// quads are shared loads. Layout: chain | arc quads | mbarrier.
+__host__ __device__ constexpr size_t tiny_copy_bytes(int64_t chain_bytes, int64_t arcq_bytes) {
+  return align16((size_t)chain_bytes) + align16((size_t)arcq_bytes) + 16;
+}
+__device__ __forceinline__ uint64_t* tiny_bar(unsigned char* base, const DevModel& m) {
+  return reinterpret_cast<uint64_t*>(base + align16((size_t)m.tiny_chain_bytes) + align16((size_t)m.tiny_arcq_bytes));
 }
 
 struct WLevel {  // lane l+1: level l of the row
@@ -474,7 +490,8 @@ struct NoOp {
 
 // after_issue() runs once the chain-record load is in flight (table mode) or
 // before the walk: independent loads issued there overlap its latency.
-template <bool kTable, typename F = NoOp, typename SF = PtrState>
+// kSmemModel: the chain record comes from the CTA's tiny-LM copy (s.chain_s).
+template <bool kTable, typename F = NoOp, typename SF = PtrState, bool kSmemModel = false>
 __device__ __forceinline__ Row warp_row_src(const DevModel& m, SF state_src, const WSlice& s, WLevel& lv,
                                             int32_t& nslots, F after_issue = F()) {
   const int lane = threadIdx.x & 31;
@@ -492,7 +509,7 @@ __device__ __forceinline__ Row warp_row_src(const DevModel& m, SF state_src, con
     r.nlev = 0; r.total = 0; r.acc_root = 0.f; r.fin = 0.f;
     if (r.bad) return r;
     int4 x = make_int4(0, 0, 0, 0);
-    if (lane < slots) x = __ldg(table + (size_t)st * slots);
+    if (lane < slots) x = kSmemModel ? s.chain_s[(size_t)st * slots + lane] : __ldg(table + (size_t)st * slots);
     after_issue();
     r.nlev = __shfl_sync(kFull, x.x, 0);
     r.acc_root = __int_as_float(__shfl_sync(kFull, x.y, 0));
@@ -664,6 +681,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+
+// The tiny-LM copy into `base` (tiny_copy_bytes), issued by one thread; the
+// caller makes the barrier init visible to the CTA (__syncthreads) and every
+// row waits on tiny_bar (phase 0) before its first record read.
+__device__ __forceinline__ void tiny_copy_issue(const DevModel& m, unsigned char* base) {
+  uint64_t* bar = tiny_bar(base, m);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"((uint32_t)(m.tiny_chain_bytes + m.tiny_arcq_bytes))
+               : "memory");
+  bulk_g2s(base, m.chain, (uint32_t)m.tiny_chain_bytes, bar);
+  bulk_g2s(base + align16((size_t)m.tiny_chain_bytes), m.arc_q, (uint32_t)m.tiny_arcq_bytes, bar);
 }
 
 // Generic-proxy shared-memory writes -> later async-proxy accesses (a bulk

@@ -99,12 +99,12 @@ struct DevModel {
 
 // Kernel launchers (advance.cu, fused.cu, decode.cu). Return cudaError_t as int.
 int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* scores,
-                   int32_t* next, float* final_out, void* stream);
+                   int32_t* next, float* final_out, void* stream, uint32_t flags = 0);
 int launch_final(const DevModel& m, const int32_t* states, int32_t B, float* out, void* stream);
 int launch_fused(const DevModel& m, int32_t mode, const float* logits, int64_t row_stride,
                  int32_t B, int32_t* states, int32_t* prev, const uint8_t* active, float lambda,
                  int32_t blank, const float* aux, int64_t aux_stride, float lambda_ilm,
-                 int32_t* tokens_out, void* stream);
+                 int32_t* tokens_out, void* stream, uint32_t flags = 0);
 int launch_fused_rows(int32_t mode, const float* logits, int64_t row_stride, const float* lm_s, const int32_t* lm_n,
                       const float* lm_f, int64_t lm_stride, int32_t B, int32_t V, int32_t* states, int32_t* prev,
                       const uint8_t* active, float lambda, int32_t blank, int32_t* tokens_out, void* stream);

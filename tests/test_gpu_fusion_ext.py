@@ -108,18 +108,24 @@ def test_topk_invalid_state_and_bad_k(pairs):
         m.fused_topk(T(x), T(st), ng.MAX_TOPK + 1)
 
 
+@pytest.mark.parametrize("kernel", [ng.ADVANCE_AUTO, ng.ADVANCE_WARP])
 @pytest.mark.parametrize("B", [100, 592, 593, 1500])
 @pytest.mark.parametrize("mode", [CTC, RNNT, AED])
-def test_fused_step_kernel_paths_by_batch(pairs, mode, B):
+def test_fused_step_kernel_paths_by_batch(pairs, mode, B, kernel):
     """Both transducer paths (the warp pair up to 4 rows per SM, one warp per row
-    beyond) and the CTC/AED warp kernel across batch sizes, vs the oracle."""
+    beyond) and the CTC/AED warp kernel across batch sizes, vs the oracle; AUTO
+    takes the tiny-LM path (model in shared memory), WARP the global-memory kernels."""
     m, o, _ = pairs["five48"]
     x = synth.rnnt_logits(B, 1, o.V, seed=B)[0]
     st = synth.uniform_states(o.num_states, B, seed=B + 1)
     prev = np.random.default_rng(B).integers(-1, o.V, size=B).astype(np.int32) if mode == CTC else None
     st_d, pv_d = T(st), (T(prev) if prev is not None else None)
-    tok = m.fused_greedy_step(mode, T(x), st_d, prev=pv_d, lam=0.8)
-    torch.cuda.synchronize()
+    m.set_advance_kernel(kernel)
+    try:
+        tok = m.fused_greedy_step(mode, T(x), st_d, prev=pv_d, lam=0.8)
+        torch.cuda.synchronize()
+    finally:
+        m.set_advance_kernel(ng.ADVANCE_AUTO)
     to, so, po = o.fused_step(mode, x, st, prev=prev, lam=0.8)
     assert np.array_equal(tok.cpu().numpy(), to) and np.array_equal(st_d.cpu().numpy(), so)
     if mode == CTC:
@@ -190,3 +196,39 @@ def test_every_hot_call_is_graph_capturable(pairs):
             assert same_bits(a.cpu().numpy(), b.cpu().numpy())
         else:
             assert torch.equal(a.cpu(), b.cpu())
+
+
+@pytest.mark.parametrize("plain", [False, True])
+@pytest.mark.parametrize("lm", ["five48", "lm6"])
+def test_logits_ready_ctc_frame_loop(pairs, lm6, lm, plain):
+    """NGPULM_STEP_LOGITS_READY (logits copied before the PDL wait): a CTC frame
+    loop over precomputed logits, every step flagged, equals the
+    oracle's decode; with the LM (tiny and global paths) and plain greedy."""
+    m, o, f = pairs[lm] if lm != "lm6" else lm6
+    B, Tn = 300, 60
+    x = synth.ctc_logits(synth.read_sentences(f.heldout), B, Tn, o.V, seed=17)
+    xd = T(x)
+    lam = 0.0 if plain else 0.5
+    st, pv = T(np.zeros(B, np.int32)), T(np.full(B, -1, np.int32))
+    frames = torch.empty((Tn, B), dtype=torch.int32, device=dev())
+    for t in range(Tn):
+        m.fused_greedy_step(CTC, xd[:, t], None if plain else st, prev=pv, lam=lam, tokens_out=frames[t],
+                            logits_ready=True)
+    torch.cuda.synchronize()
+    ref = o.ctc_decode(x, np.zeros(B, np.int32), prev=np.full(B, -1, np.int32), lam=lam)
+    assert np.array_equal(frames.cpu().numpy().T, ref[0])
+    assert np.array_equal(pv.cpu().numpy(), ref[4])
+    if not plain:
+        assert np.array_equal(st.cpu().numpy(), ref[3])
+
+
+@pytest.mark.parametrize("mode,B", [(AED, 200), (RNNT, 700)])
+def test_logits_ready_other_modes(lm6, mode, B):
+    m, o, f = lm6
+    x = synth.rnnt_logits(B, 1, o.V, seed=B)[0]
+    st = synth.uniform_states(o.num_states, B, seed=B + 3)
+    st_d = T(st)
+    tok = m.fused_greedy_step(mode, T(x), st_d, lam=0.4, logits_ready=True)
+    torch.cuda.synchronize()
+    to, so, _ = o.fused_step(mode, x, st, lam=0.4)
+    assert np.array_equal(tok.cpu().numpy(), to) and np.array_equal(st_d.cpu().numpy(), so)

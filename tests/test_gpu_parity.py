@@ -494,3 +494,41 @@ def test_random_lms_exhaustive(tmp_path_factory, V, order, tokens, seed, prune, 
         tg, sg, _ = gpu_step(m, mode, x, states, pv, None, lam)
         to, so, _ = o.fused_step(mode, x, states, prev=pv, lam=lam)
         assert np.array_equal(tg, to) and np.array_equal(sg, so), mode
+
+
+@pytest.mark.parametrize("B", [1024, 4096, 100])
+def test_advance_independent_calls(lm6, B):
+    """NGPULM_ADVANCE_INDEPENDENT (rows built and stored before the PDL wait, the wait
+    at the end): K back-to-back calls over independent batches into distinct buffers,
+    captured in one CUDA graph and replayed — every row of every call bit-exact vs the
+    oracle; a consumer kernel right after the last call sees all calls complete
+    (stream completion order kept)."""
+    m, o, f = lm6
+    K = 6
+    st_np = np.stack([trajectory_states(m, f, B, seed=40 + k)[0] for k in range(K)])
+    st = torch.from_numpy(st_np).to(dev())
+    sc = torch.empty((K, B, m.V), dtype=torch.float32, device=dev())
+    nx = torch.empty((K, B, m.V), dtype=torch.int32, device=dev())
+    fi = torch.empty((K, B), dtype=torch.float32, device=dev())
+    stream = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        for k in range(K):  # warm-up
+            m.advance(st[k], sc[k], nx[k], fi[k], stream=stream, independent=True)
+        stream.synchronize()
+        sc.zero_(); nx.fill_(-7)
+        with torch.cuda.graph(g, stream=stream):
+            for k in range(K):
+                m.advance(st[k], sc[k], nx[k], fi[k], stream=stream, independent=True)
+            total = nx.sum(dtype=torch.int64)  # a consumer of every call's outputs
+        g.replay()
+    stream.synchronize()
+    tot_host = 0
+    for k in range(K):
+        uniq, inv = np.unique(st_np[k], return_inverse=True)
+        s32, _, n_o, _ = o.rows(uniq, want64=False)
+        f32, _ = o.finals(uniq)
+        assert same_bits(sc[k].cpu().numpy(), s32[inv]) and np.array_equal(nx[k].cpu().numpy(), n_o[inv])
+        assert same_bits(fi[k].cpu().numpy(), f32[inv])
+        tot_host += int(n_o[inv].astype(np.int64).sum())
+    assert int(total.item()) == tot_host

@@ -18,6 +18,7 @@ ctx = synth.sample_contexts(synth.read_sentences(f.heldout), 6, 4096 * 64, seed=
 allst = np.array([m.state_of(b, t) for b, t in ctx], dtype=np.int32)
 stream = torch.cuda.Stream()
 R_BYTES = 600 * 2**20
+INDEP = bool(int(os.environ.get("SWEEP_INDEP", "0")))  # NGPULM_ADVANCE_INDEPENDENT calls
 
 
 def run(B, mode, n=400):
@@ -30,11 +31,11 @@ def run(B, mode, n=400):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(stream):
         for k in range(3):
-            m.advance(st[k % R], sc[k % R], nx[k % R], fi[k % R], stream=stream)
+            m.advance(st[k % R], sc[k % R], nx[k % R], fi[k % R], stream=stream, independent=INDEP)
         stream.synchronize()
         with torch.cuda.graph(g, stream=stream):
             for k in range(n):
-                m.advance(st[k % R], sc[k % R], nx[k % R], fi[k % R], stream=stream)
+                m.advance(st[k % R], sc[k % R], nx[k % R], fi[k % R], stream=stream, independent=INDEP)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ts = []
     for _ in range(5):

@@ -7,7 +7,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["NGPULM_LIB"] = os.path.join(ROOT, "paper_2505_22857_b200", "lib", "libngpulm_timing.so")
+os.environ.setdefault("NGPULM_LIB", os.path.join(ROOT, "paper_2505_22857_b200", "lib", "libngpulm_timing.so"))
+NET = int(os.environ.get("NET", 0))  # 1: a (non-PDL) network kernel writes each step's logits first
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
@@ -33,6 +34,9 @@ def q(a):
 
 
 def report(tag, ph):
+    if len(ph) == 0:
+        print(f"{tag}: no stamps (this kernel path carries no phase stamps)", flush=True)
+        return
     names = [("wait", 1, 2), ("st+rec", 2, 11), ("issue", 11, 3), ("fill", 3, 4), ("rootto", 4, 5),
              ("write", 5, 6), ("logits", 6, 12), ("argmax", 12, 7), ("out", 7, 8)]
     parts = " ".join(f"{n} {q(ph[:, b] - ph[:, a])}" for n, a, b in names)
@@ -47,9 +51,14 @@ for name, mode, gen in (("rnnt", ng.RNNT, synth.rnnt_logits), ("aed", ng.AED, sy
     st = torch.from_numpy(synth.uniform_states(m.num_states, B, seed=3)).cuda()
     pv = torch.full((B,), -1, dtype=torch.int32, device="cuda")
     tok = torch.empty(B, dtype=torch.int32, device="cuda")
+    buf = torch.empty_like(xs[0])
     with torch.cuda.stream(stream):
         for k in range(64):
-            m.fused_greedy_step(mode, xs[k % NB], st, prev=pv if mode == ng.CTC else None, lam=0.3, tokens_out=tok,
+            x = xs[k % NB]
+            if NET:
+                torch.mul(x, 1.0, out=buf)
+                x = buf
+            m.fused_greedy_step(mode, x, st, prev=pv if mode == ng.CTC else None, lam=0.3, tokens_out=tok,
                                 stream=stream)
     stream.synchronize()
-    report(f"{name} B={B} (64th step)", phases(B))
+    report(f"{name} B={B} (64th step{', after a network kernel' if NET else ''})", phases(B))

@@ -18,13 +18,35 @@ p = argparse.ArgumentParser()
 p.add_argument("--batch", type=int, default=1024)
 p.add_argument("--iters", type=int, default=20)
 p.add_argument("--mode", default="advance", choices=["advance", "ctc", "rnnt", "aed", "decode"])
+p.add_argument("--graph", type=int, default=0,
+               help="advance: capture this many calls in one CUDA graph (outputs rotating over 64 sets = "
+                    "512 MiB at B=1024, as bench.py) and replay it --iters times; for ncu --graph-profiling graph")
 a = p.parse_args()
 f = synth.make_lm("/tmp/ngpulm_prof", 1024, 6, tokens=430000, seed=1, heldout=4000, tag="bench_6gram")
 m = ng.load_arpa(f.arpa, vocab_size=1024, device=0)
 ctx = synth.sample_contexts(synth.read_sentences(f.heldout), 6, a.batch * 4, seed=2)
 st_np = np.array([m.state_of(b, t) for b, t in ctx], dtype=np.int32).reshape(4, a.batch)
 st = torch.from_numpy(st_np).cuda()
-if a.mode == "advance":
+if a.mode == "advance" and a.graph:
+    R = 64
+    ctx = synth.sample_contexts(synth.read_sentences(f.heldout), 6, a.batch * R, seed=2)
+    st = torch.from_numpy(np.array([m.state_of(b, t) for b, t in ctx], dtype=np.int32).reshape(R, a.batch)).cuda()
+    sc = torch.empty((R, a.batch, 1024), dtype=torch.float32, device="cuda")
+    nx = torch.empty((R, a.batch, 1024), dtype=torch.int32, device="cuda")
+    fi = torch.empty((R, a.batch), dtype=torch.float32, device="cuda")
+    s_ = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s_):
+        for i in range(3):
+            m.advance(st[i % R], sc[i % R], nx[i % R], fi[i % R], stream=s_)
+        s_.synchronize()
+        with torch.cuda.graph(g, stream=s_):
+            for i in range(a.graph):
+                m.advance(st[i % R], sc[i % R], nx[i % R], fi[i % R], stream=s_)
+        for _ in range(a.iters):
+            g.replay()
+    s_.synchronize()
+elif a.mode == "advance":
     sc = torch.empty((4, a.batch, 1024), dtype=torch.float32, device="cuda")
     nx = torch.empty((4, a.batch, 1024), dtype=torch.int32, device="cuda")
     fi = torch.empty((4, a.batch), dtype=torch.float32, device="cuda")
