@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(32, NGPULM_ADV_MINB(kW, kPacked))
   extern __shared__ __align__(16) unsigned char smem[];
   const int32_t V = m.V;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, R = blockDim.x >> 5;
-  const size_t rb = align16((size_t)V * 4);
+  const size_t rb = kRegRoot ? 0 : align16((size_t)V * 4);  // (kRegRoot: the root weights live in registers)
   const float* root_w = reinterpret_cast<const float*>(smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + rb);
   const WSlice s = wcarve(smem + rb + 16 + (size_t)w * wslice_bytes(V, m.order, 0), V, m.order, 0);
@@ -454,7 +454,8 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
     // per CTA 3.29 us, 1 row 2.83 us; B=4096: 10.1 -> 9.4 us)
     const int R = NGPULM_ADV_ROWS;
     if (wcta_smem(m.V, m.order, R, 0) <= 227 * 1024) {
-      const size_t wsm = wcta_smem(m.V, m.order, R, 0);
+      // (V <= 1024: root weights in registers, no shared copy)
+      const size_t wsm = wcta_smem(m.V, m.order, R, 0) - (small_v ? align16((size_t)m.V * 4) : 0);
       // the grid is padded to a multiple of the SM count (the extra CTAs exit at
       // once), so every SM holds the same number of rows of a call and
       // consecutive calls' CTAs line up on the same SMs: measured B=128 1.92 ->

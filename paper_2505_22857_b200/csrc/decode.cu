@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
       issue_frame(lrow0 + (size_t)t * frame_stride, ncols, ring + (size_t)slot * lstride, full + slot, pol);
       if (++slot == depth) { slot = 0; if (t >= depth) phase ^= 1u; }
     }
+    cp_async_settle();
     if (threadIdx.x == R * 32) mbar_wait(cbar, 0);
     return;
   }
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
       val[j] = col == pc ? x : __fmaf_rn(lambda, lm[j], x);
       mx[j] = val[j];
     }
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + slot)) : "memory");
+    release_slot(empty + slot);
     if (++slot == depth) { slot = 0; phase ^= 1u; }
 #pragma unroll
     for (int d = 1; d < kMaxColsPerLane; d *= 2)
@@ -422,6 +423,7 @@ __global__ void __launch_bounds__(32 * (2 + kSumWarps), 2)
       if (t >= kRing2) mbar_wait(empty + slot, (uint32_t)(t / kRing2 - 1) & 1u);
       issue_frame(lrow0 + (size_t)t * frame_stride, ncols, ring + (size_t)slot * lstride, full + slot, pol);
     }
+    cp_async_settle();
     return;
   }
   mbar_wait(cbar, 0);
@@ -444,9 +446,8 @@ __global__ void __launch_bounds__(32 * (2 + kSumWarps), 2)
         d4[0] = make_float4(fb[sp], x1, x2, x3);
         d4[1] = make_float4(__int_as_float(c1), __int_as_float(c2), 0.f, 0.f);
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(sfull + slot)) : "memory");
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + slot)) : "memory");
       }
-      __syncwarp();
+      release_slot(empty + slot);
     }
     return;
   }
@@ -675,8 +676,7 @@ __global__ void __launch_bounds__(32 * (2 + kSumWarps), 2)
       }
     }
     if (lane == 0 && fout) fout[t] = tok;
-    __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + slot)) : "memory");
+    release_slot(empty + slot);
     D2STAMP(7);
   }
 #ifdef NGPULM_PHASE_TIMING

@@ -241,10 +241,11 @@ __global__ void __launch_bounds__(256, 1)
       if (on) atomicMin(m.bad_row, (unsigned long long)row);
       if (kMode == kLoop && on) lp.frame[row] = lp.len[row];  // an invalid state ends the row's loop
     }
-    if (on || kEarly) mbar_wait(lbar, 0);  // no exit with a bulk copy in flight
+    if (on || kEarly) { mbar_wait(lbar, 0); cp_async_settle(); }  // no exit with a copy in flight
     return;
   }
   mbar_wait(lbar, 0);
+  cp_async_settle();
   __syncwarp();
   STAMP(12);
   // fused values and the row's argmax (R13, R14, R19):
@@ -384,6 +385,7 @@ __global__ void __launch_bounds__(256, 1)
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
       issue_frame(lrow, ncols, lbuf, lbar, pol);
       mbar_wait(lbar, 0);
+      cp_async_settle();
 #pragma unroll
       for (int j = 0; j < kMaxColsPerLane; ++j) {
         const int32_t col = lane + 32 * j;
@@ -663,7 +665,7 @@ __global__ void __launch_bounds__(256, 1)
       if (onx) onx[i] = -1;
     }
     mbar_wait(s.bar, 0);
-    if (started) mbar_wait(lbar, 0);
+    if (started) { mbar_wait(lbar, 0); cp_async_settle(); }
     return;
   }
   Window<kW, kPacked> a;
@@ -689,6 +691,7 @@ __global__ void __launch_bounds__(256, 1)
     if (k0 < nslots) load_window<kW, kPacked>(m, s, lv, r.nlev, k0, nslots, a);
   }
   mbar_wait(lbar, 0);
+  cp_async_settle();
   __syncwarp();
   float val[kMaxColsPerLane];
 #pragma unroll

@@ -398,7 +398,10 @@ __device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, con
 #ifndef NGPULM_ADV_MINB_WIDE
 #define NGPULM_ADV_MINB_WIDE 8
 #endif
-#define NGPULM_ADV_MINB(kW, kPacked) ((kW) == 8 ? ((kPacked) ? 16 : 10) : NGPULM_ADV_MINB_WIDE)
+#ifndef NGPULM_ADV_MINB_PACKED8
+#define NGPULM_ADV_MINB_PACKED8 16
+#endif
+#define NGPULM_ADV_MINB(kW, kPacked) ((kW) == 8 ? ((kPacked) ? NGPULM_ADV_MINB_PACKED8 : 10) : NGPULM_ADV_MINB_WIDE)
 #ifndef NGPULM_TINY_MAX_B
 #define NGPULM_TINY_MAX_B 148  // tiny LM in shared memory up to one row per SM (B=128: 1.34 vs 1.66 us);
 #endif                         // beyond, the one-row-per-CTA global kernel wins (B=1024: 2.53 vs 3.08)
@@ -696,6 +699,21 @@ __device__ __forceinline__ void tiny_copy_issue(const DevModel& m, unsigned char
   bulk_g2s(base, m.chain, (uint32_t)m.tiny_chain_bytes, bar);
   bulk_g2s(base + align16((size_t)m.tiny_chain_bytes), m.arc_q, (uint32_t)m.tiny_arcq_bytes, bar);
 }
+
+// A ring slot's consumers are done with it: every lane's generic reads of the
+// slot are ordered before the async-proxy (TMA / cp.async) writes that refill
+// it (proxy fence + warp sync), then lane 0 arrives on the slot's "empty"
+// mbarrier (release).
+__device__ __forceinline__ void release_slot(uint64_t* empty) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0)
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty)) : "memory");
+}
+// After waiting on an mbarrier that tracks this thread's cp.async (edge
+// columns of issue_frame): the thread's own completion wait (a no-op by then;
+// the mbarrier phase already implies it) so every cp.async has a matching wait.
+__device__ __forceinline__ void cp_async_settle() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Generic-proxy shared-memory writes -> later async-proxy accesses (a bulk
 // store reading the row, or a bulk copy overwriting it): every writing lane

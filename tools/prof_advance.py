@@ -21,6 +21,7 @@ p.add_argument("--mode", default="advance", choices=["advance", "ctc", "rnnt", "
 p.add_argument("--graph", type=int, default=0,
                help="advance: capture this many calls in one CUDA graph (outputs rotating over 64 sets = "
                     "512 MiB at B=1024, as bench.py) and replay it --iters times; for ncu --graph-profiling graph")
+p.add_argument("--independent", action="store_true", help="advance calls with NGPULM_ADVANCE_INDEPENDENT")
 a = p.parse_args()
 f = synth.make_lm("/tmp/ngpulm_prof", 1024, 6, tokens=430000, seed=1, heldout=4000, tag="bench_6gram")
 m = ng.load_arpa(f.arpa, vocab_size=1024, device=0)
@@ -38,11 +39,11 @@ if a.mode == "advance" and a.graph:
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s_):
         for i in range(3):
-            m.advance(st[i % R], sc[i % R], nx[i % R], fi[i % R], stream=s_)
+            m.advance(st[i % R], sc[i % R], nx[i % R], fi[i % R], stream=s_, independent=a.independent)
         s_.synchronize()
         with torch.cuda.graph(g, stream=s_):
             for i in range(a.graph):
-                m.advance(st[i % R], sc[i % R], nx[i % R], fi[i % R], stream=s_)
+                m.advance(st[i % R], sc[i % R], nx[i % R], fi[i % R], stream=s_, independent=a.independent)
         for _ in range(a.iters):
             g.replay()
     s_.synchronize()
@@ -51,7 +52,7 @@ elif a.mode == "advance":
     nx = torch.empty((4, a.batch, 1024), dtype=torch.int32, device="cuda")
     fi = torch.empty((4, a.batch), dtype=torch.float32, device="cuda")
     for i in range(a.iters):
-        m.advance(st[i % 4], sc[i % 4], nx[i % 4], fi[i % 4])
+        m.advance(st[i % 4], sc[i % 4], nx[i % 4], fi[i % 4], independent=a.independent)
 elif a.mode == "decode":  # persistent CTC decode, BASELINE configs[2] shape
     T = 500
     x = torch.from_numpy(synth.ctc_logits(synth.read_sentences(f.heldout), a.batch, T, 1024, seed=4)).cuda()

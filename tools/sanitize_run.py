@@ -109,7 +109,8 @@ for name, (m, o, f) in models.items():
         m.set_chain_mode(chain)
         st0 = np.zeros(Bc, np.int32); pv0 = np.full(Bc, -1, np.int32)
         sd, pd = T_(st0), T_(pv0)
-        fr, em, el = m.ctc_greedy_decode(T_(xc), sd, pd, lam=0.7, lengths=T_(lengths))
+        em0 = torch.full((Bc, Tc), -1, dtype=torch.int32, device=dev)  # entries past emit_len are never written
+        fr, em, el = m.ctc_greedy_decode(T_(xc), sd, pd, lam=0.7, lengths=T_(lengths), emit_out=em0)
         torch.cuda.synchronize()
         ref = o.ctc_decode(xc, st0, prev=pv0, lam=0.7, lengths=lengths)
         check(f"ctc decode {name} chain={chain}", np.array_equal(fr.cpu().numpy(), ref[0])
@@ -117,7 +118,8 @@ for name, (m, o, f) in models.items():
     m.set_chain_mode(ng.CHAIN_TABLE)
     if Bc:
         pd = T_(np.full(Bc, -1, np.int32))
-        fr, em, el = m.ctc_greedy_decode(T_(xc), None, pd, lam=0.0, lengths=T_(lengths))
+        em0 = torch.full((Bc, Tc), -1, dtype=torch.int32, device=dev)
+        fr, em, el = m.ctc_greedy_decode(T_(xc), None, pd, lam=0.0, lengths=T_(lengths), emit_out=em0)
         torch.cuda.synchronize()
         ref = o.ctc_decode(xc, np.zeros(Bc, np.int32), prev=np.full(Bc, -1, np.int32), lam=0.0, lengths=lengths)
         check(f"ctc decode plain {name}", np.array_equal(fr.cpu().numpy(), ref[0]))
