@@ -650,12 +650,13 @@ def bench_config4(args, rank, local, world, dev, stream, barrier):
     nx = torch.empty((R, Bl, V), dtype=torch.int32, device=dev)
     fi = torch.empty((R, Bl), dtype=torch.float32, device=dev)
 
-    def call(k):
+    def call(k, ind=True):  # independent batches (NGPULM_ADVANCE_INDEPENDENT), as the headline
         r = k % R
-        m.advance(st[r], sc[r], nx[r], fi[r], stream=stream)
+        m.advance(st[r], sc[r], nx[r], fi[r], stream=stream, independent=ind)
     K = 128
     ms = window_ms(call, K, stream, reps=7, barrier=barrier)
     us = ms * 1e3 / K
+    us_dep = window_ms(lambda k: call(k, False), K, stream, reps=7, barrier=barrier) * 1e3 / K
     peak_gbs, _ = peaks()
     comp = 8 * Bl * V + 8 * Bl
     touched = statistics.mean(m.touched_bytes(allst[r, lo:hi]) for r in range(min(R, 4)))
@@ -667,6 +668,8 @@ def bench_config4(args, rank, local, world, dev, stream, barrier):
                         "algorithmic_bytes_per_launch": comp,
                         "trie_unique_bytes_per_launch": touched,
                         "frac_incl_trie": (comp + touched) / (us * 1e-6) / 1e9 / peak_gbs},
+           "us_per_call_dependent": us_dep,
+           "frac_dependent": comp / (us_dep * 1e-6) / 1e9 / peak_gbs,
            "model_bytes_per_gpu": m.info.device_bytes, "load_s_rank0": load_s,
            "single_call_latency_us": single_call_us(call, stream)}
     # the NCCL gather of per-rank results (outside the timed region) and the check
@@ -720,16 +723,18 @@ def bench_config3(args, rank, world, dev, stream, barrier, no_fused):
     nx = torch.empty((R, B, V), dtype=torch.int32, device=dev)
     fi = torch.empty((R, B), dtype=torch.float32, device=dev)
 
-    def adv(k):
+    def adv(k, ind=True):  # independent batches (NGPULM_ADVANCE_INDEPENDENT), as the headline
         r = k % R
-        m.advance(st[r], sc[r], nx[r], fi[r], stream=stream)
+        m.advance(st[r], sc[r], nx[r], fi[r], stream=stream, independent=ind)
     us = window_ms(adv, 256, stream) * 1e3 / 256
+    us_dep = window_ms(lambda k: adv(k, False), 256, stream) * 1e3 / 256
     peak_gbs, _ = peaks()
     comp = 8 * B * V + 8 * B
     touched = statistics.mean(m.touched_bytes(stn[r]) for r in range(4))
     out = {"workload": f"token 8-gram LM, V={V}, {m.info.num_arcs} arcs / {m.num_states} states (~4.9M n-grams), "
                        f"B={B}",
            "advance_us_per_call": us,
+           "advance_us_per_call_dependent": us_dep,
            "advance_roofline": {"bound": "hbm", "achieved": comp / (us * 1e-6) / 1e9, "peak": peak_gbs,
                                 "unit": "GB/s", "frac": comp / (us * 1e-6) / 1e9 / peak_gbs,
                                 "algorithmic_bytes_per_launch": comp, "trie_unique_bytes_per_launch": touched},

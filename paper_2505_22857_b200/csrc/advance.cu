@@ -477,11 +477,17 @@ int launch_advance(const DevModel& m, const int32_t* states, int32_t B, float* s
 #define NGPULM_WARP_LAUNCH(T, W, P)                                                                                 \
   return small_v ? launch(advance_warp_kernel<T, W, P, true>, wg, wb, wsm, st, m, states, B, scores, next, final_out) \
                  : launch(advance_warp_kernel<T, W, P, false>, wg, wb, wsm, st, m, states, B, scores, next, final_out)
-      if (indep && table && pk && small_v)
-        return wide ? launch(advance_warp_kernel<true, 16, true, true, true>, wg, wb, wsm, st, m, states, B, scores,
+      if (indep && table && small_v) {
+        if (pk)
+          return wide ? launch(advance_warp_kernel<true, 16, true, true, true>, wg, wb, wsm, st, m, states, B,
+                               scores, next, final_out)
+                      : launch(advance_warp_kernel<true, 8, true, true, true>, wg, wb, wsm, st, m, states, B,
+                               scores, next, final_out);
+        return wide ? launch(advance_warp_kernel<true, 16, false, true, true>, wg, wb, wsm, st, m, states, B, scores,
                              next, final_out)
-                    : launch(advance_warp_kernel<true, 8, true, true, true>, wg, wb, wsm, st, m, states, B, scores,
+                    : launch(advance_warp_kernel<true, 8, false, true, true>, wg, wb, wsm, st, m, states, B, scores,
                              next, final_out);
+      }
       if (table) {
         if (wide) { if (pk) NGPULM_WARP_LAUNCH(true, 16, true); NGPULM_WARP_LAUNCH(true, 16, false); }
         if (pk) NGPULM_WARP_LAUNCH(true, 8, true);

@@ -496,8 +496,9 @@ def test_random_lms_exhaustive(tmp_path_factory, V, order, tokens, seed, prune, 
         assert np.array_equal(tg, to) and np.array_equal(sg, so), mode
 
 
+@pytest.mark.parametrize("kernel", [ng.ADVANCE_AUTO, ng.ADVANCE_WARP])
 @pytest.mark.parametrize("B", [1024, 4096, 100])
-def test_advance_independent_calls(lm6, B):
+def test_advance_independent_calls(lm6, B, kernel):
     """NGPULM_ADVANCE_INDEPENDENT (rows built and stored before the PDL wait, the wait
     at the end): K back-to-back calls over independent batches into distinct buffers,
     captured in one CUDA graph and replayed — every row of every call bit-exact vs the
@@ -512,7 +513,7 @@ def test_advance_independent_calls(lm6, B):
     fi = torch.empty((K, B), dtype=torch.float32, device=dev())
     stream = torch.cuda.Stream()
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(stream):
+    with using(m, kernel=kernel), torch.cuda.stream(stream):
         for k in range(K):  # warm-up
             m.advance(st[k], sc[k], nx[k], fi[k], stream=stream, independent=True)
         stream.synchronize()
@@ -522,7 +523,7 @@ def test_advance_independent_calls(lm6, B):
                 m.advance(st[k], sc[k], nx[k], fi[k], stream=stream, independent=True)
             total = nx.sum(dtype=torch.int64)  # a consumer of every call's outputs
         g.replay()
-    stream.synchronize()
+        stream.synchronize()
     tot_host = 0
     for k in range(K):
         uniq, inv = np.unique(st_np[k], return_inverse=True)

@@ -20,7 +20,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 600 ncu --graph-profiling graph --clock-control none \
     --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sector_hit_rate.pct \
     --csv --log-file gpurun_out/graph_$TAG.csv python tools/prof_advance.py --batch 1024 --graph 256 --iters 3 > /dev/null 2>&1
-cat gpurun_out/graph_$TAG.csv | tail -8
+timeout 600 ncu --graph-profiling graph --clock-control none \
+    --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sector_hit_rate.pct \
+    --csv --log-file gpurun_out/graph_indep_$TAG.csv python tools/prof_advance.py --batch 1024 --graph 256 --iters 3 --independent > /dev/null 2>&1
+cat gpurun_out/graph_$TAG.csv | tail -4; cat gpurun_out/graph_indep_$TAG.csv | tail -4
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:advance_warp -s 10 -c 1 \
     -o gpurun_out/adv_$TAG -f python tools/prof_advance.py --batch 1024 > gpurun_out/ncu_full_$TAG.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused_warp -s 10 -c 1 \
