@@ -23,7 +23,8 @@ namespace {
 //    slot through its "empty" mbarrier.
 constexpr int kRingMax = 8;
 
-__host__ __device__ constexpr size_t lbuf_bytes(int32_t V) { return align16((size_t)(V + 1) * 4 + 16); }
+// a frame slot: V+1 columns + the slack of a 16-byte-aligned cover (issue_frame_cover)
+__host__ __device__ constexpr size_t lbuf_bytes(int32_t V) { return align16((size_t)(V + 1) * 4 + 32); }
 // per row: row_s | row_n | levels | 2 mbarriers | full [kRingMax] | empty [kRingMax] | ring buffers [depth]
 __host__ __device__ constexpr size_t dslice_bytes(int32_t V, int32_t order, int depth) {
   return wslice_bytes(V, order, 0) + 2 * kRingMax * 8 + (size_t)depth * lbuf_bytes(V);
@@ -695,6 +696,339 @@ __global__ void __launch_bounds__(32 * (2 + kSumWarps), 2)
   }
 }
 
+// ---------------------------------------------------------------- segment-parallel exact CTC decode
+// A row's decisions form one chain (frame t needs the LM state and prev after
+// frame t-1), ~290 emissions long at configs[2], each emission a dependent
+// record -> arcs -> row rebuild. The chain is cut into K segments decoded at
+// once (pass 1): segment 0 from the row's true start; segment k >= 1 from the
+// root state and no prev, kSegWarm frames before its first frame (an n-gram
+// state is the suffix of the last N-1 emitted tokens, so the warm-up usually
+// reaches the true trajectory before the segment starts). Pass 2 walks the
+// segments of a row in order from the TRUE state at each boundary (the
+// previous segment's last record) and re-decides frames until its decision
+// and state equal pass 1's at the same frame — decisions depend only on
+// (state, prev) and the frame, so from there on pass 1's records are the true
+// ones; a segment that never meets is re-decided to its end. The same warp then turns the
+// per-frame decisions into the emission list, the final state and prev.
+// Every output is therefore exactly ctc_decode_kernel's (tested bit-exact).
+// Records: frames_out holds the decisions, emit_out (row stride T) the state
+// after every frame until the end of pass 2 overwrites it with the emissions.
+// One warp per chain with its own TMA ring (lane 0 refills a slot right after
+// the warp has read it), so a segment costs one warp's registers.
+#ifndef NGPULM_SEG_CHAINS
+#define NGPULM_SEG_CHAINS 1184  // chains (rows x segments) one launch holds at once (8 one-warp chains per SM)
+#endif
+#ifndef NGPULM_SEG_MIN_FRAMES
+#define NGPULM_SEG_MIN_FRAMES 64  // fewest frames per segment
+#endif
+#ifndef NGPULM_SEG_EXPT
+#define NGPULM_SEG_EXPT 0  // timing experiments only (tools/): bit 0 no proxy fence, bit 1 no pass-1 records
+#endif
+#ifndef NGPULM_SEG_RING
+#define NGPULM_SEG_RING 4
+#endif
+constexpr int kSegRing = NGPULM_SEG_RING;  // frames in flight per chain
+constexpr int kSegWarm = 16;  // warm-up frames before a segment >= 1
+constexpr int kSegRows = 4;   // chains (warps) per CTA, sharing the root-level copy: 2 CTAs = 8 chains per SM
+                              // (2 chains per CTA: 3 CTAs fit the shared memory, 6 chains, two waves at B=256)
+
+__host__ __device__ constexpr size_t sslice_bytes(int32_t V, int32_t order) {
+  return wslice_bytes(V, order, 0) + kSegRing * 8 + (size_t)kSegRing * lbuf_bytes(V);
+}
+// [tiny model copy] | root_w | root_to | cbar | R slices (row | levels | 2 bars | full[kSegRing] | ring)
+__host__ __device__ constexpr size_t scta_smem(int32_t V, int32_t order, int R) {
+  return 2 * align16((size_t)V * 4) + 16 + (size_t)R * sslice_bytes(V, order);
+}
+
+// The end of pass 2, per row (one warp): the emissions from the decisions (CTC
+// collapse: a selection that is neither blank nor prev), the final state and
+// prev; frames past the row's length -1; an invalid row as ctc_decode_kernel
+// (bad-row word, nothing decided, state and prev unchanged).
+__device__ __forceinline__ void compact_row(int32_t row, int32_t T, int32_t len, int32_t st0, int32_t sp,
+                                            int32_t* frames_out, int32_t* rec, int32_t* states, int32_t* prev,
+                                            int32_t* emit_len, unsigned long long* bad_row, bool bad) {
+  const int lane = threadIdx.x & 31;
+  int32_t* fo = frames_out + (size_t)row * T;
+  int32_t* eo = rec + (size_t)row * T;
+  if (bad) {
+    for (int32_t t = lane; t < T; t += 32) fo[t] = -1;
+    if (lane == 0) {
+      if (len > 0) atomicMin(bad_row, (unsigned long long)row);
+      if (emit_len) emit_len[row] = 0;
+    }
+    return;
+  }
+  const int32_t st_final = len > 0 ? eo[len - 1] : st0;  // the last record, read before eo is overwritten
+  int32_t pc = prev[row], count = 0;
+  __syncwarp();
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int32_t b = 0; b < len; b += 32) {
+    const int32_t t = b + lane;
+    const int32_t f = t < len ? fo[t] : -1;
+    const uint32_t valid = __ballot_sync(kFull, f >= 0);
+    const uint32_t before = valid & lt;  // prev before frame t: the last selecting frame before it
+    const int32_t fp = __shfl_sync(kFull, f, before ? 31 - __clz(before) : 0);
+    const int32_t pcb = before ? (fp == sp ? -1 : fp) : pc;
+    const bool emit = f >= 0 && f != sp && f != pcb;
+    const uint32_t em = __ballot_sync(kFull, emit);
+    if (emit) eo[count + __popc(em & lt)] = f;
+    count += __popc(em);
+    if (valid) {
+      const int32_t fl = __shfl_sync(kFull, f, 31 - __clz(valid));
+      pc = fl == sp ? -1 : fl;
+    }
+  }
+  for (int32_t t = len + lane; t < T; t += 32) fo[t] = -1;
+  __syncwarp();
+  if (lane == 0) {
+    states[row] = st_final;
+    prev[row] = pc;
+    if (emit_len) emit_len[row] = count;
+  }
+}
+
+template <bool kTable, bool kPacked, bool kTiny, bool kFix>
+__global__ void __launch_bounds__(32 * kSegRows, 8 / kSegRows)
+    ctc_seg_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int64_t frame_stride,
+                   int32_t B, int32_t T, int32_t K, int32_t L, const int32_t* __restrict__ lengths,
+                   int32_t* __restrict__ states, int32_t* __restrict__ prev, float lambda, int32_t sp,
+                   int32_t* __restrict__ frames_out, int32_t* __restrict__ rec, int32_t* __restrict__ emit_len) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int32_t V = m.V, ncols = V + 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, R = blockDim.x >> 5;
+  const size_t rb = align16((size_t)V * 4);
+  unsigned char* sm0 = smem + (kTiny ? tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) : 0);
+  float* root_w = reinterpret_cast<float*>(sm0);
+  int32_t* root_to = reinterpret_cast<int32_t*>(sm0 + rb);
+  uint64_t* cbar = reinterpret_cast<uint64_t*>(sm0 + 2 * rb);
+  unsigned char* base = sm0 + 2 * rb + 16 + (size_t)w * sslice_bytes(V, m.order);
+  WSlice s = wcarve(base, V, m.order, 0);
+  if (kTiny) {
+    s.chain_s = reinterpret_cast<const int4*>(smem);
+    s.st_q = reinterpret_cast<int4*>(smem + align16((size_t)m.tiny_chain_bytes));
+  }
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + wslice_bytes(V, m.order, 0));
+  float* ring = reinterpret_cast<float*>(base + wslice_bytes(V, m.order, 0) + kSegRing * 8);
+  const size_t lstride = lbuf_bytes(V) / 4;
+  pdl_trigger();
+  if (threadIdx.x == 0) {  // the root level (immutable model data: before the wait)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(cbar)) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(cbar)), "r"((uint32_t)V * 8u)
+                 : "memory");
+    bulk_g2s(root_w, m.arc_w, (uint32_t)V * 4u, cbar);
+    bulk_g2s(root_to, m.arc_to, (uint32_t)V * 4u, cbar);
+    if (kTiny) tiny_copy_issue(m, smem);
+  }
+  if (lane == 0) {
+    for (int i = 0; i < kSegRing; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + i)) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  const int32_t chain = (int32_t)blockIdx.x * R + w;
+  const int32_t row = kFix ? chain : chain / K;
+  const int32_t k0 = kFix ? 0 : chain % K;
+  auto cta_exit = [&]() {  // no exit with the CTA's bulk copies in flight
+    if (threadIdx.x == 0) {
+      mbar_wait(cbar, 0);
+      if (kTiny) mbar_wait(tiny_bar(smem, m), 0);
+    }
+  };
+  if (row >= B) { cta_exit(); return; }
+  pdl_wait();  // (pass 2 reads pass 1's records)
+  int32_t len = T;
+  if (lengths) len = min(T, max(0, __ldg(&lengths[row])));
+  const int32_t st0 = states[row];  // (pass 2 rewrites it last, in compact_row)
+  if (!kFix && (st0 < 0 || st0 >= m.S || k0 * L >= len)) { cta_exit(); return; }
+  if (kFix && (st0 < 0 || st0 >= m.S)) {  // an invalid row decides nothing (as ctc_decode_kernel)
+    compact_row(row, T, len, st0, sp, frames_out, rec, states, prev, emit_len, m.bad_row, true);
+    cta_exit();
+    return;
+  }
+  mbar_wait(cbar, 0);
+  if (kTiny) mbar_wait(tiny_bar(smem, m), 0);
+  const float* lrow0 = logits + (size_t)row * row_stride;
+  int32_t* fo = frames_out + (size_t)row * T;
+  int32_t* ro = rec + (size_t)row * T;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  // the ring: frame number `idx` (counted over the warp's life) sits in slot idx % kSegRing
+  uint32_t issued = 0, consumed = 0;
+  int32_t next_t = 0, stop_t = 0;
+  // the bytes the logits view spans (frame covers may read a few columns of the neighbouring frames)
+  const float* lo_b = logits;
+  const float* hi_b = logits + (size_t)(B - 1) * row_stride + (size_t)(T - 1) * frame_stride + ncols;
+  auto issue_upto = [&]() {
+    while (issued - consumed < (uint32_t)kSegRing && next_t < stop_t) {
+      issue_frame_cover(lrow0 + (size_t)next_t * frame_stride, ncols, ring + (size_t)(issued % kSegRing) * lstride,
+                        full + issued % kSegRing, pol, lo_b, hi_b);
+      ++issued;
+      ++next_t;
+    }
+  };
+  auto take = [&](int32_t t) {  // wait for the next frame (t) of the ring; column c at [c]
+    mbar_wait(full + consumed % kSegRing, (consumed / kSegRing) & 1u);  // (it tracks the edge cp.asyncs too)
+    const float* lrow = lrow0 + (size_t)t * frame_stride;
+    return ring + (size_t)(consumed % kSegRing) * lstride + (reinterpret_cast<uintptr_t>(lrow) & 15) / 4;
+  };
+  auto give = [&]() {  // the warp is done with the frame: its slot may be refilled
+    if (!(NGPULM_SEG_EXPT & 1)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    ++consumed;
+  };
+#ifdef NGPULM_PHASE_TIMING
+  // debug build: per chain 0 rebuilds, 1 frame waits, 2 loads + refill issue, 3 decision, 4 records;
+  // counts 5 frames, 6 rebuilds
+  long long ck[7] = {0};
+  long long tq0 = clock64(), tq1;
+#define SSTAMP(i) do { tq1 = clock64(); ck[i] += tq1 - tq0; tq0 = tq1; } while (0)
+#else
+#define SSTAMP(i) do { } while (0)
+#endif
+  float lm[kMaxColsPerLane];
+  int32_t row_state = -1;
+  auto ensure_row = [&](int32_t st) {
+    if (row_state == st) return;
+#ifdef NGPULM_PHASE_TIMING
+    ck[6] += 1;
+#endif
+    build_row_warp<kTable, kPacked, NoStamp, kTiny>(m, s, root_w, root_to, st);
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j) {
+      const int32_t col = lane + 32 * j;
+      lm[j] = (col < ncols && col != sp) ? s.row_s[col - (col > sp)] : 0.f;  // blank: 0 (fused value = asr)
+    }
+    row_state = st;
+  };
+  // the fused CTC decision of one frame (ctc_decode_kernel's, R13, R14, R17, R19); the frame's
+  // slot is handed back (and refilled) as soon as its columns are in registers
+  auto decide = [&](const float* fb, int32_t pc) {
+    float val[kMaxColsPerLane], mx[kMaxColsPerLane];
+    const float* bp = fb + lane;
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j) {
+      const int32_t col = lane + 32 * j;
+      val[j] = __int_as_float(0x7fc00000);
+      if (col < ncols) val[j] = bp[32 * j];
+    }
+    give();
+    issue_upto();
+    SSTAMP(2);
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j) {
+      const int32_t col = lane + 32 * j;
+      val[j] = col == pc ? val[j] : __fmaf_rn(lambda, lm[j], val[j]);
+      mx[j] = val[j];
+    }
+#pragma unroll
+    for (int d = 1; d < kMaxColsPerLane; d *= 2)
+#pragma unroll
+      for (int j = 0; j + d < kMaxColsPerLane; j += 2 * d) mx[j] = fmaxf(mx[j], mx[j + d]);
+    const float lmax = mx[0] == mx[0] ? mx[0] : -INFINITY;
+    const uint32_t kmax = __reduce_max_sync(kFull, fkey(lmax));
+    const float M = __uint_as_float((kmax & 0x80000000u) ? (kmax ^ 0x80000000u) : ~kmax);
+    int32_t cm[kMaxColsPerLane];
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerLane; ++j) cm[j] = val[j] == M ? lane + 32 * j : INT_MAX;
+#pragma unroll
+    for (int d = 1; d < kMaxColsPerLane; d *= 2)
+#pragma unroll
+      for (int j = 0; j + d < kMaxColsPerLane; j += 2 * d) cm[j] = min(cm[j], cm[j + d]);
+    return (int32_t)__reduce_min_sync(kFull, (uint32_t)cm[0]);
+  };
+  // one frame t: decision from (st, pc), then (st, pc) after it; returns the selected column or -1
+  auto step = [&](int32_t t, int32_t& st, int32_t& pc) {
+    SSTAMP(4);
+    ensure_row(st);  // (a rebuild runs while the ring's next frames land)
+    SSTAMP(0);
+    const float* fb = take(t);
+    SSTAMP(1);
+    const int32_t bc = decide(fb, pc);
+    SSTAMP(3);
+#ifdef NGPULM_PHASE_TIMING
+    ck[5] += 1;
+#endif
+    if (bc < 0 || bc >= ncols) return -1;  // all-NaN frame: nothing changes
+    if (bc == sp) {
+      pc = -1;
+    } else if (bc != pc) {  // an emission: LM advance
+      st = s.row_n[bc < sp ? bc : bc - 1];
+      pc = bc;
+    }
+    return bc;
+  };
+  if (!kFix) {  // ---- pass 1: segment k0
+    const int32_t t0 = k0 * L, t1 = min(t0 + L, len);
+    const int32_t tb = k0 == 0 ? 0 : max(0, t0 - kSegWarm);
+    int32_t st = k0 == 0 ? st0 : 0, pc = k0 == 0 ? __ldg(&prev[row]) : -1;
+    next_t = tb;
+    stop_t = t1;
+    issue_upto();
+    int32_t my_tok = -1, my_st = 0;  // the records of frames t0 + 32 i + lane, stored 32 frames at a time
+    for (int32_t t = tb; t < t1; ++t) {
+      const int32_t tok = step(t, st, pc);
+      if (t >= t0 && !(NGPULM_SEG_EXPT & 2)) {
+        const int32_t i = (t - t0) & 31;
+        if (lane == i) { my_tok = tok; my_st = st; }
+        if (i == 31 || t == t1 - 1) {
+          if (lane <= i) {
+            fo[t - i + lane] = my_tok;
+            ro[t - i + lane] = my_st;
+          }
+        }
+      }
+      SSTAMP(4);
+    }
+  } else {  // ---- pass 2: the segments of the row in order, from the true boundary state
+    for (int32_t k = 1; k < K; ++k) {
+      const int32_t t0 = k * L, t1 = min(t0 + L, len);
+      if (t0 >= len) break;
+      int32_t st = ro[t0 - 1], pc = __ldg(&prev[row]);
+      // prev before t0: the last frame before t0 that selected a column (blank -> -1)
+      for (int32_t b = t0 - 1; b >= 0; b -= 32) {
+        const int32_t t = b - lane;
+        const int32_t f = t >= 0 ? fo[t] : -1;
+        const uint32_t hit = __ballot_sync(kFull, f >= 0);
+        if (hit) {
+          const int32_t fl = __shfl_sync(kFull, f, __ffs(hit) - 1);
+          pc = fl == sp ? -1 : fl;
+          break;
+        }
+      }
+      next_t = t0;
+      stop_t = t1;
+      issue_upto();
+      for (int32_t t = t0; t < t1; ++t) {
+        const int32_t tok = step(t, st, pc);
+#ifdef NGPULM_PHASE_TIMING
+        if (lane == 0 && row < 4096) g_phase[(8192 + row) * 16 + k] += 1;  // fix-up frames of segment k
+#endif
+        const int32_t f_rec = fo[t], s_rec = ro[t];
+        const bool met = tok >= 0 && tok == f_rec && st == s_rec;  // same (state, prev) from here on
+        if (!met && lane == 0) {
+          fo[t] = tok;
+          ro[t] = st;
+        }
+        __syncwarp();
+        if (met) break;
+      }
+      while (consumed < issued) {  // frames issued past the meeting point: let them land
+        take(0);
+        give();
+      }
+    }
+    __syncwarp();
+    compact_row(row, T, len, st0, sp, frames_out, rec, states, prev, emit_len, m.bad_row, false);
+  }
+  cp_async_settle();  // every edge cp.async of this warp has landed (the ring waits already implied it)
+#ifdef NGPULM_PHASE_TIMING
+  if (!kFix && lane == 0 && chain < 16384)
+    for (int i = 0; i < 7; ++i) g_phase[chain * 16 + i] = (unsigned long long)ck[i];
+#endif
+#undef SSTAMP
+}
+
 }  // namespace
 
 int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride, int64_t frame_stride, int32_t B,
@@ -719,6 +1053,31 @@ int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride
     NGPULM_DECODE2(false, false);
 #endif
 #undef NGPULM_DECODE2
+  }
+  // segment-parallel exact decode: table mode, both record buffers given, enough frames per segment
+  int K = (int)(NGPULM_SEG_CHAINS / (B > 0 ? B : 1));
+  K = K > 8 ? 8 : K;
+  if (K > T / NGPULM_SEG_MIN_FRAMES) K = T / NGPULM_SEG_MIN_FRAMES;
+  if (table && frames_out && emit_out && K >= 2 && NGPULM_SEG_CHAINS > 0) {
+    const int32_t L = (T + K - 1) / K;
+    const bool tiny = pk && m.tiny_chain_bytes > 0;
+    const size_t sm = scta_smem(m.V, m.order, kSegRows) + (tiny ? tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) : 0);
+    if (sm <= 227 * 1024) {
+      const dim3 b1(32 * kSegRows), g1((B * K + kSegRows - 1) / kSegRows), g2((B + kSegRows - 1) / kSegRows);
+      int e;
+#define NGPULM_SEG(P, TI, FIX, G)                                                                                   \
+  launch(ctc_seg_kernel<true, P, TI, FIX>, G, b1, sm, st, m, logits, row_stride, frame_stride, B, T, K, L, lengths,   \
+         states, prev, lambda, blank, frames_out, emit_out, emit_len)
+      if (tiny) e = NGPULM_SEG(true, true, false, g1);
+      else if (pk) e = NGPULM_SEG(true, false, false, g1);
+      else e = NGPULM_SEG(false, false, false, g1);
+      if (e) return e;
+      if (tiny) e = NGPULM_SEG(true, true, true, g2);
+      else if (pk) e = NGPULM_SEG(true, false, true, g2);
+      else e = NGPULM_SEG(false, false, true, g2);
+#undef NGPULM_SEG
+      return e;
+    }
   }
   if (table && pk && m.tiny_chain_bytes > 0) {  // tiny LM: the model in every CTA's shared memory
     const size_t mb = tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes);

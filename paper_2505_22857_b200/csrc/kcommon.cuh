@@ -829,6 +829,32 @@ __device__ __forceinline__ void issue_frame(const float* lrow, int32_t ncols, fl
   }
 }
 
+// issue_frame when the frame's 16-byte-aligned cover [floor16(lrow),
+// ceil16(lrow + ncols)) lies inside [lo, hi) (the bytes the caller's logits
+// view spans): ONE bulk copy of the cover by lane 0 (the few columns of the
+// neighbouring frames it also brings are never read); column c lands at
+// buf[h + c] as with issue_frame. Otherwise (the first / last frame of the
+// view, unaligned) issue_frame's interior + edge copies. Warp-uniform call.
+__device__ __forceinline__ void issue_frame_cover(const float* lrow, int32_t ncols, float* buf, uint64_t* bar,
+                                                  uint64_t pol, const float* lo, const float* hi) {
+  const uintptr_t src = reinterpret_cast<uintptr_t>(lrow);
+  const uintptr_t c0 = src & ~(uintptr_t)15, c1 = (src + (uintptr_t)ncols * 4 + 15) & ~(uintptr_t)15;
+  if (c0 >= reinterpret_cast<uintptr_t>(lo) && c1 <= reinterpret_cast<uintptr_t>(hi)) {
+    if ((threadIdx.x & 31) == 0) {
+      const uint32_t bytes = (uint32_t)(c1 - c0);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+              smem_u32(buf)),
+          "l"(c0), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+          : "memory");
+    }
+    return;
+  }
+  issue_frame(lrow, ncols, buf, bar, pol);
+}
+
 // Total order of floats as unsigned keys (larger float -> larger key).
 __device__ __forceinline__ uint32_t fkey(float v) {
   const uint32_t u = __float_as_uint(v);

@@ -139,3 +139,80 @@ def test_decode_refuses_v_not_multiple_of_4(pairs):
     st = torch.zeros(2, dtype=torch.int32, device=dev())
     with pytest.raises(ng.NgpulmError):
         m.ctc_greedy_decode(x, st, st.clone() - 1)
+
+
+@pytest.mark.parametrize("lam", [0.0, 0.3, 3.0])
+@pytest.mark.parametrize("B,T", [(1, 700), (7, 300), (64, 256), (300, 200)])
+def test_segmented_decode_matches_oracle_and_sequential(lm6, B, T, lam):
+    """The segment-parallel decode (frames_out and emit_out given, T >= 128): every
+    row vs the oracle's decode and vs the single-chain kernel (frames_out = NULL),
+    with ragged lengths around the segment boundaries (0, 1, 63, 64, 65, T)."""
+    m, o, f = lm6
+    rng = np.random.default_rng(B * 7 + T)
+    x = synth.ctc_logits(synth.read_sentences(f.heldout), B, T, m.V, seed=B + T)
+    lengths = rng.integers(0, T + 1, size=B).astype(np.int32)
+    special = [0, 1, 63, 64, 65, T, T // 2, T - 1]
+    lengths[: min(B, len(special))] = special[: min(B, len(special))]
+    start = np.where(rng.random(B) < 0.5, 0, m.bos_state).astype(np.int32)
+    prev0 = np.where(rng.random(B) < 0.7, -1, rng.integers(0, m.V, B)).astype(np.int32)
+    g = gpu_decode(m, x, start, prev0, lam, lengths)
+    assert_same(g, o.ctc_decode(x, start, prev=prev0, lam=lam, lengths=lengths))
+    # the single-chain kernel (no frame records): same emissions, states, prev
+    xd = torch.from_numpy(x).cuda()
+    st, pv = torch.from_numpy(start.copy()).cuda(), torch.from_numpy(prev0.copy()).cuda()
+    _, em, el = m.ctc_greedy_decode(xd, st, pv, lam=lam, lengths=torch.from_numpy(lengths).cuda(),
+                                    want_frames=False)
+    torch.cuda.synchronize()
+    el = el.cpu().numpy()
+    assert np.array_equal(el, g[2]) and np.array_equal(st.cpu().numpy(), g[3]) and np.array_equal(pv.cpu().numpy(), g[4])
+    emn = em.cpu().numpy()
+    for r in range(B):
+        assert np.array_equal(emn[r, : el[r]], g[1][r, : el[r]])
+
+
+def T_(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev())
+
+
+@pytest.mark.parametrize("kernel", [ng.ADVANCE_AUTO, ng.ADVANCE_WARP])
+def test_segmented_decode_edge_cases(pairs, kernel):
+    """Segments on a small LM (tiny path with AUTO, unpacked global path with WARP):
+    an invalid start state, all-NaN frames (no column selected), ties, blank column 0."""
+    m, o, f = pairs["five48"]
+    B, T = 40, 260
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((B, T, o.V + 1)).astype(np.float32)
+    x[:, :, 0] += 1.0
+    x[3, 70:75] = np.nan          # frames selecting nothing, inside a segment
+    x[4, 64] = np.nan             # on a segment boundary
+    x[5, ::7] = np.round(x[5, ::7] * 2) / 2  # ties
+    start = synth.uniform_states(o.num_states, B, seed=10)
+    start[6] = o.num_states + 5   # invalid
+    prev0 = np.full(B, -1, np.int32)
+    lengths = np.full(B, T, np.int32)
+    m.set_advance_kernel(kernel)
+    try:
+        g = gpu_decode(m, x, start, prev0, 0.8, lengths, blank=0)
+        assert m.check() == 6
+    finally:
+        m.set_advance_kernel(ng.ADVANCE_AUTO)
+    ok = np.ones(B, bool)
+    ok[[3, 4, 6]] = False  # NaN frames are unspecified (R15): rows 3, 4 are checked against the single chain
+    ref = o.ctc_decode(x[ok], start[ok], prev=prev0[ok], lam=0.8, lengths=lengths[ok], blank_id=0)
+    assert np.array_equal(g[0][ok], ref[0]) and np.array_equal(g[2][ok], ref[2])
+    assert np.array_equal(g[3][ok], ref[3]) and np.array_equal(g[4][ok], ref[4])
+    assert (g[0][6] == -1).all() and g[2][6] == 0 and g[3][6] == start[6]
+    # every row, NaN frames included: the segments agree with the single-chain kernel
+    m.set_advance_kernel(kernel)
+    try:
+        st, pv = T_(start), T_(prev0)
+        _, em, el = m.ctc_greedy_decode(T_(x), st, pv, lam=0.8, blank_id=0, lengths=T_(lengths), want_frames=False)
+        torch.cuda.synchronize()
+    finally:
+        m.set_advance_kernel(ng.ADVANCE_AUTO)
+    el = el.cpu().numpy()
+    assert np.array_equal(el, g[2]) and np.array_equal(st.cpu().numpy(), g[3]) and np.array_equal(pv.cpu().numpy(), g[4])
+    emn = em.cpu().numpy()
+    for r in range(B):
+        assert np.array_equal(emn[r, : el[r]], g[1][r, : el[r]])
+    assert (g[0][3, 70:75] == -1).all() and g[0][4, 64] == -1  # a NaN frame selects nothing
