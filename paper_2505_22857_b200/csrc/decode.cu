@@ -152,7 +152,8 @@ __global__ void __launch_bounds__(64 * kDecodeMaxRows, 1)
     uint32_t phase = 0;  // parity of the slot's previous use
     for (int32_t t = 0; t < run; ++t) {
       if (t >= depth) mbar_wait(empty + slot, phase);  // the consumer is done with frame t - depth
-      issue_frame(lrow0 + (size_t)t * frame_stride, ncols, ring + (size_t)slot * lstride, full + slot, pol);
+      issue_frame_cover(lrow0 + (size_t)t * frame_stride, ncols, ring + (size_t)slot * lstride, full + slot, pol, logits,
+                        logits + (size_t)(B - 1) * row_stride + (size_t)(T - 1) * frame_stride + ncols);
       if (++slot == depth) { slot = 0; if (t >= depth) phase ^= 1u; }
     }
     cp_async_settle();
@@ -422,7 +423,8 @@ __global__ void __launch_bounds__(32 * (2 + kSumWarps), 2)
     for (int32_t t = 0; t < run; ++t) {
       const int32_t slot = t % kRing2;
       if (t >= kRing2) mbar_wait(empty + slot, (uint32_t)(t / kRing2 - 1) & 1u);
-      issue_frame(lrow0 + (size_t)t * frame_stride, ncols, ring + (size_t)slot * lstride, full + slot, pol);
+      issue_frame_cover(lrow0 + (size_t)t * frame_stride, ncols, ring + (size_t)slot * lstride, full + slot, pol, logits,
+                        logits + (size_t)(B - 1) * row_stride + (size_t)(T - 1) * frame_stride + ncols);
     }
     cp_async_settle();
     return;

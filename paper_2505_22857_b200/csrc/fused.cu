@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(256, 1)
   if (kEarly) {  // the caller guarantees no running kernel writes the logits (NGPULM_STEP_LOGITS_READY)
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));  // read once
-    issue_frame(lrow, ncols, lbuf, lbar, pol);
+    issue_frame_cover(lrow, ncols, lbuf, lbar, pol, logits, logits + (size_t)(B - 1) * row_stride + ncols);
   }
   // Speculative build (as advance_warp_kernel): the LM row from the state read
   // before griddepcontrol.wait, re-checked after it. Inputs (prev, active, ILM
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(256, 1)
   if (on && !kEarly) {  // the logits (an input: after the wait), copied while the state is checked
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));  // read once
-    issue_frame(lrow, ncols, lbuf, lbar, pol);
+    issue_frame_cover(lrow, ncols, lbuf, lbar, pol, logits, logits + (size_t)(B - 1) * row_stride + ncols);
   }
   const float* lb = lbuf + (reinterpret_cast<uintptr_t>(lrow) & 15) / 4;  // column c at lb[c]
   int32_t dsel = -1;  // TDT duration (loop mode with durations), else -1
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(256, 1)
     if (on) {
       uint64_t pol;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-      issue_frame(lrow, ncols, lbuf, lbar, pol);
+      issue_frame_cover(lrow, ncols, lbuf, lbar, pol, logits, logits + (size_t)(B - 1) * row_stride + ncols);
       mbar_wait(lbar, 0);
       cp_async_settle();
 #pragma unroll
@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(256, 1)
   auto begin_logits = [&]() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    issue_frame(lrow, ncols, lbuf, lbar, pol);
+    issue_frame_cover(lrow, ncols, lbuf, lbar, pol, logits, logits + (size_t)(B - 1) * row_stride + ncols);
     started = true;
   };
   const Row r = warp_row<kTable>(m, states + row, s, lv, nslots, begin_logits);

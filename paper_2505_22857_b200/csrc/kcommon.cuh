@@ -796,7 +796,7 @@ constexpr int kMaxColsPerLane = 33;  // (1024 + 1 + 31) / 32
 
 // per warp: row_s | row_n | levels | 2 mbarriers | logits (V+1 floats + 16-byte slack)
 __host__ __device__ constexpr size_t fslice_bytes(int32_t V, int32_t order) {
-  return wslice_bytes(V, order, 0) + align16((size_t)(V + 1) * 4 + 16);
+  return wslice_bytes(V, order, 0) + align16((size_t)(V + 1) * 4 + 32);  // (+ a 16-byte-aligned cover's slack)
 }
 
 // Issue frame row `lrow` (ncols floats) into `buf` (column c lands at

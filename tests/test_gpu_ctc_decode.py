@@ -216,3 +216,4 @@ def test_segmented_decode_edge_cases(pairs, kernel):
     for r in range(B):
         assert np.array_equal(emn[r, : el[r]], g[1][r, : el[r]])
     assert (g[0][3, 70:75] == -1).all() and g[0][4, 64] == -1  # a NaN frame selects nothing
+    assert m.check() == 6  # (the single-chain run set the sticky word again; read and clear it)
