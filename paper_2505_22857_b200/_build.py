@@ -25,10 +25,11 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_variant(name: str, defines: list[str]) -> str:
-    """Tuning variants (tools/): same sources, other compile-time constants."""
+def build_variant(name: str, defines: list[str], only: list[str] | None = None) -> str:
+    """Tuning variants (tools/): same sources, other compile-time constants. `only`: the
+    sources the defines affect; the other objects are the main build's (build() first)."""
     out = os.path.join(LIBDIR, f"libngpulm_{name}.so")
-    _compile_link(out, [f"-D{d}" for d in defines], os.path.join(HERE, "build", name))
+    _compile_link(out, [f"-D{d}" for d in defines], os.path.join(HERE, "build", name), only=only)
     return out
 
 
@@ -42,7 +43,8 @@ def build_phase_timing() -> str:
     return out
 
 
-def _compile_link(out: str, extra: list[str], objdir: str, verbose: bool = False) -> None:
+def _compile_link(out: str, extra: list[str], objdir: str, verbose: bool = False,
+                  only: list[str] | None = None) -> None:
     """Each source compiles to an object in parallel, then one nvcc link."""
     from concurrent.futures import ThreadPoolExecutor
     os.makedirs(objdir, exist_ok=True)
@@ -50,6 +52,8 @@ def _compile_link(out: str, extra: list[str], objdir: str, verbose: bool = False
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        if only is not None and src not in only:
+            return os.path.join(HERE, "build", "main", os.path.splitext(src)[0] + ".o")
         cmd = [NVCC, *ARCH, *cflags, "-c", "-o", obj, os.path.join(CSRC, src)]
         if verbose and src.endswith(".cu"):
             cmd.insert(1, "-Xptxas=-v")

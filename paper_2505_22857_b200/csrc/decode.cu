@@ -717,8 +717,8 @@ __global__ void __launch_bounds__(32 * (2 + kSumWarps), 2)
 // after every frame until the end of pass 2 overwrites it with the emissions.
 // One warp per chain with its own TMA ring (lane 0 refills a slot right after
 // the warp has read it), so a segment costs one warp's registers.
-#ifndef NGPULM_SEG_CHAINS
-#define NGPULM_SEG_CHAINS 1184  // chains (rows x segments) one launch holds at once (8 one-warp chains per SM)
+#ifndef NGPULM_SEG_CTAS
+#define NGPULM_SEG_CTAS 2  // resident CTAs per SM (kSegRows chains each): the chains one launch holds at once
 #endif
 #ifndef NGPULM_SEG_MIN_FRAMES
 #define NGPULM_SEG_MIN_FRAMES 64  // fewest frames per segment
@@ -726,21 +726,92 @@ __global__ void __launch_bounds__(32 * (2 + kSumWarps), 2)
 #ifndef NGPULM_SEG_EXPT
 #define NGPULM_SEG_EXPT 0  // timing experiments only (tools/): bit 0 no proxy fence, bit 1 no pass-1 records
 #endif
+#ifndef NGPULM_SEG_RW_REGS
+#define NGPULM_SEG_RW_REGS 0  // root weights: 1 in registers (33 per lane), 0 read from the CTA's copy
+#endif
 #ifndef NGPULM_SEG_RING
-#define NGPULM_SEG_RING 4
+#define NGPULM_SEG_RING 2
 #endif
 constexpr int kSegRing = NGPULM_SEG_RING;  // frames in flight per chain
 constexpr int kSegWarm = 16;  // warm-up frames before a segment >= 1
-constexpr int kSegRows = 4;   // chains (warps) per CTA, sharing the root-level copy: 2 CTAs = 8 chains per SM
-                              // (2 chains per CTA: 3 CTAs fit the shared memory, 6 chains, two waves at B=256)
+#ifndef NGPULM_SEG_ROWS
+#define NGPULM_SEG_ROWS 4
+#endif
+constexpr int kSegRows = NGPULM_SEG_ROWS;  // chains (warps) per CTA, sharing the root-level copy
+constexpr int kSegCtas = NGPULM_SEG_CTAS;
 
+// A chain's row: arc-level entries only, tagged with the rebuild that wrote them
+// ({acc_boff + weight, generation} per token, next states apart); a token without
+// an entry of the current generation takes the root level (acc_root + root
+// weight from the lane's registers, root target from the CTA's copy), so a
+// rebuild writes only the arcs, not the V root entries.
+__host__ __device__ constexpr size_t grow_bytes(int32_t V) { return align16((size_t)(V + 1) * 8); }
 __host__ __device__ constexpr size_t sslice_bytes(int32_t V, int32_t order) {
-  return wslice_bytes(V, order, 0) + kSegRing * 8 + (size_t)kSegRing * lbuf_bytes(V);
+  return grow_bytes(V) + wrow_bytes(V) + levels_bytes(order) + 16 + align16(kSegRing * 8) +
+         (size_t)kSegRing * lbuf_bytes(V);
 }
-// [tiny model copy] | root_w | root_to | cbar | R slices (row | levels | 2 bars | full[kSegRing] | ring)
+// [tiny model copy] | root_w | root_to | cbar | R slices (row_g | row_n | levels | 2 bars | full[kSegRing] | ring)
 __host__ __device__ constexpr size_t scta_smem(int32_t V, int32_t order, int R) {
   return 2 * align16((size_t)V * 4) + 16 + (size_t)R * sslice_bytes(V, order);
 }
+
+// write_window with generation-tagged score entries (row_g) and next states (row_n).
+template <int kW, bool kPacked>
+__device__ __forceinline__ void write_window_gen(float2* row_g, int32_t* row_n, const Window<kW, kPacked>& a,
+                                                 int32_t k0, int32_t nslots, int32_t pk_bits, int32_t gen) {
+  const uint32_t tmask = (1u << pk_bits) - 1u;
+  const float gtag = __int_as_float(gen);
+#pragma unroll
+  for (int g = 0; g < kW; g += 8) {
+    if (g > 0 && k0 + g >= nslots) break;
+#pragma unroll
+    for (int u = g; u < g + 8; ++u) {
+      if (u > g && k0 + u >= nslots) break;  // (uniform) past the row's last slot: nothing to write
+      if (u > 0) __syncwarp();  // slots in level order: a lower order is done before a higher one
+      const int32_t x[4] = {a.tok[u].x, a.tok[u].y, a.tok[u].z, a.tok[u].w};
+      const float ww[4] = {a.w[u].x, a.w[u].y, a.w[u].z, a.w[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int32_t tk, nx;
+        if (kPacked) {
+          tk = (int32_t)((uint32_t)x[j] & tmask);
+          nx = (int32_t)((uint32_t)x[j] >> pk_bits);
+        } else {
+          const int32_t t4[4] = {a.to[u].x, a.to[u].y, a.to[u].z, a.to[u].w};
+          tk = x[j];
+          nx = t4[j];
+        }
+        row_g[tk] = make_float2(__fadd_rn(a.acc[u], ww[j]), gtag);  // acc_boff + arc_weights (Alg. 1 line 74)
+        row_n[tk] = nx;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// The arc levels of state `st` into row_g / row_n with tag `gen` (Algorithm 1's
+// levels 1..N-1; the root level stays implicit). Returns the row scalars.
+template <bool kPacked, bool kTiny>
+__device__ __forceinline__ Row build_row_gen(const DevModel& m, const WSlice& s, float2* row_g, int32_t st,
+                                             int32_t gen) {
+  constexpr int kW = 8;
+  WLevel lv;
+  int32_t nslots;
+  const Row r = warp_row_src<true, NoOp, ValState, kTiny>(m, ValState{st}, s, lv, nslots);
+  if (r.bad) return r;
+  Window<kW, kPacked> a;
+  load_window<kW, kPacked, kTiny>(m, s, lv, r.nlev, 0, nslots, a);
+  for (int32_t k0 = 0; k0 < nslots;) {
+    write_window_gen<kW, kPacked>(row_g, s.row_n, a, k0, nslots, m.pk_bits, gen);
+    k0 += kW;
+    if (k0 < nslots) load_window<kW, kPacked, kTiny>(m, s, lv, r.nlev, k0, nslots, a);
+  }
+  __syncwarp();
+  return r;
+}
+
+// the first frame of segment k: segment 0 is [0, L0), segment k >= 1 [L0 + (k - 1) L, L0 + k L)
+__device__ __forceinline__ int32_t seg_begin(int32_t k, int32_t L0, int32_t L) { return k == 0 ? 0 : L0 + (k - 1) * L; }
 
 // The end of pass 2, per row (one warp): the emissions from the decisions (CTC
 // collapse: a selection that is neither blank nor prev), the final state and
@@ -764,9 +835,19 @@ __device__ __forceinline__ void compact_row(int32_t row, int32_t T, int32_t len,
   int32_t pc = prev[row], count = 0;
   __syncwarp();
   const uint32_t lt = (1u << lane) - 1u;
-  for (int32_t b = 0; b < len; b += 32) {
-    const int32_t t = b + lane;
-    const int32_t f = t < len ? fo[t] : -1;
+  constexpr int kU = 16;  // 32-frame blocks whose decisions are loaded at once (one memory latency per 512 frames)
+  for (int32_t b0 = 0; b0 < len; b0 += 32 * kU) {
+    int32_t fr[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int32_t t = b0 + 32 * u + lane;
+      fr[u] = t < len ? fo[t] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+    const int32_t b = b0 + 32 * u;
+    if (b >= len) break;
+    const int32_t f = fr[u];
     const uint32_t valid = __ballot_sync(kFull, f >= 0);
     const uint32_t before = valid & lt;  // prev before frame t: the last selecting frame before it
     const int32_t fp = __shfl_sync(kFull, f, before ? 31 - __clz(before) : 0);
@@ -779,6 +860,7 @@ __device__ __forceinline__ void compact_row(int32_t row, int32_t T, int32_t len,
       const int32_t fl = __shfl_sync(kFull, f, 31 - __clz(valid));
       pc = fl == sp ? -1 : fl;
     }
+    }
   }
   for (int32_t t = len + lane; t < T; t += 32) fo[t] = -1;
   __syncwarp();
@@ -789,10 +871,13 @@ __device__ __forceinline__ void compact_row(int32_t row, int32_t T, int32_t len,
   }
 }
 
+// registers: as many as kSegCtas resident CTAs leave (65536 per SM, allocated in units of 8 per thread)
+constexpr int kSegMaxReg = (65536 / (32 * kSegRows * kSegCtas)) / 8 * 8 > 255 ? 255
+                                                                               : (65536 / (32 * kSegRows * kSegCtas)) / 8 * 8;
 template <bool kTable, bool kPacked, bool kTiny, bool kFix>
-__global__ void __launch_bounds__(32 * kSegRows, 8 / kSegRows)
+__global__ void __maxnreg__(kSegMaxReg)
     ctc_seg_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int64_t frame_stride,
-                   int32_t B, int32_t T, int32_t K, int32_t L, const int32_t* __restrict__ lengths,
+                   int32_t B, int32_t T, int32_t K, int32_t L0, int32_t L, const int32_t* __restrict__ lengths,
                    int32_t* __restrict__ states, int32_t* __restrict__ prev, float lambda, int32_t sp,
                    int32_t* __restrict__ frames_out, int32_t* __restrict__ rec, int32_t* __restrict__ emit_len) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -803,15 +888,32 @@ __global__ void __launch_bounds__(32 * kSegRows, 8 / kSegRows)
   float* root_w = reinterpret_cast<float*>(sm0);
   int32_t* root_to = reinterpret_cast<int32_t*>(sm0 + rb);
   uint64_t* cbar = reinterpret_cast<uint64_t*>(sm0 + 2 * rb);
+  static_assert(kTable, "the segment decode reads the chain table");
   unsigned char* base = sm0 + 2 * rb + 16 + (size_t)w * sslice_bytes(V, m.order);
-  WSlice s = wcarve(base, V, m.order, 0);
+  float2* row_g = reinterpret_cast<float2*>(base);
+  WSlice s;
+  {
+    unsigned char* lp = base + grow_bytes(V) + wrow_bytes(V);
+    int32_t* l = reinterpret_cast<int32_t*>(lp);
+    const int32_t Lc = level_cap(m.order);
+    s.row_s = nullptr;
+    s.row_n = reinterpret_cast<int32_t*>(base + grow_bytes(V));
+    s.beg = l;
+    s.pre = l + Lc;
+    s.acc = reinterpret_cast<float*>(l + 2 * Lc + 1);
+    s.bar = reinterpret_cast<uint64_t*>(lp + levels_bytes(m.order));
+    s.abar = s.bar + 1;
+    s.st_q = nullptr;
+    s.chain_s = nullptr;
+  }
   if (kTiny) {
     s.chain_s = reinterpret_cast<const int4*>(smem);
     s.st_q = reinterpret_cast<int4*>(smem + align16((size_t)m.tiny_chain_bytes));
   }
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + wslice_bytes(V, m.order, 0));
-  float* ring = reinterpret_cast<float*>(base + wslice_bytes(V, m.order, 0) + kSegRing * 8);
+  uint64_t* full = s.bar + 2;
+  float* ring = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(full) + align16(kSegRing * 8));
   const size_t lstride = lbuf_bytes(V) / 4;
+  for (int32_t c = lane; c < V; c += 32) row_g[c] = make_float2(0.f, __int_as_float(-1));  // no generation yet
   pdl_trigger();
   if (threadIdx.x == 0) {  // the root level (immutable model data: before the wait)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(cbar)) : "memory");
@@ -842,7 +944,7 @@ __global__ void __launch_bounds__(32 * kSegRows, 8 / kSegRows)
   int32_t len = T;
   if (lengths) len = min(T, max(0, __ldg(&lengths[row])));
   const int32_t st0 = states[row];  // (pass 2 rewrites it last, in compact_row)
-  if (!kFix && (st0 < 0 || st0 >= m.S || k0 * L >= len)) { cta_exit(); return; }
+  if (!kFix && (st0 < 0 || st0 >= m.S || seg_begin(k0, L0, L) >= len)) { cta_exit(); return; }
   if (kFix && (st0 < 0 || st0 >= m.S)) {  // an invalid row decides nothing (as ctc_decode_kernel)
     compact_row(row, T, len, st0, sp, frames_out, rec, states, prev, emit_len, m.bad_row, true);
     cta_exit();
@@ -888,20 +990,50 @@ __global__ void __launch_bounds__(32 * kSegRows, 8 / kSegRows)
 #else
 #define SSTAMP(i) do { } while (0)
 #endif
-  float lm[kMaxColsPerLane];
-  int32_t row_state = -1;
+  float lm[kMaxColsPerLane];  // the row's LM scores
+#if NGPULM_SEG_RW_REGS
+  float rw[kMaxColsPerLane];  // the root weights of the same columns
+#pragma unroll
+  for (int j = 0; j < kMaxColsPerLane; ++j) {
+    const int32_t col = lane + 32 * j;
+    rw[j] = (col < ncols && col != sp) ? root_w[col - (col > sp)] : 0.f;
+  }
+#define NGPULM_RW(j, tk) rw[j]
+#else
+#define NGPULM_RW(j, tk) root_w[tk]
+#endif
+  int32_t row_state = -1, gen = 0;
   auto ensure_row = [&](int32_t st) {
     if (row_state == st) return;
 #ifdef NGPULM_PHASE_TIMING
     ck[6] += 1;
 #endif
-    build_row_warp<kTable, kPacked, NoStamp, kTiny>(m, s, root_w, root_to, st);
+    ++gen;
+    const Row r = build_row_gen<kPacked, kTiny>(m, s, row_g, st, gen);
+    // branch-free, loads in groups of 11 columns (lane i: columns i + 32 j); out-of-row columns read token V-1
+    static_assert(kMaxColsPerLane % 11 == 0, "groups of 11 columns");
 #pragma unroll
-    for (int j = 0; j < kMaxColsPerLane; ++j) {
-      const int32_t col = lane + 32 * j;
-      lm[j] = (col < ncols && col != sp) ? s.row_s[col - (col > sp)] : 0.f;  // blank: 0 (fused value = asr)
+    for (int g = 0; g < kMaxColsPerLane; g += 11) {
+      float2 e[11];
+      float rv[11];
+#pragma unroll
+      for (int u = 0; u < 11; ++u) {
+        const int32_t col = lane + 32 * (g + u);
+        const int32_t tk = min(col - (col > sp), V - 1);
+        e[u] = row_g[tk];
+        rv[u] = NGPULM_RW(g + u, tk);
+      }
+#pragma unroll
+      for (int u = 0; u < 11; ++u) {
+        const int32_t col = lane + 32 * (g + u);
+        const float v = __float_as_int(e[u].y) == gen ? e[u].x : __fadd_rn(r.acc_root, rv[u]);  // arc, else root
+        lm[g + u] = (col < ncols && col != sp) ? v : 0.f;  // blank: 0 (fused value = asr)
+      }
     }
     row_state = st;
+  };
+  auto next_state = [&](int32_t tk) {  // the state after token tk from the row's state
+    return __float_as_int(row_g[tk].y) == gen ? s.row_n[tk] : root_to[tk];
   };
   // the fused CTC decision of one frame (ctc_decode_kernel's, R13, R14, R17, R19); the frame's
   // slot is handed back (and refilled) as soon as its columns are in registers
@@ -955,13 +1087,13 @@ __global__ void __launch_bounds__(32 * kSegRows, 8 / kSegRows)
     if (bc == sp) {
       pc = -1;
     } else if (bc != pc) {  // an emission: LM advance
-      st = s.row_n[bc < sp ? bc : bc - 1];
+      st = next_state(bc < sp ? bc : bc - 1);
       pc = bc;
     }
     return bc;
   };
   if (!kFix) {  // ---- pass 1: segment k0
-    const int32_t t0 = k0 * L, t1 = min(t0 + L, len);
+    const int32_t t0 = seg_begin(k0, L0, L), t1 = min(seg_begin(k0 + 1, L0, L), len);
     const int32_t tb = k0 == 0 ? 0 : max(0, t0 - kSegWarm);
     int32_t st = k0 == 0 ? st0 : 0, pc = k0 == 0 ? __ldg(&prev[row]) : -1;
     next_t = tb;
@@ -983,30 +1115,52 @@ __global__ void __launch_bounds__(32 * kSegRows, 8 / kSegRows)
       SSTAMP(4);
     }
   } else {  // ---- pass 2: the segments of the row in order, from the true boundary state
+    const int32_t pc_row = __ldg(&prev[row]);
     for (int32_t k = 1; k < K; ++k) {
-      const int32_t t0 = k * L, t1 = min(t0 + L, len);
+      const int32_t t0 = seg_begin(k, L0, L), t1 = min(seg_begin(k + 1, L0, L), len);
       if (t0 >= len) break;
-      int32_t st = ro[t0 - 1], pc = __ldg(&prev[row]);
+      // one round of loads: the boundary state, the 32 frames before t0 (prev) and pass 1's
+      // records of the first 32 frames of the segment
+      int32_t st = ro[t0 - 1], pc = pc_row;
+      const int32_t fb = t0 - 1 - lane >= 0 ? fo[t0 - 1 - lane] : -1;
+      const int32_t f_pre = t0 + lane < t1 ? fo[t0 + lane] : -1, s_pre = t0 + lane < t1 ? ro[t0 + lane] : -1;
       // prev before t0: the last frame before t0 that selected a column (blank -> -1)
-      for (int32_t b = t0 - 1; b >= 0; b -= 32) {
-        const int32_t t = b - lane;
-        const int32_t f = t >= 0 ? fo[t] : -1;
-        const uint32_t hit = __ballot_sync(kFull, f >= 0);
-        if (hit) {
-          const int32_t fl = __shfl_sync(kFull, f, __ffs(hit) - 1);
-          pc = fl == sp ? -1 : fl;
-          break;
+      uint32_t hit = __ballot_sync(kFull, fb >= 0);
+      if (hit) {
+        const int32_t fl = __shfl_sync(kFull, fb, __ffs(hit) - 1);
+        pc = fl == sp ? -1 : fl;
+      } else {
+        for (int32_t b = t0 - 33; b >= 0; b -= 32) {
+          const int32_t t = b - lane;
+          const int32_t f = t >= 0 ? fo[t] : -1;
+          hit = __ballot_sync(kFull, f >= 0);
+          if (hit) {
+            const int32_t fl = __shfl_sync(kFull, f, __ffs(hit) - 1);
+            pc = fl == sp ? -1 : fl;
+            break;
+          }
         }
       }
+      // frames still in the ring from the previous segment's meeting point: their slots are
+      // taken back after this segment's row is built (they have landed by then)
+      const uint32_t stale_end = issued;
       next_t = t0;
       stop_t = t1;
+      issue_upto();
+      ensure_row(st);
+      while (consumed < stale_end) {
+        take(0);
+        give();
+      }
       issue_upto();
       for (int32_t t = t0; t < t1; ++t) {
         const int32_t tok = step(t, st, pc);
 #ifdef NGPULM_PHASE_TIMING
         if (lane == 0 && row < 4096) g_phase[(8192 + row) * 16 + k] += 1;  // fix-up frames of segment k
 #endif
-        const int32_t f_rec = fo[t], s_rec = ro[t];
+        const int32_t i = t - t0;
+        const int32_t f_rec = i < 32 ? __shfl_sync(kFull, f_pre, i) : fo[t];
+        const int32_t s_rec = i < 32 ? __shfl_sync(kFull, s_pre, i) : ro[t];
         const bool met = tok >= 0 && tok == f_rec && st == s_rec;  // same (state, prev) from here on
         if (!met && lane == 0) {
           fo[t] = tok;
@@ -1015,13 +1169,13 @@ __global__ void __launch_bounds__(32 * kSegRows, 8 / kSegRows)
         __syncwarp();
         if (met) break;
       }
-      while (consumed < issued) {  // frames issued past the meeting point: let them land
-        take(0);
-        give();
-      }
     }
     __syncwarp();
     compact_row(row, T, len, st0, sp, frames_out, rec, states, prev, emit_len, m.bad_row, false);
+    while (consumed < issued) {  // frames issued past the last meeting point: let them land
+      take(0);
+      give();
+    }
   }
   cp_async_settle();  // every edge cp.async of this warp has landed (the ring waits already implied it)
 #ifdef NGPULM_PHASE_TIMING
@@ -1029,6 +1183,7 @@ __global__ void __launch_bounds__(32 * kSegRows, 8 / kSegRows)
     for (int i = 0; i < 7; ++i) g_phase[chain * 16 + i] = (unsigned long long)ck[i];
 #endif
 #undef SSTAMP
+#undef NGPULM_RW
 }
 
 }  // namespace
@@ -1057,19 +1212,27 @@ int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride
 #undef NGPULM_DECODE2
   }
   // segment-parallel exact decode: table mode, both record buffers given, enough frames per segment
-  int K = (int)(NGPULM_SEG_CHAINS / (B > 0 ? B : 1));
+  // (148 SMs x kSegCtas resident CTAs x kSegRows chains: one wave of chains)
+  int K = 148 * kSegCtas * kSegRows / B;
   K = K > 8 ? 8 : K;
   if (K > T / NGPULM_SEG_MIN_FRAMES) K = T / NGPULM_SEG_MIN_FRAMES;
-  if (table && frames_out && emit_out && K >= 2 && NGPULM_SEG_CHAINS > 0) {
-    const int32_t L = (T + K - 1) / K;
-    const bool tiny = pk && m.tiny_chain_bytes > 0;
-    const size_t sm = scta_smem(m.V, m.order, kSegRows) + (tiny ? tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) : 0);
-    if (sm <= 227 * 1024) {
+  if (table && frames_out && emit_out && K >= 2 && kSegCtas > 0) {
+    // every chain the same number of frames: segment 0 (no warm-up) kSegWarm frames longer
+    const int32_t L = (T - kSegWarm + K - 1) / K, L0 = T - (K - 1) * L;
+    // the tiny-LM copy only where it keeps kSegCtas CTAs per SM: one CTA per SM halves the chains
+    // in flight, which costs more than the shared-memory model saves (B=256: 0.38 vs 0.26 ms)
+    const size_t sm0 = scta_smem(m.V, m.order, kSegRows);
+    const bool tiny = pk && m.tiny_chain_bytes > 0 &&
+                      kSegCtas * (sm0 + tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) + 1024) <= 228 * 1024;
+    const size_t sm = sm0 + (tiny ? tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) : 0);
+    if (kSegCtas * (sm + 1024) <= 228 * 1024) {
       const dim3 b1(32 * kSegRows), g1((B * K + kSegRows - 1) / kSegRows), g2((B + kSegRows - 1) / kSegRows);
       int e;
 #define NGPULM_SEG(P, TI, FIX, G)                                                                                   \
-  launch(ctc_seg_kernel<true, P, TI, FIX>, G, b1, sm, st, m, logits, row_stride, frame_stride, B, T, K, L, lengths,   \
-         states, prev, lambda, blank, frames_out, emit_out, emit_len)
+  ((e = ensure_max_carveout((const void*)ctc_seg_kernel<true, P, TI, FIX>)) != 0                                     \
+       ? e                                                                                                          \
+       : launch(ctc_seg_kernel<true, P, TI, FIX>, G, b1, sm, st, m, logits, row_stride, frame_stride, B, T, K, L0, L, \
+                lengths, states, prev, lambda, blank, frames_out, emit_out, emit_len))
       if (tiny) e = NGPULM_SEG(true, true, false, g1);
       else if (pk) e = NGPULM_SEG(true, false, false, g1);
       else e = NGPULM_SEG(false, false, false, g1);

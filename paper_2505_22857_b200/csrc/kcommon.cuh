@@ -1001,6 +1001,23 @@ inline int ensure_smem(const void* kern, size_t smem) {
   return 0;
 }
 
+// Kernels whose residency is sized by several CTAs' shared memory per SM ask
+// for the largest shared-memory carveout once per (device, kernel).
+inline int ensure_max_carveout(const void* kern) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, bool> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  bool& d = done[{dev, kern}];
+  if (d) return 0;
+  const cudaError_t e =
+      cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return (int)e;
+  d = true;
+  return 0;
+}
+
 template <typename... KArgs, typename... Args>
 int launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
   if (smem > 48 * 1024) {

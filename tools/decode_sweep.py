@@ -12,6 +12,13 @@ ts = []
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for _ in range(5):
     st.zero_(); pv.fill_(-1)
-    e0.record(); m.ctc_greedy_decode(x, st, pv, lam=0.3); e1.record(); torch.cuda.synchronize()
+    e0.record(); fr, em, el = m.ctc_greedy_decode(x, st, pv, lam=0.3); e1.record(); torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
-print(f"decode ms: {statistics.median(ts[1:]):.4f}", flush=True)
+# outputs digest (variants must agree bit for bit)
+import hashlib
+h = hashlib.sha1()
+for t in (fr, el, st, pv):
+    h.update(t.cpu().numpy().tobytes())
+for b in range(B):
+    h.update(em[b, :int(el[b])].cpu().numpy().tobytes())
+print(f"decode ms: {statistics.median(ts[1:]):.4f} digest {h.hexdigest()[:12]}", flush=True)
