@@ -789,16 +789,51 @@ __device__ __forceinline__ void write_window_gen(float2* row_g, int32_t* row_n, 
   __syncwarp();
 }
 
-// The arc levels of state `st` into row_g / row_n with tag `gen` (Algorithm 1's
-// levels 1..N-1; the root level stays implicit). Returns the row scalars.
+// The chain record of state `st` (chain table row: lane l < chain_slots holds
+// slot l), loaded by an ordered (volatile) access so that it is in flight while
+// the caller does other work before build_row_gen consumes it.
+template <bool kTiny>
+__device__ __forceinline__ int4 record_issue(const DevModel& m, const WSlice& s, int32_t st) {
+  const int lane = threadIdx.x & 31;
+  int4 x = make_int4(0, 0, 0, 0);
+  if (st >= 0 && st < m.S && lane < m.chain_slots) {
+    if (kTiny) {
+      x = s.chain_s[(size_t)st * m.chain_slots + lane];
+    } else {
+      const int4* p = reinterpret_cast<const int4*>(m.chain) + (size_t)st * m.chain_slots + lane;
+      asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(p));
+    }
+  }
+  return x;
+}
+
+// The arc levels of state `st` (record x from record_issue) into row_g / row_n
+// with tag `gen` (Algorithm 1's levels 1..N-1; the root level stays implicit).
+// Returns the row scalars (warp_row_src's, table mode).
 template <bool kPacked, bool kTiny>
 __device__ __forceinline__ Row build_row_gen(const DevModel& m, const WSlice& s, float2* row_g, int32_t st,
-                                             int32_t gen) {
+                                             const int4 x, int32_t gen) {
   constexpr int kW = 8;
+  const int lane = threadIdx.x & 31;
   WLevel lv;
-  int32_t nslots;
-  const Row r = warp_row_src<true, NoOp, ValState, kTiny>(m, ValState{st}, s, lv, nslots);
+  lv.beg = 0; lv.qbase = 0; lv.info = 0; lv.eslot = INT_MAX; lv.acc = 0.f;
+  Row r;
+  r.state = st;
+  r.bad = st < 0 || st >= m.S;
+  r.nlev = 0; r.total = 0; r.acc_root = 0.f; r.fin = 0.f;
   if (r.bad) return r;
+  r.nlev = __shfl_sync(kFull, x.x, 0);
+  r.acc_root = __int_as_float(__shfl_sync(kFull, x.y, 0));
+  r.fin = __int_as_float(__shfl_sync(kFull, x.z, 0));
+  r.total = __shfl_sync(kFull, x.w, 0);
+  if (lane >= 1 && lane <= r.nlev) {
+    lv.beg = x.x;
+    lv.acc = __int_as_float(x.z);
+    lv.info = x.w;
+    lv.eslot = (lv.info >> 16) + (((lv.info & 0xffff) + 31) >> 5);
+  }
+  lv.qbase = lv.beg >> 2;
+  const int32_t nslots = r.nlev > 0 ? __shfl_sync(kFull, lv.eslot, 1) : 0;
   Window<kW, kPacked> a;
   load_window<kW, kPacked, kTiny>(m, s, lv, r.nlev, 0, nslots, a);
   for (int32_t k0 = 0; k0 < nslots;) {
@@ -1003,13 +1038,12 @@ __global__ void __maxnreg__(kSegMaxReg)
 #define NGPULM_RW(j, tk) root_w[tk]
 #endif
   int32_t row_state = -1, gen = 0;
-  auto ensure_row = [&](int32_t st) {
-    if (row_state == st) return;
+  auto finish_row = [&](int32_t st, const int4 x) {  // the row of st from its record x
 #ifdef NGPULM_PHASE_TIMING
     ck[6] += 1;
 #endif
     ++gen;
-    const Row r = build_row_gen<kPacked, kTiny>(m, s, row_g, st, gen);
+    const Row r = build_row_gen<kPacked, kTiny>(m, s, row_g, st, x, gen);
     // branch-free, loads in groups of 11 columns (lane i: columns i + 32 j); out-of-row columns read token V-1
     static_assert(kMaxColsPerLane % 11 == 0, "groups of 11 columns");
 #pragma unroll
@@ -1032,14 +1066,17 @@ __global__ void __maxnreg__(kSegMaxReg)
     }
     row_state = st;
   };
+  auto ensure_row = [&](int32_t st) {
+    if (row_state != st) finish_row(st, record_issue<kTiny>(m, s, st));
+  };
   auto next_state = [&](int32_t tk) {  // the state after token tk from the row's state
     return __float_as_int(row_g[tk].y) == gen ? s.row_n[tk] : root_to[tk];
   };
   // the fused CTC decision of one frame (ctc_decode_kernel's, R13, R14, R17, R19); the frame's
   // slot is handed back (and refilled) as soon as its columns are in registers
-  auto decide = [&](const float* fb, int32_t pc) {
-    float val[kMaxColsPerLane], mx[kMaxColsPerLane];
-    const float* bp = fb + lane;
+  auto load_frame = [&](int32_t t, float (&val)[kMaxColsPerLane]) {  // frame t's columns into registers
+    const float* bp = take(t) + lane;
+    SSTAMP(1);
 #pragma unroll
     for (int j = 0; j < kMaxColsPerLane; ++j) {
       const int32_t col = lane + 32 * j;
@@ -1049,6 +1086,9 @@ __global__ void __maxnreg__(kSegMaxReg)
     give();
     issue_upto();
     SSTAMP(2);
+  };
+  auto decide = [&](float (&val)[kMaxColsPerLane], int32_t pc) {
+    float mx[kMaxColsPerLane];
 #pragma unroll
     for (int j = 0; j < kMaxColsPerLane; ++j) {
       const int32_t col = lane + 32 * j;
@@ -1074,11 +1114,16 @@ __global__ void __maxnreg__(kSegMaxReg)
   // one frame t: decision from (st, pc), then (st, pc) after it; returns the selected column or -1
   auto step = [&](int32_t t, int32_t& st, int32_t& pc) {
     SSTAMP(4);
-    ensure_row(st);  // (a rebuild runs while the ring's next frames land)
-    SSTAMP(0);
-    const float* fb = take(t);
-    SSTAMP(1);
-    const int32_t bc = decide(fb, pc);
+    float val[kMaxColsPerLane];
+    if (row_state != st) {  // a rebuild: the record load flies while the frame's columns are read
+      const int4 x = record_issue<kTiny>(m, s, st);
+      load_frame(t, val);
+      finish_row(st, x);
+      SSTAMP(0);
+    } else {
+      load_frame(t, val);
+    }
+    const int32_t bc = decide(val, pc);
     SSTAMP(3);
 #ifdef NGPULM_PHASE_TIMING
     ck[5] += 1;

@@ -28,6 +28,8 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:adva
     -o gpurun_out/adv_$TAG -f python tools/prof_advance.py --batch 1024 > gpurun_out/ncu_full_$TAG.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused_warp -s 10 -c 1 \
     -o gpurun_out/fused_ctc_$TAG -f python tools/prof_advance.py --batch 256 --mode ctc > gpurun_out/ncu_fused_$TAG.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:ctc_ --csv \
+    --log-file gpurun_out/decode_launches_$TAG.csv python tools/prof_advance.py --batch 256 --mode decode --iters 4 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:ctc_seg -s 4 -c 2 \
     -o gpurun_out/decode_$TAG -f python tools/prof_advance.py --batch 256 --mode decode --iters 4 > gpurun_out/ncu_decode_$TAG.log 2>&1
 python -c "from paper_2505_22857_b200 import _build; _build.build_phase_timing()" > /dev/null 2>&1
