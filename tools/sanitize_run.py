@@ -116,6 +116,19 @@ for name, (m, o, f) in models.items():
         check(f"ctc decode {name} chain={chain}", np.array_equal(fr.cpu().numpy(), ref[0])
               and np.array_equal(el.cpu().numpy(), ref[2]))
     m.set_chain_mode(ng.CHAIN_TABLE)
+    if Bc:  # segment-parallel decode (T >= 128: K = 3 segments), ragged lengths
+        Bs, Ts = 3, 200
+        xs = rng.standard_normal((Bs, Ts, V + 1)).astype(np.float32)
+        xs[:, :, V] += 1.0
+        ls = np.array([200, 130, 70], np.int32)
+        st0 = np.zeros(Bs, np.int32); pv0 = np.full(Bs, -1, np.int32)
+        sd, pd = T_(st0), T_(pv0)
+        em0 = torch.full((Bs, Ts), -1, dtype=torch.int32, device=dev)
+        fr, em, el = m.ctc_greedy_decode(T_(xs), sd, pd, lam=0.7, lengths=T_(ls), emit_out=em0)
+        torch.cuda.synchronize()
+        ref = o.ctc_decode(xs, st0, prev=pv0, lam=0.7, lengths=ls)
+        check(f"ctc segment decode {name}", np.array_equal(fr.cpu().numpy(), ref[0])
+              and np.array_equal(el.cpu().numpy(), ref[2]) and np.array_equal(sd.cpu().numpy(), ref[3]))
     if Bc:
         pd = T_(np.full(Bc, -1, np.int32))
         em0 = torch.full((Bc, Tc), -1, dtype=torch.int32, device=dev)
