@@ -860,6 +860,7 @@ def bench_fused(m, files, dev, stream, rank):
             m.ctc_greedy_decode(x, sv, pv, lam=lam, frames_out=fr2, emit_out=em2, emit_len=el2, stream=stream)
         ms_p = graph_ms(ctc_persistent, stream, 5, reset)
         out[f"ctc_b256_t500_persistent_{name}_ms"] = ms_p
+        out[f"ctc_b256_t500_persistent_{name}_us_per_frame"] = ms_p * 1e3 / T  # per frame of the whole batch
         out[f"ctc_b256_t500_persistent_{name}_logits_gbs"] = x.numel() * 4 / (ms_p * 1e-3) / 1e9
     peak_gbs, _ = peaks()
     out["ctc_persistent_roofline"] = {
