@@ -747,20 +747,23 @@ constexpr int kSegCtas = NGPULM_SEG_CTAS;
 // rebuild writes only the arcs, not the V root entries.
 __host__ __device__ constexpr size_t grow_bytes(int32_t V) { return align16((size_t)(V + 1) * 8); }
 __host__ __device__ constexpr size_t sslice_bytes(int32_t V, int32_t order) {
-  return grow_bytes(V) + wrow_bytes(V) + levels_bytes(order) + 16 + align16(kSegRing * 8) +
+  return grow_bytes(V) + levels_bytes(order) + 16 + align16(kSegRing * 8) +
          (size_t)kSegRing * lbuf_bytes(V);
 }
-// [tiny model copy] | root_w | root_to | cbar | R slices (row_g | row_n | levels | 2 bars | full[kSegRing] | ring)
+// [tiny model copy] | root_w | root_to | cbar | pass-2 boundary starts [2 x 8] | R slices
+// (row_g | levels | 2 bars | full[kSegRing] | ring)
+constexpr int kSegHdr = 16 + 64;
 __host__ __device__ constexpr size_t scta_smem(int32_t V, int32_t order, int R) {
-  return 2 * align16((size_t)V * 4) + 16 + (size_t)R * sslice_bytes(V, order);
+  return 2 * align16((size_t)V * 4) + kSegHdr + (size_t)R * sslice_bytes(V, order);
 }
 
-// write_window with generation-tagged score entries (row_g) and next states (row_n).
+// write_window into generation-tagged entries: row_g[token] = {acc_boff + weight,
+// (generation << 24) | next state} (states < 2^24, generations 1..255).
 template <int kW, bool kPacked>
-__device__ __forceinline__ void write_window_gen(float2* row_g, int32_t* row_n, const Window<kW, kPacked>& a,
-                                                 int32_t k0, int32_t nslots, int32_t pk_bits, int32_t gen) {
+__device__ __forceinline__ void write_window_gen(float2* row_g, const Window<kW, kPacked>& a, int32_t k0,
+                                                 int32_t nslots, int32_t pk_bits, int32_t gen) {
   const uint32_t tmask = (1u << pk_bits) - 1u;
-  const float gtag = __int_as_float(gen);
+  const uint32_t gtag = (uint32_t)gen << 24;
 #pragma unroll
   for (int g = 0; g < kW; g += 8) {
     if (g > 0 && k0 + g >= nslots) break;
@@ -781,8 +784,8 @@ __device__ __forceinline__ void write_window_gen(float2* row_g, int32_t* row_n, 
           tk = x[j];
           nx = t4[j];
         }
-        row_g[tk] = make_float2(__fadd_rn(a.acc[u], ww[j]), gtag);  // acc_boff + arc_weights (Alg. 1 line 74)
-        row_n[tk] = nx;
+        // acc_boff + arc_weights (Alg. 1 line 74), the arc's target
+        row_g[tk] = make_float2(__fadd_rn(a.acc[u], ww[j]), __uint_as_float(gtag | (uint32_t)nx));
       }
     }
   }
@@ -807,12 +810,12 @@ __device__ __forceinline__ int4 record_issue(const DevModel& m, const WSlice& s,
   return x;
 }
 
-// The arc levels of state `st` (record x from record_issue) into row_g / row_n
-// with tag `gen` (Algorithm 1's levels 1..N-1; the root level stays implicit).
+// The arc levels of state `st` (record x from record_issue) into row_g with tag
+// `gen` (Algorithm 1's levels 1..N-1; the root level stays implicit).
 // Returns the row scalars (warp_row_src's, table mode).
-template <bool kPacked, bool kTiny>
+template <bool kPacked, bool kTiny, typename F = NoStamp>
 __device__ __forceinline__ Row build_row_gen(const DevModel& m, const WSlice& s, float2* row_g, int32_t st,
-                                             const int4 x, int32_t gen) {
+                                             const int4 x, int32_t gen, F stamp = F()) {
   constexpr int kW = 8;
   const int lane = threadIdx.x & 31;
   WLevel lv;
@@ -834,14 +837,17 @@ __device__ __forceinline__ Row build_row_gen(const DevModel& m, const WSlice& s,
   }
   lv.qbase = lv.beg >> 2;
   const int32_t nslots = r.nlev > 0 ? __shfl_sync(kFull, lv.eslot, 1) : 0;
+  stamp(7);
   Window<kW, kPacked> a;
   load_window<kW, kPacked, kTiny>(m, s, lv, r.nlev, 0, nslots, a);
   for (int32_t k0 = 0; k0 < nslots;) {
-    write_window_gen<kW, kPacked>(row_g, s.row_n, a, k0, nslots, m.pk_bits, gen);
+    write_window_gen<kW, kPacked>(row_g, a, k0, nslots, m.pk_bits, gen);
+    stamp(8);
     k0 += kW;
     if (k0 < nslots) load_window<kW, kPacked, kTiny>(m, s, lv, r.nlev, k0, nslots, a);
   }
   __syncwarp();
+  stamp(9);
   return r;
 }
 
@@ -924,15 +930,15 @@ __global__ void __maxnreg__(kSegMaxReg)
   int32_t* root_to = reinterpret_cast<int32_t*>(sm0 + rb);
   uint64_t* cbar = reinterpret_cast<uint64_t*>(sm0 + 2 * rb);
   static_assert(kTable, "the segment decode reads the chain table");
-  unsigned char* base = sm0 + 2 * rb + 16 + (size_t)w * sslice_bytes(V, m.order);
+  unsigned char* base = sm0 + 2 * rb + kSegHdr + (size_t)w * sslice_bytes(V, m.order);
   float2* row_g = reinterpret_cast<float2*>(base);
   WSlice s;
   {
-    unsigned char* lp = base + grow_bytes(V) + wrow_bytes(V);
+    unsigned char* lp = base + grow_bytes(V);
     int32_t* l = reinterpret_cast<int32_t*>(lp);
     const int32_t Lc = level_cap(m.order);
     s.row_s = nullptr;
-    s.row_n = reinterpret_cast<int32_t*>(base + grow_bytes(V));
+    s.row_n = nullptr;
     s.beg = l;
     s.pre = l + Lc;
     s.acc = reinterpret_cast<float*>(l + 2 * Lc + 1);
@@ -948,7 +954,7 @@ __global__ void __maxnreg__(kSegMaxReg)
   uint64_t* full = s.bar + 2;
   float* ring = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(full) + align16(kSegRing * 8));
   const size_t lstride = lbuf_bytes(V) / 4;
-  for (int32_t c = lane; c < V; c += 32) row_g[c] = make_float2(0.f, __int_as_float(-1));  // no generation yet
+  for (int32_t c = lane; c < V; c += 32) row_g[c] = make_float2(0.f, 0.f);  // generation 0: never current
   pdl_trigger();
   if (threadIdx.x == 0) {  // the root level (immutable model data: before the wait)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(cbar)) : "memory");
@@ -966,7 +972,7 @@ __global__ void __maxnreg__(kSegMaxReg)
   }
   __syncthreads();
   const int32_t chain = (int32_t)blockIdx.x * R + w;
-  const int32_t row = kFix ? chain : chain / K;
+  const int32_t row = kFix ? (int32_t)blockIdx.x : chain / K;  // pass 2: one row per CTA
   const int32_t k0 = kFix ? 0 : chain % K;
   auto cta_exit = [&]() {  // no exit with the CTA's bulk copies in flight
     if (threadIdx.x == 0) {
@@ -981,7 +987,7 @@ __global__ void __maxnreg__(kSegMaxReg)
   const int32_t st0 = states[row];  // (pass 2 rewrites it last, in compact_row)
   if (!kFix && (st0 < 0 || st0 >= m.S || seg_begin(k0, L0, L) >= len)) { cta_exit(); return; }
   if (kFix && (st0 < 0 || st0 >= m.S)) {  // an invalid row decides nothing (as ctc_decode_kernel)
-    compact_row(row, T, len, st0, sp, frames_out, rec, states, prev, emit_len, m.bad_row, true);
+    if (w == 0) compact_row(row, T, len, st0, sp, frames_out, rec, states, prev, emit_len, m.bad_row, true);
     cta_exit();
     return;
   }
@@ -1019,7 +1025,7 @@ __global__ void __maxnreg__(kSegMaxReg)
 #ifdef NGPULM_PHASE_TIMING
   // debug build: per chain 0 rebuilds, 1 frame waits, 2 loads + refill issue, 3 decision, 4 records;
   // counts 5 frames, 6 rebuilds
-  long long ck[7] = {0};
+  long long ck[11] = {0};
   long long tq0 = clock64(), tq1;
 #define SSTAMP(i) do { tq1 = clock64(); ck[i] += tq1 - tq0; tq0 = tq1; } while (0)
 #else
@@ -1042,8 +1048,18 @@ __global__ void __maxnreg__(kSegMaxReg)
 #ifdef NGPULM_PHASE_TIMING
     ck[6] += 1;
 #endif
-    ++gen;
-    const Row r = build_row_gen<kPacked, kTiny>(m, s, row_g, st, x, gen);
+    if (++gen == 256) {  // generations wrap: no entry may carry the new one
+      __syncwarp();
+      for (int32_t c = lane; c < V; c += 32) row_g[c].y = 0.f;
+      __syncwarp();
+      gen = 1;
+    }
+#ifdef NGPULM_PHASE_TIMING
+    auto bstamp = [&](int i) { SSTAMP(i); };
+#else
+    NoStamp bstamp;
+#endif
+    const Row r = build_row_gen<kPacked, kTiny>(m, s, row_g, st, x, gen, bstamp);
     // branch-free, loads in groups of 11 columns (lane i: columns i + 32 j); out-of-row columns read token V-1
     static_assert(kMaxColsPerLane % 11 == 0, "groups of 11 columns");
 #pragma unroll
@@ -1060,7 +1076,7 @@ __global__ void __maxnreg__(kSegMaxReg)
 #pragma unroll
       for (int u = 0; u < 11; ++u) {
         const int32_t col = lane + 32 * (g + u);
-        const float v = __float_as_int(e[u].y) == gen ? e[u].x : __fadd_rn(r.acc_root, rv[u]);  // arc, else root
+        const float v = (__float_as_uint(e[u].y) >> 24) == (uint32_t)gen ? e[u].x : __fadd_rn(r.acc_root, rv[u]);
         lm[g + u] = (col < ncols && col != sp) ? v : 0.f;  // blank: 0 (fused value = asr)
       }
     }
@@ -1070,7 +1086,8 @@ __global__ void __maxnreg__(kSegMaxReg)
     if (row_state != st) finish_row(st, record_issue<kTiny>(m, s, st));
   };
   auto next_state = [&](int32_t tk) {  // the state after token tk from the row's state
-    return __float_as_int(row_g[tk].y) == gen ? s.row_n[tk] : root_to[tk];
+    const uint32_t e = __float_as_uint(row_g[tk].y);
+    return (e >> 24) == (uint32_t)gen ? (int32_t)(e & 0xffffffu) : root_to[tk];
   };
   // the fused CTC decision of one frame (ctc_decode_kernel's, R13, R14, R17, R19); the frame's
   // slot is handed back (and refilled) as soon as its columns are in registers
@@ -1159,35 +1176,32 @@ __global__ void __maxnreg__(kSegMaxReg)
       }
       SSTAMP(4);
     }
-  } else {  // ---- pass 2: the segments of the row in order, from the true boundary state
+  } else {  // ---- pass 2: every boundary of the row at once (warp w: k = 1 + w, 1 + w + R, ...), then warp 0
+    // re-does, in order, any boundary whose start its predecessor's fix-up rewrote, and compacts
+    int32_t* used = reinterpret_cast<int32_t*>(sm0 + 2 * rb + 16);  // [k]: start state, [8 + k]: start prev
     const int32_t pc_row = __ldg(&prev[row]);
-    for (int32_t k = 1; k < K; ++k) {
-      const int32_t t0 = seg_begin(k, L0, L), t1 = min(seg_begin(k + 1, L0, L), len);
-      if (t0 >= len) break;
-      // one round of loads: the boundary state, the 32 frames before t0 (prev) and pass 1's
-      // records of the first 32 frames of the segment
-      int32_t st = ro[t0 - 1], pc = pc_row;
-      const int32_t fb = t0 - 1 - lane >= 0 ? fo[t0 - 1 - lane] : -1;
-      const int32_t f_pre = t0 + lane < t1 ? fo[t0 + lane] : -1, s_pre = t0 + lane < t1 ? ro[t0 + lane] : -1;
-      // prev before t0: the last frame before t0 that selected a column (blank -> -1)
-      uint32_t hit = __ballot_sync(kFull, fb >= 0);
-      if (hit) {
-        const int32_t fl = __shfl_sync(kFull, fb, __ffs(hit) - 1);
-        pc = fl == sp ? -1 : fl;
-      } else {
-        for (int32_t b = t0 - 33; b >= 0; b -= 32) {
-          const int32_t t = b - lane;
-          const int32_t f = t >= 0 ? fo[t] : -1;
-          hit = __ballot_sync(kFull, f >= 0);
-          if (hit) {
-            const int32_t fl = __shfl_sync(kFull, f, __ffs(hit) - 1);
-            pc = fl == sp ? -1 : fl;
-            break;
-          }
+    // prev before t0: the last frame before t0 that selected a column (blank -> -1), else the row's prev
+    auto prev_before = [&](int32_t t0) {
+      int32_t pc = pc_row;
+      for (int32_t b = t0 - 1; b >= 0; b -= 32) {
+        const int32_t t = b - lane;
+        const int32_t f = t >= 0 ? fo[t] : -1;
+        const uint32_t hit = __ballot_sync(kFull, f >= 0);
+        if (hit) {
+          const int32_t fl = __shfl_sync(kFull, f, __ffs(hit) - 1);
+          pc = fl == sp ? -1 : fl;
+          break;
         }
       }
-      // frames still in the ring from the previous segment's meeting point: their slots are
-      // taken back after this segment's row is built (they have landed by then)
+      return pc;
+    };
+    // re-decide segment k from (st, pc) at its first frame until the decision and the state meet the
+    // records (any record sequence in the arrays is one continuous run of the decision process)
+    auto fix = [&](int32_t k, int32_t st, int32_t pc) {
+      const int32_t t0 = seg_begin(k, L0, L), t1 = min(seg_begin(k + 1, L0, L), len);
+      const int32_t f_pre = t0 + lane < t1 ? fo[t0 + lane] : -1, s_pre = t0 + lane < t1 ? ro[t0 + lane] : -1;
+      // frames still in the ring from the warp's previous meeting point: their slots are taken
+      // back after this segment's row is built (they have landed by then)
       const uint32_t stale_end = issued;
       next_t = t0;
       stop_t = t1;
@@ -1214,9 +1228,28 @@ __global__ void __maxnreg__(kSegMaxReg)
         __syncwarp();
         if (met) break;
       }
+    };
+    for (int32_t k = 1 + w; k < K; k += R) {
+      const int32_t t0 = seg_begin(k, L0, L);
+      if (t0 >= len) break;
+      const int32_t st = ro[t0 - 1], pc = prev_before(t0);  // (the predecessor's fix-up may be rewriting them)
+      if (lane == 0) {
+        used[k] = st;
+        used[8 + k] = pc;
+      }
+      fix(k, st, pc);
     }
-    __syncwarp();
-    compact_row(row, T, len, st0, sp, frames_out, rec, states, prev, emit_len, m.bad_row, false);
+    __syncthreads();  // every fix-up's records are visible to the CTA
+    if (w == 0) {
+      for (int32_t k = 1; k < K; ++k) {  // segments before k are final: k's true start decides
+        const int32_t t0 = seg_begin(k, L0, L);
+        if (t0 >= len) break;
+        const int32_t st = ro[t0 - 1], pc = prev_before(t0);
+        if (st != used[k] || pc != used[8 + k]) fix(k, st, pc);
+      }
+      __syncwarp();
+      compact_row(row, T, len, st0, sp, frames_out, rec, states, prev, emit_len, m.bad_row, false);
+    }
     while (consumed < issued) {  // frames issued past the last meeting point: let them land
       take(0);
       give();
@@ -1225,7 +1258,7 @@ __global__ void __maxnreg__(kSegMaxReg)
   cp_async_settle();  // every edge cp.async of this warp has landed (the ring waits already implied it)
 #ifdef NGPULM_PHASE_TIMING
   if (!kFix && lane == 0 && chain < 16384)
-    for (int i = 0; i < 7; ++i) g_phase[chain * 16 + i] = (unsigned long long)ck[i];
+    for (int i = 0; i < 11; ++i) g_phase[chain * 16 + i] = (unsigned long long)ck[i];
 #endif
 #undef SSTAMP
 #undef NGPULM_RW
@@ -1261,7 +1294,7 @@ int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride
   int K = 148 * kSegCtas * kSegRows / B;
   K = K > 8 ? 8 : K;
   if (K > T / NGPULM_SEG_MIN_FRAMES) K = T / NGPULM_SEG_MIN_FRAMES;
-  if (table && frames_out && emit_out && K >= 2 && kSegCtas > 0) {
+  if (table && frames_out && emit_out && K >= 2 && kSegCtas > 0 && m.S <= (1 << 24)) {  // (24-bit states)
     // every chain the same number of frames: segment 0 (no warm-up) kSegWarm frames longer
     const int32_t L = (T - kSegWarm + K - 1) / K, L0 = T - (K - 1) * L;
     // the tiny-LM copy only where it keeps kSegCtas CTAs per SM: one CTA per SM halves the chains
@@ -1271,20 +1304,25 @@ int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride
                       kSegCtas * (sm0 + tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) + 1024) <= 228 * 1024;
     const size_t sm = sm0 + (tiny ? tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) : 0);
     if (kSegCtas * (sm + 1024) <= 228 * 1024) {
-      const dim3 b1(32 * kSegRows), g1((B * K + kSegRows - 1) / kSegRows), g2((B + kSegRows - 1) / kSegRows);
+      // pass 2: one CTA per row, one warp per boundary as far as 8 warps per SM (the register file) allow
+      const int rows_per_sm = (B + 147) / 148;
+      int w2 = 8 / rows_per_sm;
+      w2 = w2 < 1 ? 1 : (w2 > K - 1 ? K - 1 : w2);
+      const size_t sm2 = scta_smem(m.V, m.order, w2) + (tiny ? tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) : 0);
+      const dim3 b1(32 * kSegRows), g1((B * K + kSegRows - 1) / kSegRows), b2(32 * w2), g2(B);
       int e;
-#define NGPULM_SEG(P, TI, FIX, G)                                                                                   \
+#define NGPULM_SEG(P, TI, FIX, G, BL, SM)                                                                           \
   ((e = ensure_max_carveout((const void*)ctc_seg_kernel<true, P, TI, FIX>)) != 0                                     \
        ? e                                                                                                          \
-       : launch(ctc_seg_kernel<true, P, TI, FIX>, G, b1, sm, st, m, logits, row_stride, frame_stride, B, T, K, L0, L, \
+       : launch(ctc_seg_kernel<true, P, TI, FIX>, G, BL, SM, st, m, logits, row_stride, frame_stride, B, T, K, L0, L, \
                 lengths, states, prev, lambda, blank, frames_out, emit_out, emit_len))
-      if (tiny) e = NGPULM_SEG(true, true, false, g1);
-      else if (pk) e = NGPULM_SEG(true, false, false, g1);
-      else e = NGPULM_SEG(false, false, false, g1);
+      if (tiny) e = NGPULM_SEG(true, true, false, g1, b1, sm);
+      else if (pk) e = NGPULM_SEG(true, false, false, g1, b1, sm);
+      else e = NGPULM_SEG(false, false, false, g1, b1, sm);
       if (e) return e;
-      if (tiny) e = NGPULM_SEG(true, true, true, g2);
-      else if (pk) e = NGPULM_SEG(true, false, true, g2);
-      else e = NGPULM_SEG(false, false, true, g2);
+      if (tiny) e = NGPULM_SEG(true, true, true, g2, b2, sm2);
+      else if (pk) e = NGPULM_SEG(true, false, true, g2, b2, sm2);
+      else e = NGPULM_SEG(false, false, true, g2, b2, sm2);
 #undef NGPULM_SEG
       return e;
     }

@@ -217,3 +217,26 @@ def test_segmented_decode_edge_cases(pairs, kernel):
         assert np.array_equal(emn[r, : el[r]], g[1][r, : el[r]])
     assert (g[0][3, 70:75] == -1).all() and g[0][4, 64] == -1  # a NaN frame selects nothing
     assert m.check() == 6  # (the single-chain run set the sticky word again; read and clear it)
+
+
+@pytest.mark.parametrize("kernel", [ng.ADVANCE_AUTO, ng.ADVANCE_WARP])
+def test_segmented_decode_long_chains(pairs, kernel):
+    """Two segments per row (B in (395, 592]) of ~450 frames with an emission on most
+    frames: a chain rebuilds its row more than 255 times, so the 8-bit rebuild
+    generations of the row entries wrap inside one chain; every row vs the oracle."""
+    m, o, f = pairs["tri64"]
+    B, T = 420, 900
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal((B, T, o.V + 1)).astype(np.float32)
+    x[:, :, o.V] -= 1.0  # blank rarely wins: an emission on most frames
+    start = synth.uniform_states(o.num_states, B, seed=22)
+    prev0 = np.full(B, -1, np.int32)
+    lengths = np.full(B, T, np.int32)
+    lengths[:4] = [T - 1, 451, 450, 449]
+    m.set_advance_kernel(kernel)
+    try:
+        g = gpu_decode(m, x, start, prev0, 0.1, lengths)
+    finally:
+        m.set_advance_kernel(ng.ADVANCE_AUTO)
+    assert (g[2] > 600).sum() > B // 2  # most rows emit on most frames: > 255 rebuilds per segment
+    assert_same(g, o.ctc_decode(x, start, prev=prev0, lam=0.1, lengths=lengths))

@@ -1,5 +1,6 @@
 """Per-chain phase cycles of the segment-parallel CTC decode's pass 1 (debug build lib/libngpulm_timing.so):
-rebuilds, frame waits, loads + refill issue, decisions, record writes; medians over chains."""
+per frame: ring wait, loads + refill issue, decision, record writes; per rebuild: chain record, arc gathers +
+writes, final sync, register reload; medians over chains."""
 import ctypes as C
 import os
 import sys
@@ -36,12 +37,14 @@ for B in (1, 148, 256):
     allp = buf.reshape(8192 + 4096, 16).astype(np.int64)
     ph = allp[:4096]
     ph = ph[ph[:, 5] > 0]
-    names = ["rebuild", "wait", "load+issue", "decide", "records", "frames", "rebuilds"]
+    names = ["reload", "wait", "load+issue", "decide", "records", "frames", "rebuilds", "record", "arcs+writes",
+             "sync"]
     med = {n: int(np.median(ph[:, i])) for i, n in enumerate(names)}
-    per = {n: round(med[n] / max(1, med["frames"])) for n in names[:5]}
-    tot = ph[:, :5].sum(1)
+    per = {n: round(med[n] / max(1, med["frames"])) for n in ["wait", "load+issue", "decide", "records"]}
+    per_rb = {n: round(med[n] / max(1, med["rebuilds"])) for n in ["record", "arcs+writes", "sync", "reload"]}
+    tot = ph[:, [0, 1, 2, 3, 4, 7, 8, 9]].sum(1)
     fix = allp[8192:8192 + B, 1:8]
     print(f"B={B}: {e0.elapsed_time(e1) * 1e3:.0f} us, {len(ph)} chains; medians {med}; per frame {per}; "
-          f"per rebuild {med['rebuild'] / max(1, med['rebuilds']):.0f}; chain cycles median {int(np.median(tot))} "
+          f"per rebuild {per_rb}; chain cycles median {int(np.median(tot))} "
           f"p90 {int(np.percentile(tot, 90))} max {int(tot.max())}; pass-2 frames per row: mean "
           f"{fix.sum(1).mean():.1f} max {fix.sum(1).max()} (per segment max {fix.max(0).tolist()})", flush=True)
