@@ -733,7 +733,10 @@ __global__ void __launch_bounds__(32 * (2 + kSumWarps), 2)
 #define NGPULM_SEG_RING 2
 #endif
 constexpr int kSegRing = NGPULM_SEG_RING;  // frames in flight per chain
-constexpr int kSegWarm = 16;  // warm-up frames before a segment >= 1
+#ifndef NGPULM_SEG_WARM
+#define NGPULM_SEG_WARM 16
+#endif
+constexpr int kSegWarm = NGPULM_SEG_WARM;  // warm-up frames before a segment >= 1
 #ifndef NGPULM_SEG_ROWS
 #define NGPULM_SEG_ROWS 4
 #endif
