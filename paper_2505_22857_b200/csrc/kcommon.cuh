@@ -401,7 +401,11 @@ __device__ __forceinline__ void build_row(const DevModel& m, const Slice& s, con
 #ifndef NGPULM_ADV_MINB_PACKED8
 #define NGPULM_ADV_MINB_PACKED8 16
 #endif
-#define NGPULM_ADV_MINB(kW, kPacked) ((kW) == 8 ? ((kPacked) ? NGPULM_ADV_MINB_PACKED8 : 10) : NGPULM_ADV_MINB_WIDE)
+#ifndef NGPULM_ADV_MINB_UNPACKED8
+#define NGPULM_ADV_MINB_UNPACKED8 10
+#endif
+#define NGPULM_ADV_MINB(kW, kPacked) \
+  ((kW) == 8 ? ((kPacked) ? NGPULM_ADV_MINB_PACKED8 : NGPULM_ADV_MINB_UNPACKED8) : NGPULM_ADV_MINB_WIDE)
 #ifndef NGPULM_TINY_MAX_B
 #define NGPULM_TINY_MAX_B 148  // tiny LM in shared memory up to one row per SM (B=128: 1.34 vs 1.66 us);
 #endif                         // beyond, the one-row-per-CTA global kernel wins (B=1024: 2.53 vs 3.08)
