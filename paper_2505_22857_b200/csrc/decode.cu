@@ -726,6 +726,10 @@ __global__ void __launch_bounds__(32 * (2 + kSumWarps), 2)
 #ifndef NGPULM_SEG_EXPT
 #define NGPULM_SEG_EXPT 0  // timing experiments only (tools/): bit 0 no proxy fence, bit 1 no pass-1 records
 #endif
+#ifndef NGPULM_SEG_MERGED
+#define NGPULM_SEG_MERGED 0  // 1: both passes in one launch (one CTA per row; measured 0.322 vs 0.305 ms: the
+                             // pass-2 code spills registers into the pass-1 loop); 0: two launches
+#endif
 #ifndef NGPULM_SEG_RW_REGS
 #define NGPULM_SEG_RW_REGS 1  // root weights: 1 in registers (33 per lane; 0.305 vs 0.323 ms), 0 read from the CTA copy
 #endif
@@ -918,7 +922,9 @@ __device__ __forceinline__ void compact_row(int32_t row, int32_t T, int32_t len,
 // registers: as many as kSegCtas resident CTAs leave (65536 per SM, allocated in units of 8 per thread)
 constexpr int kSegMaxReg = (65536 / (32 * kSegRows * kSegCtas)) / 8 * 8 > 255 ? 255
                                                                                : (65536 / (32 * kSegRows * kSegCtas)) / 8 * 8;
-template <bool kTable, bool kPacked, bool kTiny, bool kFix>
+// kPass: 1 = pass 1 only (one warp per chain), 2 = pass 2 only (one CTA per row), 3 = both in one launch
+// (one CTA per row, warp w decodes segment w, then the same CTA fixes the row's boundaries)
+template <bool kTable, bool kPacked, bool kTiny, int kPass>
 __global__ void __maxnreg__(kSegMaxReg)
     ctc_seg_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int64_t frame_stride,
                    int32_t B, int32_t T, int32_t K, int32_t L0, int32_t L, const int32_t* __restrict__ lengths,
@@ -975,8 +981,8 @@ __global__ void __maxnreg__(kSegMaxReg)
   }
   __syncthreads();
   const int32_t chain = (int32_t)blockIdx.x * R + w;
-  const int32_t row = kFix ? (int32_t)blockIdx.x : chain / K;  // pass 2: one row per CTA
-  const int32_t k0 = kFix ? 0 : chain % K;
+  const int32_t row = kPass == 1 ? chain / K : (int32_t)blockIdx.x;  // passes 2 and 3: one row per CTA
+  const int32_t k0 = kPass == 1 ? chain % K : (kPass == 3 ? w : 0);
   auto cta_exit = [&]() {  // no exit with the CTA's bulk copies in flight
     if (threadIdx.x == 0) {
       mbar_wait(cbar, 0);
@@ -988,8 +994,8 @@ __global__ void __maxnreg__(kSegMaxReg)
   int32_t len = T;
   if (lengths) len = min(T, max(0, __ldg(&lengths[row])));
   const int32_t st0 = states[row];  // (pass 2 rewrites it last, in compact_row)
-  if (!kFix && (st0 < 0 || st0 >= m.S || seg_begin(k0, L0, L) >= len)) { cta_exit(); return; }
-  if (kFix && (st0 < 0 || st0 >= m.S)) {  // an invalid row decides nothing (as ctc_decode_kernel)
+  if (kPass == 1 && (st0 < 0 || st0 >= m.S || seg_begin(k0, L0, L) >= len)) { cta_exit(); return; }
+  if (kPass != 1 && (st0 < 0 || st0 >= m.S)) {  // an invalid row decides nothing (as ctc_decode_kernel)
     if (w == 0) compact_row(row, T, len, st0, sp, frames_out, rec, states, prev, emit_len, m.bad_row, true);
     cta_exit();
     return;
@@ -1157,7 +1163,7 @@ __global__ void __maxnreg__(kSegMaxReg)
     }
     return bc;
   };
-  if (!kFix) {  // ---- pass 1: segment k0
+  if (kPass == 1 || (kPass == 3 && seg_begin(k0, L0, L) < len)) {  // ---- pass 1: segment k0
     const int32_t t0 = seg_begin(k0, L0, L), t1 = min(seg_begin(k0 + 1, L0, L), len);
     const int32_t tb = k0 == 0 ? 0 : max(0, t0 - kSegWarm);
     int32_t st = k0 == 0 ? st0 : 0, pc = k0 == 0 ? __ldg(&prev[row]) : -1;
@@ -1179,7 +1185,9 @@ __global__ void __maxnreg__(kSegMaxReg)
       }
       SSTAMP(4);
     }
-  } else {  // ---- pass 2: every boundary of the row at once (warp w: k = 1 + w, 1 + w + R, ...), then warp 0
+  }
+  if (kPass == 3) __syncthreads();  // every segment of the row decoded: its records are visible to the CTA
+  if (kPass != 1) {  // ---- pass 2: every boundary of the row at once (warp w: k = 1 + w, 1 + w + R, ...), then warp 0
     // re-does, in order, any boundary whose start its predecessor's fix-up rewrote, and compacts
     int32_t* used = reinterpret_cast<int32_t*>(sm0 + 2 * rb + 16);  // [k]: start state, [8 + k]: start prev
     const int32_t pc_row = __ldg(&prev[row]);
@@ -1260,7 +1268,7 @@ __global__ void __maxnreg__(kSegMaxReg)
   }
   cp_async_settle();  // every edge cp.async of this warp has landed (the ring waits already implied it)
 #ifdef NGPULM_PHASE_TIMING
-  if (!kFix && lane == 0 && chain < 16384)
+  if (kPass != 2 && lane == 0 && chain < 16384)
     for (int i = 0; i < 11; ++i) g_phase[chain * 16 + i] = (unsigned long long)ck[i];
 #endif
 #undef SSTAMP
@@ -1293,43 +1301,69 @@ int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride
 #undef NGPULM_DECODE2
   }
   // segment-parallel exact decode: table mode, both record buffers given, enough frames per segment
-  // (148 SMs x kSegCtas resident CTAs x kSegRows chains: one wave of chains)
-  int K = 148 * kSegCtas * kSegRows / B;
-  K = K > 8 ? 8 : K;
-  if (K > T / NGPULM_SEG_MIN_FRAMES) K = T / NGPULM_SEG_MIN_FRAMES;
-  if (table && frames_out && emit_out && K >= 2 && kSegCtas > 0 && m.S <= (1 << 24)) {  // (24-bit states)
-    // every chain the same number of frames: segment 0 (no warm-up) kSegWarm frames longer
-    const int32_t L = (T - kSegWarm + K - 1) / K, L0 = T - (K - 1) * L;
-    // the tiny-LM copy only where it keeps kSegCtas CTAs per SM: one CTA per SM halves the chains
-    // in flight, which costs more than the shared-memory model saves (B=256: 0.38 vs 0.26 ms)
-    const size_t sm0 = scta_smem(m.V, m.order, kSegRows);
-    const bool tiny = pk && m.tiny_chain_bytes > 0 &&
-                      kSegCtas * (sm0 + tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) + 1024) <= 228 * 1024;
-    const size_t sm = sm0 + (tiny ? tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) : 0);
-    if (kSegCtas * (sm + 1024) <= 228 * 1024) {
-      // pass 2: one CTA per row, one warp per boundary as far as 8 warps per SM (the register file) allow
-      const int rows_per_sm = (B + 147) / 148;
-      int w2 = 8 / rows_per_sm;
-      w2 = w2 < 1 ? 1 : (w2 > K - 1 ? K - 1 : w2);
-      const size_t sm2 = scta_smem(m.V, m.order, w2) + (tiny ? tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) : 0);
-      const dim3 b1(32 * kSegRows), g1((B * K + kSegRows - 1) / kSegRows), b2(32 * w2), g2(B);
-      int e;
-#define NGPULM_SEG(P, TI, FIX, G, BL, SM)                                                                           \
-  ((e = ensure_max_carveout((const void*)ctc_seg_kernel<true, P, TI, FIX>)) != 0                                     \
+  const size_t tinyb = pk && m.tiny_chain_bytes > 0 ? tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) : 0;
+#define NGPULM_SEG(P, TI, PASS, G, BL, SM)                                                                          \
+  ((e = ensure_max_carveout((const void*)ctc_seg_kernel<true, P, TI, PASS>)) != 0                                    \
        ? e                                                                                                          \
-       : launch(ctc_seg_kernel<true, P, TI, FIX>, G, BL, SM, st, m, logits, row_stride, frame_stride, B, T, K, L0, L, \
-                lengths, states, prev, lambda, blank, frames_out, emit_out, emit_len))
-      if (tiny) e = NGPULM_SEG(true, true, false, g1, b1, sm);
-      else if (pk) e = NGPULM_SEG(true, false, false, g1, b1, sm);
-      else e = NGPULM_SEG(false, false, false, g1, b1, sm);
-      if (e) return e;
-      if (tiny) e = NGPULM_SEG(true, true, true, g2, b2, sm2);
-      else if (pk) e = NGPULM_SEG(true, false, true, g2, b2, sm2);
-      else e = NGPULM_SEG(false, false, true, g2, b2, sm2);
-#undef NGPULM_SEG
-      return e;
+       : launch(ctc_seg_kernel<true, P, TI, PASS>, G, BL, SM, st, m, logits, row_stride, frame_stride, B, T, K, L0, \
+                L, lengths, states, prev, lambda, blank, frames_out, emit_out, emit_len))
+  const bool seg_ok = table && frames_out && emit_out && kSegCtas > 0 && m.S <= (1 << 24);  // (24-bit states)
+#if NGPULM_SEG_MERGED
+  // one launch, one CTA per row, warp w decodes segment w and the CTA then fixes the row's boundaries:
+  // a row's fix-ups start as soon as its own segments are done. K warps per CTA x ceil(B / 148) CTAs
+  // per SM within the 8 warps per SM the register file holds (B <= 148: 8 segments, <= 296: 4, <= 592: 2)
+  {
+    const int cps = (B + 147) / 148;
+    int K = 8 / cps;
+    K = K > 8 ? 8 : K;
+    if (K > T / NGPULM_SEG_MIN_FRAMES) K = T / NGPULM_SEG_MIN_FRAMES;
+    if (seg_ok && K >= 2) {
+      // every chain the same number of frames: segment 0 (no warm-up) kSegWarm frames longer
+      const int32_t L = (T - kSegWarm + K - 1) / K, L0 = T - (K - 1) * L;
+      const size_t sm0 = scta_smem(m.V, m.order, K);
+      // the tiny-LM copy only where the CTAs of a wave still fit
+      const bool tiny = tinyb > 0 && cps * (sm0 + tinyb + 1024) <= 228 * 1024;
+      const size_t sm = sm0 + (tiny ? tinyb : 0);
+      if (cps * (sm + 1024) <= 228 * 1024) {
+        int e;
+        const dim3 g(B), b(32 * K);
+        if (tiny) return NGPULM_SEG(true, true, 3, g, b, sm);
+        if (pk) return NGPULM_SEG(true, false, 3, g, b, sm);
+        return NGPULM_SEG(false, false, 3, g, b, sm);
+      }
     }
   }
+#else
+  // two launches: pass 1 (148 SMs x kSegCtas resident CTAs x kSegRows chains: one wave of chains), pass 2
+  {
+    int K = 148 * kSegCtas * kSegRows / B;
+    K = K > 8 ? 8 : K;
+    if (K > T / NGPULM_SEG_MIN_FRAMES) K = T / NGPULM_SEG_MIN_FRAMES;
+    if (seg_ok && K >= 2) {
+      const int32_t L = (T - kSegWarm + K - 1) / K, L0 = T - (K - 1) * L;
+      const size_t sm0 = scta_smem(m.V, m.order, kSegRows);
+      const bool tiny = tinyb > 0 && kSegCtas * (sm0 + tinyb + 1024) <= 228 * 1024;
+      const size_t sm = sm0 + (tiny ? tinyb : 0);
+      if (kSegCtas * (sm + 1024) <= 228 * 1024) {
+        // pass 2: one CTA per row, one warp per boundary as far as 8 warps per SM (the register file) allow
+        const int rows_per_sm = (B + 147) / 148;
+        int w2 = 8 / rows_per_sm;
+        w2 = w2 < 1 ? 1 : (w2 > K - 1 ? K - 1 : w2);
+        const size_t sm2 = scta_smem(m.V, m.order, w2) + (tiny ? tinyb : 0);
+        const dim3 b1(32 * kSegRows), g1((B * K + kSegRows - 1) / kSegRows), b2(32 * w2), g2(B);
+        int e;
+        if (tiny) e = NGPULM_SEG(true, true, 1, g1, b1, sm);
+        else if (pk) e = NGPULM_SEG(true, false, 1, g1, b1, sm);
+        else e = NGPULM_SEG(false, false, 1, g1, b1, sm);
+        if (e) return e;
+        if (tiny) return NGPULM_SEG(true, true, 2, g2, b2, sm2);
+        if (pk) return NGPULM_SEG(true, false, 2, g2, b2, sm2);
+        return NGPULM_SEG(false, false, 2, g2, b2, sm2);
+      }
+    }
+  }
+#endif
+#undef NGPULM_SEG
   if (table && pk && m.tiny_chain_bytes > 0) {  // tiny LM: the model in every CTA's shared memory
     const size_t mb = tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes);
     int R = (B + 147) / 148;
