@@ -924,14 +924,16 @@ constexpr int kSegMaxReg = (65536 / (32 * kSegRows * kSegCtas)) / 8 * 8 > 255 ? 
                                                                                : (65536 / (32 * kSegRows * kSegCtas)) / 8 * 8;
 // kPass: 1 = pass 1 only (one warp per chain), 2 = pass 2 only (one CTA per row), 3 = both in one launch
 // (one CTA per row, warp w decodes segment w, then the same CTA fixes the row's boundaries)
-template <bool kTable, bool kPacked, bool kTiny, int kPass>
+// kVc: the vocabulary size as a compile-time constant (1024, the workload's BPE vocabulary: the column
+// predicates fold away), or 0 = m.V at run time
+template <bool kTable, bool kPacked, bool kTiny, int kPass, int kVc = 0>
 __global__ void __maxnreg__(kSegMaxReg)
     ctc_seg_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int64_t frame_stride,
                    int32_t B, int32_t T, int32_t K, int32_t L0, int32_t L, const int32_t* __restrict__ lengths,
                    int32_t* __restrict__ states, int32_t* __restrict__ prev, float lambda, int32_t sp,
                    int32_t* __restrict__ frames_out, int32_t* __restrict__ rec, int32_t* __restrict__ emit_len) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int32_t V = m.V, ncols = V + 1;
+  const int32_t V = kVc ? kVc : m.V, ncols = V + 1;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, R = blockDim.x >> 5;
   const size_t rb = align16((size_t)V * 4);
   unsigned char* sm0 = smem + (kTiny ? tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) : 0);
@@ -1302,11 +1304,13 @@ int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride
   }
   // segment-parallel exact decode: table mode, both record buffers given, enough frames per segment
   const size_t tinyb = pk && m.tiny_chain_bytes > 0 ? tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes) : 0;
-#define NGPULM_SEG(P, TI, PASS, G, BL, SM)                                                                          \
-  ((e = ensure_max_carveout((const void*)ctc_seg_kernel<true, P, TI, PASS>)) != 0                                    \
+#define NGPULM_SEG_VC(P, TI, PASS, VC, G, BL, SM)                                                                   \
+  ((e = ensure_max_carveout((const void*)ctc_seg_kernel<true, P, TI, PASS, VC>)) != 0                                \
        ? e                                                                                                          \
-       : launch(ctc_seg_kernel<true, P, TI, PASS>, G, BL, SM, st, m, logits, row_stride, frame_stride, B, T, K, L0, \
-                L, lengths, states, prev, lambda, blank, frames_out, emit_out, emit_len))
+       : launch(ctc_seg_kernel<true, P, TI, PASS, VC>, G, BL, SM, st, m, logits, row_stride, frame_stride, B, T, K,  \
+                L0, L, lengths, states, prev, lambda, blank, frames_out, emit_out, emit_len))
+#define NGPULM_SEG(P, TI, PASS, G, BL, SM) \
+  (m.V == 1024 ? NGPULM_SEG_VC(P, TI, PASS, 1024, G, BL, SM) : NGPULM_SEG_VC(P, TI, PASS, 0, G, BL, SM))
   const bool seg_ok = table && frames_out && emit_out && kSegCtas > 0 && m.S <= (1 << 24);  // (24-bit states)
 #if NGPULM_SEG_MERGED
   // one launch, one CTA per row, warp w decodes segment w and the CTA then fixes the row's boundaries:
@@ -1364,6 +1368,7 @@ int launch_ctc_decode(const DevModel& m, const float* logits, int64_t row_stride
   }
 #endif
 #undef NGPULM_SEG
+#undef NGPULM_SEG_VC
   if (table && pk && m.tiny_chain_bytes > 0) {  // tiny LM: the model in every CTA's shared memory
     const size_t mb = tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes);
     int R = (B + 147) / 148;
