@@ -767,13 +767,16 @@ def transducer_steps(m, states0, dev, stream, rank, tag, nsteps=256):
             for k in range(nsteps):
                 m.fused_greedy_step(ng.RNNT, xs[k % NB], sv, lam=lam, tokens_out=tok, stream=stream)
 
-        def with_net():
+        def with_net(ready=False):
             for k in range(nsteps):
                 network_kernel(xs[k % NB], buf)
-                m.fused_greedy_step(ng.RNNT, buf, sv, lam=lam, tokens_out=tok, stream=stream)
+                m.fused_greedy_step(ng.RNNT, buf, sv, lam=lam, tokens_out=tok, stream=stream, inputs_ready=ready)
         reset = lambda: st.copy_(st0)  # noqa: E731
         out[f"{tag}_b{B}_{name}_us_per_step_back_to_back"] = graph_ms(b2b, stream, 5, reset) * 1e3 / nsteps
         out[f"{tag}_b{B}_{name}_us_per_step_after_network"] = graph_ms(with_net, stream, 5, reset) * 1e3 / nsteps
+        # NGPULM_STEP_INPUTS_READY: the network kernel is a plain launch, so the step's inputs are final
+        out[f"{tag}_b{B}_{name}_us_per_step_after_network_inputs_ready"] = graph_ms(
+            lambda: with_net(True), stream, 5, reset) * 1e3 / nsteps
     def net_only():
         for k in range(nsteps):
             network_kernel(xs[k % NB], buf)
@@ -784,6 +787,11 @@ def transducer_steps(m, states0, dev, stream, rank, tag, nsteps=256):
     out[f"{tag}_b{B}_fused_step_us_in_loop"] = f_ - net
     out[f"{tag}_b{B}_plain_step_us_in_loop"] = p_ - net
     out[f"{tag}_b{B}_lm_overhead_vs_plain_loop"] = f_ / p_ - 1.0
+    fr_ = out[f"{tag}_b{B}_fused_us_per_step_after_network_inputs_ready"]
+    pr_ = out[f"{tag}_b{B}_plain_us_per_step_after_network_inputs_ready"]
+    out[f"{tag}_b{B}_fused_step_us_in_loop_inputs_ready"] = fr_ - net
+    out[f"{tag}_b{B}_plain_step_us_in_loop_inputs_ready"] = pr_ - net
+    out[f"{tag}_b{B}_lm_overhead_vs_plain_loop_inputs_ready"] = fr_ / pr_ - 1.0
     return out
 
 

@@ -231,8 +231,20 @@ int ngpulm_fused_greedy_step(const ngpulm_model* model, int32_t mode, const floa
  *     NGPU-LM calls never write logits, so a loop of NGPU-LM steps over
  *     precomputed logits always qualifies; a logits producer launched with
  *     programmatic dependent launch that triggers early does not.
+ *   NGPULM_STEP_INPUTS_READY: the caller guarantees that no kernel which may
+ *     still be running when this call's kernel starts writes ANY of its
+ *     inputs (logits, states, prev, active) — e.g. a transducer / AED loop
+ *     whose network kernel before each step is a plain launch (not a
+ *     programmatic dependent launch: every cuBLAS / PyTorch kernel), so the
+ *     step starts only after it has completed. The kernel then copies the
+ *     logits and builds the LM row from the state it reads at its start,
+ *     without re-reading the state after its programmatic-dependent-launch
+ *     wait. Results are identical to flags == 0 whenever the guarantee holds;
+ *     consecutive NGPU-LM steps (which write states) do not qualify.
+ *     Ignored by the ILM variant and by models without packed arcs and a
+ *     chain table (they run the flags == 0 path).
  * flags == 0 is ngpulm_fused_greedy_step. EUSAGE for unknown flags. */
-enum { NGPULM_STEP_LOGITS_READY = 1 };
+enum { NGPULM_STEP_LOGITS_READY = 1, NGPULM_STEP_INPUTS_READY = 2 };
 int ngpulm_fused_greedy_step_ex(const ngpulm_model* model, int32_t mode, const float* logits,
                                 int64_t row_stride, int32_t B, int32_t* states, int32_t* prev,
                                 const uint8_t* active, float lambda, int32_t blank_id, int32_t* tokens_out,

@@ -22,7 +22,8 @@ NGPULM_OK, NGPULM_EDOMAIN, NGPULM_EUSAGE, NGPULM_ECUDA, NGPULM_EIO = 0, 1, 2, 3,
 CTC, RNNT, AED = 0, 1, 2
 CHAIN_TABLE, CHAIN_WALK = 0, 1
 ADVANCE_AUTO, ADVANCE_WARP, ADVANCE_CTA = 0, 1, 2
-STEP_LOGITS_READY = 1  # ngpulm_fused_greedy_step_ex flag
+STEP_LOGITS_READY = 1  # ngpulm_fused_greedy_step_ex flags
+STEP_INPUTS_READY = 2
 ADVANCE_INDEPENDENT = 1  # ngpulm_advance_ex flag
 MAX_ORDER = 32
 MAX_TOPK = 256
@@ -264,9 +265,10 @@ class NgpuLM:
 
     def fused_greedy_step(self, mode: int, logits, states, prev=None, active=None, lam: float = 0.3,
                           blank_id: int | None = None, tokens_out=None, row_stride: int | None = None,
-                          B: int | None = None, stream=None, logits_ready: bool = False):
+                          B: int | None = None, stream=None, logits_ready: bool = False,
+                          inputs_ready: bool = False):
         """ngpulm_fused_greedy_step (ngpulm_fused_greedy_step_ex with logits_ready:
-        NGPULM_STEP_LOGITS_READY). logits: CUDA f32 tensor whose row b starts at
+        NGPULM_STEP_LOGITS_READY, inputs_ready: NGPULM_STEP_INPUTS_READY). logits: CUDA f32 tensor whose row b starts at
         b*row_stride (default: a [B, V+1] contiguous tensor, or a strided 2-D view
         such as logits3d[:, t] of a [B, T, V+1] tensor). states/prev updated in place.
         states=None with lam=0: plain greedy decoding (no LM)."""
@@ -283,7 +285,8 @@ class NgpuLM:
             _dev_ptr(prev, torch.int32, "prev", B) if prev is not None else None,
             _dev_ptr(active, torch.uint8, "active", B) if active is not None else None,
             float(lam), blank, _dev_ptr(tokens_out, torch.int32, "tokens_out", B),
-            STEP_LOGITS_READY if logits_ready else 0, _stream(stream)))
+            (STEP_LOGITS_READY if logits_ready else 0) | (STEP_INPUTS_READY if inputs_ready else 0),
+            _stream(stream)))
         return tokens_out
 
     def fused_greedy_step_ilm(self, mode: int, logits, states, ilm, lam_ilm: float, prev=None, active=None,

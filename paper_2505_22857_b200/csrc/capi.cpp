@@ -343,7 +343,7 @@ int ngpulm_fused_greedy_step_ex(const ngpulm_model* m, int32_t mode, const float
                                 int32_t B, int32_t* states, int32_t* prev, const uint8_t* active, float lambda,
                                 int32_t blank_id, int32_t* tokens_out, uint32_t flags, ngpulm_stream stream) {
   if (int r = check_hot(m, B)) return r;
-  if (flags & ~(uint32_t)NGPULM_STEP_LOGITS_READY) return err(NGPULM_EUSAGE, "unknown flags");
+  if (flags & ~(uint32_t)(NGPULM_STEP_LOGITS_READY | NGPULM_STEP_INPUTS_READY)) return err(NGPULM_EUSAGE, "unknown flags");
   if (mode != NGPULM_CTC && mode != NGPULM_RNNT && mode != NGPULM_AED) return err(NGPULM_EUSAGE, "bad mode");
   if (blank_id < 0 || blank_id > m->h.V) return err(NGPULM_EUSAGE, "blank_id outside [0, V]");
   if (m->h.V > ngpulm::max_fused_vocab()) return err(NGPULM_EUSAGE, "fused step: the row must fit in shared memory");

@@ -93,8 +93,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 // kTiny: a tiny LM (keyword-biasing size) resident in the CTA's shared memory
 // (tiny_copy_issue before the wait): records and arc quads are shared loads.
 // kEarly (NGPULM_STEP_LOGITS_READY): the logits are copied before the wait.
+// kReady (NGPULM_STEP_INPUTS_READY): no running kernel writes any input, so the
+// logits are copied before the wait as well and the state read before it is
+// final: no re-read after the wait (a decoder loop whose network kernel is not a
+// programmatic-dependent launch: the step starts after it has completed).
 template <int kMode, bool kTable, bool kPacked, bool kAux, bool kNoLM = false, bool kTiny = false,
-          bool kEarly = false>
+          bool kEarly = false, bool kReady = false>
 __global__ void __launch_bounds__(256, 1)
     fused_warp_kernel(DevModel m, const float* __restrict__ logits, int64_t row_stride, int32_t B,
                       int32_t* __restrict__ states, int32_t* __restrict__ prev, const uint8_t* __restrict__ active,
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(256, 1)
     return __shfl_sync(kFull, v, 0);
   };
   const float* lrow = logits + (size_t)row * row_stride;
-  if (kEarly) {  // the caller guarantees no running kernel writes the logits (NGPULM_STEP_LOGITS_READY)
+  if (kEarly || kReady) {  // the caller guarantees no running kernel writes the logits (NGPULM_STEP_LOGITS_READY)
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));  // read once
     issue_frame_cover(lrow, ncols, lbuf, lbar, pol, logits, logits + (size_t)(B - 1) * row_stride + ncols);
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(256, 1)
   // rows, and the logits unless kEarly) are read after the wait only.
   int32_t st = 0;
   Row r{};
-  if (NGPULM_FUSED_SPECULATE && !nolm) {
+  if ((NGPULM_FUSED_SPECULATE || kReady) && !nolm) {
     st = load_state();
     r = build(st, 0);
   }
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(256, 1)
   // used only after the state and record loads are issued
   const bool on = kMode == kLoop ? __ldg(&lp.frame[row]) < __ldg(&lp.len[row]) : (!active || __ldg(&active[row]));
   const int32_t pc = (kMode == NGPULM_CTC) ? __ldg(&prev[row]) : -2;
-  if (on && !kEarly) {  // the logits (an input: after the wait), copied while the state is checked
+  if (on && !(kEarly || kReady)) {  // the logits (an input: after the wait), copied while the state is checked
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));  // read once
     issue_frame_cover(lrow, ncols, lbuf, lbar, pol, logits, logits + (size_t)(B - 1) * row_stride + ncols);
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(256, 1)
   const float* lb = lbuf + (reinterpret_cast<uintptr_t>(lrow) & 15) / 4;  // column c at lb[c]
   int32_t dsel = -1;  // TDT duration (loop mode with durations), else -1
   if (kMode == kLoop && lp.D > 0 && on) dsel = tdt_duration(lp, row);
-  if (!nolm) {
+  if (!nolm && !kReady) {
     const int32_t st1 = load_state();
     if (!NGPULM_FUSED_SPECULATE || st1 != st) {
       // the root targets again (the first build overwrote them)
@@ -241,7 +245,7 @@ __global__ void __launch_bounds__(256, 1)
       if (on) atomicMin(m.bad_row, (unsigned long long)row);
       if (kMode == kLoop && on) lp.frame[row] = lp.len[row];  // an invalid state ends the row's loop
     }
-    if (on || kEarly) { mbar_wait(lbar, 0); cp_async_settle(); }  // no exit with a copy in flight
+    if (on || kEarly || kReady) { mbar_wait(lbar, 0); cp_async_settle(); }  // no exit with a copy in flight
     return;
   }
   mbar_wait(lbar, 0);
@@ -738,7 +742,8 @@ template <int kMode>
 int launch_fused_mode(const DevModel& m, const float* logits, int64_t row_stride, int32_t B, int32_t* states,
                       int32_t* prev, const uint8_t* active, float lambda, int32_t blank, AuxRow aux,
                       int32_t* tokens_out, cudaStream_t st, uint32_t flags) {
-  const bool early = (flags & NGPULM_STEP_LOGITS_READY) && !aux.p;  // (a permission: other paths ignore it)
+  // (permissions: other paths ignore them; inputs ready implies logits ready)
+  const bool early = (flags & (NGPULM_STEP_LOGITS_READY | NGPULM_STEP_INPUTS_READY)) && !aux.p;
   if (m.V % 4 == 0 && m.V <= 1024 && m.adv_kind != NGPULM_ADVANCE_CTA) {
     const bool pk = m.arc_q != nullptr && m.adv_kind == NGPULM_ADVANCE_AUTO, table = m.chain != nullptr;
     if (states == nullptr) {  // plain greedy (no LM): one warp per row, no row build
@@ -768,6 +773,13 @@ int launch_fused_mode(const DevModel& m, const float* logits, int64_t row_stride
                      : launch(fused_warp_kernel<kMode, true, true, false, false, true>, tg, tb, tsm, st, m, logits,
                               row_stride, B, states, prev, active, lambda, blank, aux, Loop{}, tokens_out);
       }
+    }
+    if ((flags & NGPULM_STEP_INPUTS_READY) && !aux.p && table && pk) {  // every mode: one warp per row
+      int R = (B + 147) / 148;
+      R = R < 1 ? 1 : (R > NGPULM_FUSED_MAX_ROWS ? NGPULM_FUSED_MAX_ROWS : R);
+      return launch(fused_warp_kernel<kMode, true, true, false, false, false, false, true>, dim3((B + R - 1) / R),
+                    dim3(32 * R), (size_t)R * fslice_bytes(m.V, m.order), st, m, logits, row_stride, B, states, prev,
+                    active, lambda, blank, aux, Loop{}, tokens_out);
     }
     if (kMode != NGPULM_RNNT || B > NGPULM_PAIR_MAX_B) if (early && table && pk) {
       int R = (B + 147) / 148;

@@ -232,3 +232,30 @@ def test_logits_ready_other_modes(lm6, mode, B):
     torch.cuda.synchronize()
     to, so, _ = o.fused_step(mode, x, st, lam=0.4)
     assert np.array_equal(tok.cpu().numpy(), to) and np.array_equal(st_d.cpu().numpy(), so)
+
+
+@pytest.mark.parametrize("B", [1, 148, 512, 700])
+@pytest.mark.parametrize("mode", [CTC, RNNT, AED])
+def test_fused_step_inputs_ready_after_plain_kernel(lm6, mode, B):
+    """NGPULM_STEP_INPUTS_READY (one warp per row for every mode, the state read
+    once, logits copied at the kernel's start) after a plain (non-PDL) torch kernel
+    that writes the step's logits, as in a transducer / AED loop: every row vs the
+    oracle, and the same tokens / states / prev as flags == 0 (6-gram, packed arcs)."""
+    m, o, f = lm6
+    x = synth.rnnt_logits(B, 1, o.V, seed=B + 3)[0]
+    st, _ = trajectory_states(m, f, B, seed=B)
+    prev = np.random.default_rng(B).integers(-1, o.V, size=B).astype(np.int32) if mode == CTC else None
+    src = T(x)
+    res = []
+    for ready in (False, True):
+        buf = torch.empty_like(src)
+        st_d, pv_d = T(st), (T(prev) if prev is not None else None)
+        torch.mul(src, 1.0, out=buf)  # the "network" kernel: a plain launch writing the logits
+        tok = m.fused_greedy_step(mode, buf, st_d, prev=pv_d, lam=0.3, inputs_ready=ready)
+        torch.cuda.synchronize()
+        res.append((tok.cpu().numpy(), st_d.cpu().numpy(), pv_d.cpu().numpy() if pv_d is not None else None))
+    to, so, po = o.fused_step(mode, x, st, prev=prev, lam=0.3)
+    for tok, sd, pd in res:
+        assert np.array_equal(tok, to) and np.array_equal(sd, so)
+        if mode == CTC:
+            assert np.array_equal(pd, po)
