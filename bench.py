@@ -810,7 +810,8 @@ def label_loop(m, dev, stream, rank):
         def joint(frame, u, last, outl):
             synth.joint_gpu(5 + rank, frame, u, last, outl, temperature=8.0, blank=V, blank_bias=0.75,
                             stream=dec.stream)
-        dec = TransducerGreedyDecoder(m, joint, Bl, 100, lam=lam, use_lm=name == "fused")
+        # the synthetic joint is a plain launch: NGPULM_STEP_INPUTS_READY holds
+        dec = TransducerGreedyDecoder(m, joint, Bl, 100, lam=lam, use_lm=name == "fused", joint_plain_launch=True)
         dec(lengths)  # capture + warm-up
         ts = []
         for _ in range(3):

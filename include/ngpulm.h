@@ -315,6 +315,31 @@ int ngpulm_tdt_loop_step(const ngpulm_model* model, const float* logits, int64_t
                          int32_t* tokens_out, int32_t* emit_out, int32_t* emit_len, int32_t* last_token,
                          int32_t max_len, ngpulm_stream stream);
 
+/* ngpulm_transducer_loop_step / ngpulm_tdt_loop_step with flags:
+ *   NGPULM_STEP_INPUTS_READY: as for ngpulm_fused_greedy_step_ex — no kernel
+ *     which may still be running when this call's kernel starts writes any of
+ *     its inputs (logits, duration logits, states, frame_idx, sym_count,
+ *     lengths, last_token), e.g. a label-looping decoder whose joint kernel
+ *     before each step is a plain launch. The step then copies the logits and
+ *     builds the LM row from the state read at its start (no re-read after its
+ *     programmatic-dependent-launch wait). Results are identical to flags == 0
+ *     whenever the guarantee holds. Ignored with an ILM and for models without
+ *     packed arcs and a chain table.
+ * flags == 0 are the calls above. EUSAGE for unknown flags. */
+int ngpulm_transducer_loop_step_ex(const ngpulm_model* model, const float* logits, int64_t row_stride,
+                                   int32_t B, int32_t* states, int32_t* frame_idx, int32_t* sym_count,
+                                   const int32_t* lengths, int32_t max_symbols, float lambda,
+                                   int32_t blank_id, const float* ilm, int64_t ilm_stride, float lambda_ilm,
+                                   int32_t* tokens_out, int32_t* emit_out, int32_t* emit_len,
+                                   int32_t* last_token, int32_t max_len, uint32_t flags, ngpulm_stream stream);
+int ngpulm_tdt_loop_step_ex(const ngpulm_model* model, const float* logits, int64_t row_stride,
+                            const float* dur_logits, int64_t dur_stride, const int32_t* durations,
+                            int32_t num_durations, int32_t B, int32_t* states, int32_t* frame_idx,
+                            int32_t* sym_count, const int32_t* lengths, int32_t max_symbols, float lambda,
+                            int32_t blank_id, const float* ilm, int64_t ilm_stride, float lambda_ilm,
+                            int32_t* tokens_out, int32_t* emit_out, int32_t* emit_len, int32_t* last_token,
+                            int32_t max_len, uint32_t flags, ngpulm_stream stream);
+
 /* The fused greedy step of ngpulm_fused_greedy_step (same modes, rules and
  * outputs) from LM rows computed beforehand by ngpulm_advance on the SAME
  * states: lm_scores/lm_next dev [B, *] (row b at b*lm_stride, V entries),

@@ -77,6 +77,10 @@ SIGNATURES = {
                                                _P, _P, _P, _P, _I32, _P]),
     "ngpulm_tdt_loop_step": (C.c_int, [_P, _P, _I64, _P, _I64, _P, _I32, _I32, _P, _P, _P, _P, _I32, _F, _I32,
                                         _P, _I64, _F, _P, _P, _P, _P, _I32, _P]),
+    "ngpulm_transducer_loop_step_ex": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _P, _P, _I32, _F, _I32, _P, _I64, _F,
+                                                  _P, _P, _P, _P, _I32, C.c_uint32, _P]),
+    "ngpulm_tdt_loop_step_ex": (C.c_int, [_P, _P, _I64, _P, _I64, _P, _I32, _I32, _P, _P, _P, _P, _I32, _F, _I32,
+                                           _P, _I64, _F, _P, _P, _P, _P, _I32, C.c_uint32, _P]),
     "ngpulm_fused_greedy_step_rows": (C.c_int, [_P, _I32, _P, _I64, _I32, _P, _P, _P, _I64, _P, _P, _P, _F, _I32,
                                                  _P, _P]),
     "ngpulm_fused_topk": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _I64, _F, _F, _I32, _I32, _P, _P, _P, _P]),
@@ -312,11 +316,12 @@ class NgpuLM:
     def transducer_loop_step(self, logits, states, frame_idx, sym_count, lengths, emit_out, emit_len,
                              last_token=None, lam: float = 0.3, blank_id: int | None = None,
                              max_symbols: int = 10, ilm=None, lam_ilm: float = 0.0, tokens_out=None,
-                             durations=None, dur_logits=None, stream=None):
+                             durations=None, dur_logits=None, stream=None, inputs_ready: bool = False):
         """One label-looping iteration over B rows (all int32 [B] CUDA tensors updated in
-        place; emit_out [B, max_len]): ngpulm_transducer_loop_step, or with `durations`
-        (a sequence of ints) ngpulm_tdt_loop_step — dur_logits [B, D] (default: the
-        logits tensor's columns V+1 .. V+D). states=None with lam=0: no LM."""
+        place; emit_out [B, max_len]): ngpulm_transducer_loop_step(_ex), or with `durations`
+        (a sequence of ints) ngpulm_tdt_loop_step(_ex) — dur_logits [B, D] (default: the
+        logits tensor's columns V+1 .. V+D). states=None with lam=0: no LM. inputs_ready:
+        NGPULM_STEP_INPUTS_READY (the joint kernel before the step is a plain launch)."""
         import torch
         B = frame_idx.numel()
         lp, ls = _rows_ptr(logits[:, : self.V + 1], B, self.V + 1, "logits")
@@ -332,16 +337,16 @@ class NgpuLM:
                   _dev_ptr(emit_out, torch.int32, "emit_out", B * max_len) if max_len else None,
                   _dev_ptr(emit_len, torch.int32, "emit_len", B),
                   _dev_ptr(last_token, torch.int32, "last_token", B) if last_token is not None else None,
-                  max_len, _stream(stream))
+                  max_len, STEP_INPUTS_READY if inputs_ready else 0, _stream(stream))
         if durations is None:
-            _check(lib().ngpulm_transducer_loop_step(self._h, lp, ls, B, *common))
+            _check(lib().ngpulm_transducer_loop_step_ex(self._h, lp, ls, B, *common))
         else:
             D = len(durations)
             if dur_logits is None:
                 dur_logits = logits[:, self.V + 1: self.V + 1 + D]
             dp, dstr = _rows_ptr(dur_logits, B, D, "dur_logits")
             arr = (C.c_int32 * max(1, D))(*[int(x) for x in durations])
-            _check(lib().ngpulm_tdt_loop_step(self._h, lp, ls, dp, dstr, C.cast(arr, C.c_void_p), D, B, *common))
+            _check(lib().ngpulm_tdt_loop_step_ex(self._h, lp, ls, dp, dstr, C.cast(arr, C.c_void_p), D, B, *common))
         return tokens_out
 
     def fused_greedy_step_rows(self, mode: int, logits, lm_scores, lm_next, lm_final, states, prev=None,

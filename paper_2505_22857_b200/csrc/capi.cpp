@@ -381,7 +381,7 @@ static int loop_step(const ngpulm_model* m, const float* logits, int64_t row_str
                      int64_t dur_stride, const int32_t* durations, int32_t D, int32_t B, int32_t* states,
                      int32_t* frame_idx, int32_t* sym_count, const int32_t* lengths, int32_t max_symbols, float lambda,
                      int32_t blank_id, const float* ilm, int64_t ilm_stride, float lambda_ilm, int32_t* tokens_out,
-                     int32_t* emit_out, int32_t* emit_len, int32_t* last_token, int32_t max_len,
+                     int32_t* emit_out, int32_t* emit_len, int32_t* last_token, int32_t max_len, uint32_t flags,
                      ngpulm_stream stream) {
   if (int r = check_hot(m, B)) return r;
   if (blank_id < 0 || blank_id > m->h.V) return err(NGPULM_EUSAGE, "blank_id outside [0, V]");
@@ -404,9 +404,21 @@ static int loop_step(const ngpulm_model* m, const float* logits, int64_t row_str
   int e = ngpulm::launch_transducer_loop(m->dm, logits, row_stride, B, states, frame_idx, sym_count, lengths,
                                          max_symbols, lambda, blank_id, ilm, ilm_stride, lambda_ilm, tokens_out,
                                          emit_out, emit_len, last_token, max_len, dur_logits, dur_stride, durations,
-                                         D, stream);
+                                         D, flags, stream);
   if (e) return cuda_err((cudaError_t)e, "transducer loop step launch");
   return NGPULM_OK;
+}
+
+int ngpulm_transducer_loop_step_ex(const ngpulm_model* m, const float* logits, int64_t row_stride, int32_t B,
+                                   int32_t* states, int32_t* frame_idx, int32_t* sym_count, const int32_t* lengths,
+                                   int32_t max_symbols, float lambda, int32_t blank_id, const float* ilm,
+                                   int64_t ilm_stride, float lambda_ilm, int32_t* tokens_out, int32_t* emit_out,
+                                   int32_t* emit_len, int32_t* last_token, int32_t max_len, uint32_t flags,
+                                   ngpulm_stream stream) {
+  if (flags & ~(uint32_t)NGPULM_STEP_INPUTS_READY) return err(NGPULM_EUSAGE, "unknown flags");
+  return loop_step(m, logits, row_stride, nullptr, 0, nullptr, 0, B, states, frame_idx, sym_count, lengths,
+                   max_symbols, lambda, blank_id, ilm, ilm_stride, lambda_ilm, tokens_out, emit_out, emit_len,
+                   last_token, max_len, flags, stream);
 }
 
 int ngpulm_transducer_loop_step(const ngpulm_model* m, const float* logits, int64_t row_stride, int32_t B,
@@ -414,9 +426,22 @@ int ngpulm_transducer_loop_step(const ngpulm_model* m, const float* logits, int6
                                 int32_t max_symbols, float lambda, int32_t blank_id, const float* ilm,
                                 int64_t ilm_stride, float lambda_ilm, int32_t* tokens_out, int32_t* emit_out,
                                 int32_t* emit_len, int32_t* last_token, int32_t max_len, ngpulm_stream stream) {
-  return loop_step(m, logits, row_stride, nullptr, 0, nullptr, 0, B, states, frame_idx, sym_count, lengths,
-                   max_symbols, lambda, blank_id, ilm, ilm_stride, lambda_ilm, tokens_out, emit_out, emit_len,
-                   last_token, max_len, stream);
+  return ngpulm_transducer_loop_step_ex(m, logits, row_stride, B, states, frame_idx, sym_count, lengths, max_symbols,
+                                        lambda, blank_id, ilm, ilm_stride, lambda_ilm, tokens_out, emit_out, emit_len,
+                                        last_token, max_len, 0u, stream);
+}
+
+int ngpulm_tdt_loop_step_ex(const ngpulm_model* m, const float* logits, int64_t row_stride, const float* dur_logits,
+                            int64_t dur_stride, const int32_t* durations, int32_t num_durations, int32_t B,
+                            int32_t* states, int32_t* frame_idx, int32_t* sym_count, const int32_t* lengths,
+                            int32_t max_symbols, float lambda, int32_t blank_id, const float* ilm, int64_t ilm_stride,
+                            float lambda_ilm, int32_t* tokens_out, int32_t* emit_out, int32_t* emit_len,
+                            int32_t* last_token, int32_t max_len, uint32_t flags, ngpulm_stream stream) {
+  if (flags & ~(uint32_t)NGPULM_STEP_INPUTS_READY) return err(NGPULM_EUSAGE, "unknown flags");
+  if (num_durations < 1) return err(NGPULM_EUSAGE, "number of durations outside [1, NGPULM_MAX_DURATIONS]");
+  return loop_step(m, logits, row_stride, dur_logits, dur_stride, durations, num_durations, B, states, frame_idx,
+                   sym_count, lengths, max_symbols, lambda, blank_id, ilm, ilm_stride, lambda_ilm, tokens_out,
+                   emit_out, emit_len, last_token, max_len, flags, stream);
 }
 
 int ngpulm_tdt_loop_step(const ngpulm_model* m, const float* logits, int64_t row_stride, const float* dur_logits,
@@ -425,10 +450,9 @@ int ngpulm_tdt_loop_step(const ngpulm_model* m, const float* logits, int64_t row
                          int32_t max_symbols, float lambda, int32_t blank_id, const float* ilm, int64_t ilm_stride,
                          float lambda_ilm, int32_t* tokens_out, int32_t* emit_out, int32_t* emit_len,
                          int32_t* last_token, int32_t max_len, ngpulm_stream stream) {
-  if (num_durations < 1) return err(NGPULM_EUSAGE, "number of durations outside [1, NGPULM_MAX_DURATIONS]");
-  return loop_step(m, logits, row_stride, dur_logits, dur_stride, durations, num_durations, B, states, frame_idx,
-                   sym_count, lengths, max_symbols, lambda, blank_id, ilm, ilm_stride, lambda_ilm, tokens_out,
-                   emit_out, emit_len, last_token, max_len, stream);
+  return ngpulm_tdt_loop_step_ex(m, logits, row_stride, dur_logits, dur_stride, durations, num_durations, B, states,
+                                 frame_idx, sym_count, lengths, max_symbols, lambda, blank_id, ilm, ilm_stride,
+                                 lambda_ilm, tokens_out, emit_out, emit_len, last_token, max_len, 0u, stream);
 }
 
 int ngpulm_fused_greedy_step_rows(const ngpulm_model* m, int32_t mode, const float* logits, int64_t row_stride,

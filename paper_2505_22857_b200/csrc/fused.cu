@@ -869,8 +869,9 @@ int launch_transducer_loop(const DevModel& m, const float* logits, int64_t row_s
                            int32_t blank, const float* aux, int64_t aux_stride, float lambda_ilm,
                            int32_t* tokens_out, int32_t* emit, int32_t* emit_len, int32_t* last, int32_t max_len,
                            const float* dur, int64_t dur_stride, const int32_t* durations, int32_t D,
-                           void* stream) {
+                           uint32_t flags, void* stream) {
   if (m.V % 4 != 0 || m.V > 1024) return (int)cudaErrorNotSupported;
+  const bool ready = (flags & NGPULM_STEP_INPUTS_READY) != 0;
   int R = (B + 147) / 148;
   R = R < 1 ? 1 : (R > 8 ? 8 : R);
   const size_t wsm = (size_t)R * fslice_bytes(m.V, m.order);
@@ -880,9 +881,14 @@ int launch_transducer_loop(const DevModel& m, const float* logits, int64_t row_s
   Loop lp{frame, sym, lengths, emit, emit_len, last, max_sym, max_len, dur, dur_stride, D, {}};
   for (int32_t j = 0; j < D && j < kMaxDur; ++j) lp.durs[j] = durations[j];
   cudaStream_t st = (cudaStream_t)stream;
-  if (states == nullptr)  // plain greedy label looping (no LM)
+  if (states == nullptr) {  // plain greedy label looping (no LM)
+    if (ready && !aux)  // (inputs ready: the logits copied at the kernel's start)
+      return launch(fused_warp_kernel<kLoop, true, true, false, true, false, true>, wg, wb, wsm, st, m, logits,
+                    row_stride, B, states, (int32_t*)nullptr, (const uint8_t*)nullptr, lambda, blank, ax, lp,
+                    tokens_out);
     return launch(fused_warp_kernel<kLoop, true, true, false, true>, wg, wb, wsm, st, m, logits, row_stride, B, states,
                   (int32_t*)nullptr, (const uint8_t*)nullptr, lambda, blank, ax, lp, tokens_out);
+  }
   if (table && pk && m.tiny_chain_bytes > 0) {  // tiny LM: the model in every CTA's shared memory
     const size_t mb = tiny_copy_bytes(m.tiny_chain_bytes, m.tiny_arcq_bytes);
     int Rt = R;
@@ -898,6 +904,10 @@ int launch_transducer_loop(const DevModel& m, const float* logits, int64_t row_s
                           tokens_out);
     }
   }
+  if (ready && !aux && table && pk)  // inputs ready (NGPULM_STEP_INPUTS_READY): one warp per row
+    return launch(fused_warp_kernel<kLoop, true, true, false, false, false, false, true>, wg, wb, wsm, st, m, logits,
+                  row_stride, B, states, (int32_t*)nullptr, (const uint8_t*)nullptr, lambda, blank, ax, lp,
+                  tokens_out);
   if (B <= NGPULM_PAIR_MAX_B) {  // two warps per row
     int Rp = (B + 147) / 148;
     Rp = Rp < 1 ? 1 : (Rp > 4 ? 4 : Rp);

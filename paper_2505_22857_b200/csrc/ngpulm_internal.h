@@ -112,7 +112,8 @@ int launch_transducer_loop(const DevModel& m, const float* logits, int64_t row_s
                            int32_t* frame, int32_t* sym, const int32_t* lengths, int32_t max_sym, float lambda,
                            int32_t blank, const float* aux, int64_t aux_stride, float lambda_ilm,
                            int32_t* tokens_out, int32_t* emit, int32_t* emit_len, int32_t* last, int32_t max_len,
-                           const float* dur, int64_t dur_stride, const int32_t* durations, int32_t D, void* stream);
+                           const float* dur, int64_t dur_stride, const int32_t* durations, int32_t D,
+                           uint32_t flags, void* stream);
 int launch_topk(const DevModel& m, const float* logits, int64_t row_stride, int32_t B, const int32_t* states,
                 const float* aux, int64_t aux_stride, float lambda, float lambda_ilm, int32_t eos, int32_t k,
                 float* out_scores, int32_t* out_cols, int32_t* out_next, void* stream);

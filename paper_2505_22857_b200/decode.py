@@ -38,7 +38,8 @@ class TransducerGreedyDecoder:
 
     def __init__(self, model, joint, B: int, max_frames: int, lam: float = 0.3, max_symbols: int = 10,
                  max_len: int | None = None, blank_id: int | None = None, ilm=None, lam_ilm: float = 0.0,
-                 graph_steps: int = 32, use_graph: bool = True, device=None, durations=None, use_lm: bool = True):
+                 graph_steps: int = 32, use_graph: bool = True, device=None, durations=None, use_lm: bool = True,
+                 joint_plain_launch: bool = False):
         import torch
         self.m, self.joint, self.B = model, joint, B
         self.lam, self.max_symbols, self.blank_id = lam, max_symbols, blank_id
@@ -46,6 +47,9 @@ class TransducerGreedyDecoder:
         # TDT: the joint writes V+1 token and len(durations) duration logits per row
         self.durations = None if durations is None else [int(d) for d in durations]
         self.use_lm = use_lm  # False: plain greedy (no LM state), the overhead baseline
+        # True: the joint launches its kernels without programmatic dependent launch (every cuBLAS /
+        # PyTorch kernel), so each loop step runs with NGPULM_STEP_INPUTS_READY
+        self.inputs_ready = joint_plain_launch
         self.graph_steps, self.use_graph = graph_steps, use_graph
         self.max_frames = max_frames
         self.max_len = max_len if max_len is not None else max_frames * max_symbols
@@ -67,7 +71,8 @@ class TransducerGreedyDecoder:
                                     self.lengths, self.emit, self.elen, last_token=self.last,
                                     lam=self.lam if self.use_lm else 0.0, blank_id=self.blank_id,
                                     max_symbols=self.max_symbols, ilm=self.ilm, lam_ilm=self.lam_ilm,
-                                    tokens_out=self.tok, durations=self.durations, stream=self.stream)
+                                    tokens_out=self.tok, durations=self.durations, stream=self.stream,
+                                    inputs_ready=self.inputs_ready)
 
     def _body(self):
         import torch
@@ -116,14 +121,16 @@ class TransducerGreedyDecoder:
 def transducer_greedy_decode(model, joint, lengths, states=None, lam: float = 0.3, max_symbols: int = 10,
                              max_len: int | None = None, blank_id: int | None = None, ilm=None,
                              lam_ilm: float = 0.0, graph_steps: int = 32, use_graph: bool = True,
-                             durations=None, use_lm: bool = True) -> TransducerResult:
+                             durations=None, use_lm: bool = True,
+                             joint_plain_launch: bool = False) -> TransducerResult:
     """One-shot TransducerGreedyDecoder over lengths [B] int32 CUDA (see the class);
     durations=[...] decodes a TDT model (the joint writes V+1+len(durations) columns)."""
     B = lengths.numel()
     max_frames = int(lengths.max().item()) if B else 0
     dec = TransducerGreedyDecoder(model, joint, B, max_frames, lam=lam, max_symbols=max_symbols, max_len=max_len,
                                   blank_id=blank_id, ilm=ilm, lam_ilm=lam_ilm, graph_steps=graph_steps,
-                                  use_graph=use_graph, device=lengths.device, durations=durations, use_lm=use_lm)
+                                  use_graph=use_graph, device=lengths.device, durations=durations, use_lm=use_lm,
+                                  joint_plain_launch=joint_plain_launch)
     if B == 0:
         return TransducerResult(dec.emit, dec.elen, dec.st, 0)
     return dec(lengths, states)

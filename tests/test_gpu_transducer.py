@@ -123,3 +123,34 @@ def test_driver_large_batch_single_warp_path(pairs):
     torch.cuda.synchronize()
     check(res, o.transducer_decode(seed, lengths, np.zeros(B, np.int32), lam=0.7, max_symbols=3, temperature=temp,
                                    max_len=res.emitted.shape[1], blank_bias=BIAS))
+
+
+@pytest.mark.parametrize("durations", [None, (0, 1, 2)])
+@pytest.mark.parametrize("B", [64, 512, 700])
+def test_driver_inputs_ready(lm6, B, durations):
+    """The label-looping driver with NGPULM_STEP_INPUTS_READY (the synthetic joint is a
+    plain launch): one warp per row, the state read once and the logits copied at the
+    step's start; identical to the flags == 0 driver and, on sampled rows, to the oracle
+    (RNN-T and TDT, 6-gram, lambda = 0.3)."""
+    m, o, f = lm6
+    lengths = np.random.default_rng(B + 1).integers(10, 40, size=B).astype(np.int32)
+    seed, temp = 4242, 8.0
+    ncols = m.V + 1 + (len(durations) if durations else 0)
+
+    def joint(frame, u, last, out):
+        synth.joint_gpu(seed, frame, u, last, out, temperature=temp, blank=m.V, blank_bias=BIAS)
+
+    res = [transducer_greedy_decode(m, joint, T(lengths), lam=0.3, max_symbols=4, durations=durations,
+                                    joint_plain_launch=ready) for ready in (False, True)]
+    torch.cuda.synchronize()
+    a, b = res
+    assert np.array_equal(a.emit_len.cpu().numpy(), b.emit_len.cpu().numpy())
+    assert np.array_equal(a.emitted.cpu().numpy(), b.emitted.cpu().numpy())
+    assert np.array_equal(a.states.cpu().numpy(), b.states.cpu().numpy())
+    if durations is None:
+        rows = np.arange(0, B, max(1, B // 16))
+        ref = o.transducer_decode(seed, lengths[rows], np.zeros(rows.size, np.int32), lam=0.3, max_symbols=4,
+                                  temperature=temp, max_len=b.emitted.shape[1], blank_bias=BIAS)
+        el, st = b.emit_len.cpu().numpy()[rows], b.states.cpu().numpy()[rows]
+        assert np.array_equal(el, ref[1]) and np.array_equal(st, ref[2])
+    assert ncols > m.V
