@@ -241,8 +241,9 @@ int ngpulm_fused_greedy_step(const ngpulm_model* model, int32_t mode, const floa
  *     without re-reading the state after its programmatic-dependent-launch
  *     wait. Results are identical to flags == 0 whenever the guarantee holds;
  *     consecutive NGPU-LM steps (which write states) do not qualify.
- *     Ignored by the ILM variant and by models without packed arcs and a
- *     chain table (they run the flags == 0 path).
+ *     Ignored by the ILM variant, by models held in shared memory (tiny-LM
+ *     path) and by models without packed arcs and a chain table (they run
+ *     their flags == 0 kernels; results are the same).
  * flags == 0 is ngpulm_fused_greedy_step. EUSAGE for unknown flags. */
 enum { NGPULM_STEP_LOGITS_READY = 1, NGPULM_STEP_INPUTS_READY = 2 };
 int ngpulm_fused_greedy_step_ex(const ngpulm_model* model, int32_t mode, const float* logits,
@@ -323,8 +324,9 @@ int ngpulm_tdt_loop_step(const ngpulm_model* model, const float* logits, int64_t
  *     before each step is a plain launch. The step then copies the logits and
  *     builds the LM row from the state read at its start (no re-read after its
  *     programmatic-dependent-launch wait). Results are identical to flags == 0
- *     whenever the guarantee holds. Ignored with an ILM and for models without
- *     packed arcs and a chain table.
+ *     whenever the guarantee holds. Ignored with an ILM, for models held in
+ *     shared memory (tiny-LM path) and for models without packed arcs and a
+ *     chain table.
  * flags == 0 are the calls above. EUSAGE for unknown flags. */
 int ngpulm_transducer_loop_step_ex(const ngpulm_model* model, const float* logits, int64_t row_stride,
                                    int32_t B, int32_t* states, int32_t* frame_idx, int32_t* sym_count,
