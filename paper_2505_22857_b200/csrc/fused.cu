@@ -904,7 +904,11 @@ int launch_transducer_loop(const DevModel& m, const float* logits, int64_t row_s
                           tokens_out);
     }
   }
-  if (ready && !aux && table && pk)  // inputs ready (NGPULM_STEP_INPUTS_READY): one warp per row
+  // inputs ready (NGPULM_STEP_INPUTS_READY) beyond the warp-pair range: one warp per row without the state
+  // re-read. Up to 4 rows per SM the pair kernel stays: it reads its inputs after the wait only (no
+  // speculation to re-check), and in the label loop (B = 512, mostly-blank rows) its stage 1 beside the
+  // row build measured faster than one warp per row with the flag (1.53 vs 1.55 ms)
+  if (ready && !aux && table && pk && B > NGPULM_PAIR_MAX_B)
     return launch(fused_warp_kernel<kLoop, true, true, false, false, false, false, true>, wg, wb, wsm, st, m, logits,
                   row_stride, B, states, (int32_t*)nullptr, (const uint8_t*)nullptr, lambda, blank, ax, lp,
                   tokens_out);
