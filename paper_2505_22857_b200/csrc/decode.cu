@@ -705,12 +705,14 @@ __global__ void __launch_bounds__(32 * (2 + kSumWarps), 2)
 // once (pass 1): segment 0 from the row's true start; segment k >= 1 from the
 // root state and no prev, kSegWarm frames before its first frame (an n-gram
 // state is the suffix of the last N-1 emitted tokens, so the warm-up usually
-// reaches the true trajectory before the segment starts). Pass 2 walks the
-// segments of a row in order from the TRUE state at each boundary (the
-// previous segment's last record) and re-decides frames until its decision
-// and state equal pass 1's at the same frame — decisions depend only on
-// (state, prev) and the frame, so from there on pass 1's records are the true
-// ones; a segment that never meets is re-decided to its end. The same warp then turns the
+// reaches the true trajectory before the segment starts). Pass 2 (one CTA per
+// row) re-decides every boundary at once, one warp each, from the state
+// recorded before it (the previous segment's last record) until its decision
+// and state equal the records at the same frame — decisions depend only on
+// (state, prev) and the frame, so from there on the records are one run of the
+// decision process; a segment that never meets is re-decided to its end. A
+// boundary whose recorded start its predecessor's fix-up rewrote is re-done in
+// order by warp 0 (each warp keeps the start it used), which then turns the
 // per-frame decisions into the emission list, the final state and prev.
 // Every output is therefore exactly ctc_decode_kernel's (tested bit-exact).
 // Records: frames_out holds the decisions, emit_out (row stride T) the state
@@ -748,7 +750,7 @@ constexpr int kSegRows = NGPULM_SEG_ROWS;  // chains (warps) per CTA, sharing th
 constexpr int kSegCtas = NGPULM_SEG_CTAS;
 
 // A chain's row: arc-level entries only, tagged with the rebuild that wrote them
-// ({acc_boff + weight, generation} per token, next states apart); a token without
+// ({acc_boff + weight, generation << 24 | next state} per token); a token without
 // an entry of the current generation takes the root level (acc_root + root
 // weight from the lane's registers, root target from the CTA's copy), so a
 // rebuild writes only the arcs, not the V root entries.
