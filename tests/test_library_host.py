@@ -138,6 +138,24 @@ def test_hot_calls_refuse_host_only_model(fig1):
     assert r == ng.NGPULM_EUSAGE
 
 
+def test_step_flags_validated(fig1):
+    """Unknown flag bits are refused (EUSAGE) by every *_ex step call, before any device work."""
+    import ctypes as C
+    L = ng.lib()
+    p = C.c_void_p(16)
+    for bad in (4, 8, 1 << 31):
+        r = L.ngpulm_fused_greedy_step_ex(fig1._h, 0, p, 7, 1, p, p, None, 0.5, 6, p, bad, None)
+        assert r == ng.NGPULM_EUSAGE
+        r = L.ngpulm_transducer_loop_step_ex(fig1._h, p, 7, 1, p, p, p, p, 3, 0.5, 6, None, 0, 0.0, p, p, p, p, 8,
+                                             bad, None)
+        assert r == ng.NGPULM_EUSAGE
+        d = (C.c_int32 * 1)(1)
+        r = L.ngpulm_tdt_loop_step_ex(fig1._h, p, 7, p, 1, C.cast(d, C.c_void_p), 1, 1, p, p, p, p, 3, 0.5, 6, None,
+                                      0, 0.0, p, p, p, p, 8, bad, None)
+        assert r == ng.NGPULM_EUSAGE
+    assert ng.STEP_LOGITS_READY == 1 and ng.STEP_INPUTS_READY == 2
+
+
 def test_touched_bytes(fig1):
     # states 7 (the cat) -> 2 (cat) -> root: 2 state records + 1 + 1 arcs + root arcs + finals
     b = fig1.touched_bytes(np.array([7, 7], dtype=np.int32))
