@@ -1100,7 +1100,8 @@ __global__ void __maxnreg__(kSegMaxReg)
   };
   auto next_state = [&](int32_t tk) {  // the state after token tk from the row's state
     const uint32_t e = __float_as_uint(row_g[tk].y);
-    return (e >> 24) == (uint32_t)gen ? (int32_t)(e & 0xffffffu) : root_to[tk];
+    const int32_t rt = root_to[tk];  // (both shared loads in flight at once)
+    return (e >> 24) == (uint32_t)gen ? (int32_t)(e & 0xffffffu) : rt;
   };
   // the fused CTC decision of one frame (ctc_decode_kernel's, R13, R14, R17, R19); the frame's
   // slot is handed back (and refilled) as soon as its columns are in registers
