@@ -72,7 +72,8 @@ def test_decode_blank_column_inside(pairs, blank):
 def test_decode_equals_per_frame_steps_config2(lm6):
     """BASELINE configs[2]: B=256, T=500, V=1024+blank, 6-gram, lambda=0.3 — one
     persistent launch == 500 launches of the fused step (all rows, bit-exact), and
-    == the oracle on sampled rows (ragged lengths)."""
+    == the oracle on every row (ragged lengths), and the bench's launch (every row
+    at full length, no lengths array) == the oracle on every row."""
     m, o, f = lm6
     B, T = 256, 500
     sents = synth.read_sentences(f.heldout)
@@ -94,9 +95,9 @@ def test_decode_equals_per_frame_steps_config2(lm6):
     torch.cuda.synchronize()
     assert np.array_equal(g[0], frames.cpu().numpy().T)
     assert np.array_equal(g[3], st.cpu().numpy()) and np.array_equal(g[4], pv.cpu().numpy())
-    rows = np.arange(0, B, 32)
-    o_res = o.ctc_decode(x[rows], start[rows], prev=prev0[rows], lam=0.3, lengths=lengths[rows])
-    assert_same(tuple(a[rows] for a in g), o_res)
+    assert_same(g, o.ctc_decode(x, start, prev=prev0, lam=0.3, lengths=lengths))
+    gb = gpu_decode(m, x, start, prev0, 0.3, None, view=xd)  # the bench's call
+    assert_same(gb, o.ctc_decode(x, start, prev=prev0, lam=0.3))
     # the LM changed decisions relative to lambda = 0 (the test means something)
     g0 = gpu_decode(m, x, start, prev0, 0.0, lengths, view=xd)
     assert (g0[0] != g[0]).any()
